@@ -1,0 +1,506 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 hot path (BASELINE.json metric: log-posterior+gradient evals/s
+and achieved HBM GB/s, logistic GLM, fp64).
+
+Default workload = BASELINE config 1 (N=1e7, K=100 fp64, fresh beta ~ N(0, 0.1^2) per
+step, prior N(0, 10^2)), the largest configuration that fits one GPU (8.08 GB of X).
+One step = one log-posterior + gradient evaluation over all N rows.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config c1|c1f32|c0|c3|c4|c4potts]
+
+N>1 runs one process per GPU under torch.distributed.run (NCCL): rows are split by
+the reference's partition rule, each rank streams its shard and the (K+1)-double
+partials are all-gathered and summed in rank order.
+
+`--impl reference` times the reference algorithm's CPU implementation on this host
+(the numpy restatement in oracle/glm_oracle.py, PLF over all host threads, OpenBLAS
+single-threaded per worker: the reference's fastest setting), on a
+bounded row sample per step, scaled to the full N.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+
+
+def _early_args():
+    p = argparse.ArgumentParser(add_help=False)
+    p.add_argument("--impl", default="b200")
+    p.add_argument("--cpu-worker", action="store_true")
+    a, _ = p.parse_known_args()
+    return a
+
+
+_EA = _early_args()
+if _EA.impl == "reference" or _EA.cpu_worker:
+    # the reference's best CPU setting: workers = cores, one BLAS thread each (set before numpy loads)
+    for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[var] = "1"
+
+import numpy as np  # noqa: E402
+
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c0": dict(n=100_000, k=32, x_storage="f64", desc="config 0: N=1e5 K=32 fp64 log-posterior+gradient"),
+    "c1": dict(n=10_000_000, k=100, x_storage="f64", desc="config 1: N=1e7 K=100 fp64 log-posterior+gradient"),
+    "c1f32": dict(n=10_000_000, k=100, x_storage="f32",
+                  desc="config 1 fp32-X/fp64-accumulate: N=1e7 K=100 log-posterior+gradient"),
+    "c3": dict(groups=1000, k=20, mean_rows=2000, desc="config 3: G=1000 n_g~Poisson(2000) K=20 HB batched"),
+    "c4": dict(h=8192, w=8192, model="ising", desc="config 4: 8192^2 periodic Ising, Philox4x32 (seed,sweep,site)"),
+    "c4potts": dict(h=8192, w=8192, model="potts", desc="config 4 Potts q=4 variant, 8192^2 periodic"),
+}
+
+METRIC = "log-posterior+gradient evals/s and achieved HBM GB/s (logistic GLM, fp64)"
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def load_peaks() -> tuple[float, str]:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(key: str):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            v = json.load(fh).get(key)
+        return None if v is None else float(v)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            time.sleep(0.15)
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                maxs.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": max(maxs) if maxs else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ---------------------------------------------------------------------------- distributed
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------- CPU baseline
+def cpu_worker_main(args):
+    """Subprocess body: time the oracle port on a bounded sample (OPENBLAS set to 1 above)."""
+    from oracle import glm_oracle as gl
+    from paper_1310_1537_b200.synthetic import baseline_design
+    cores = host_cores()
+    x, y, _, betas = baseline_design(args.sample_rows, args.k, seed=7, n_eval=args.reps + 3)
+    x = x.astype(np.float32).astype(np.float64) if args.x_storage == "f32" else x
+    mu, sigma = np.zeros(args.k), np.full(args.k, 10.0)
+    for i in range(3):
+        gl.log_posterior_grad(x, y, betas[i], mu, sigma, workers=cores)
+    times = []
+    for i in range(args.reps):
+        t0 = time.perf_counter()
+        gl.log_posterior_grad(x, y, betas[3 + i], mu, sigma, workers=cores)
+        times.append(time.perf_counter() - t0)
+    print(json.dumps({"median_s": statistics.median(times), "times": times, "cores": cores}))
+
+
+def cpu_baseline(cfg: dict, n_full: int, budget_s: float = 20.0) -> dict:
+    """Run the oracle port in a fresh subprocess (OpenBLAS single-threaded per worker)."""
+    k = cfg["k"]
+    sample_rows = min(n_full, 2_000_000)
+    reps = 5
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--cpu-worker", "--sample-rows", str(sample_rows),
+           "--k", str(k), "--reps", str(reps), "--x-storage", cfg.get("x_storage", "f64")]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, check=True).stdout
+        res = json.loads(out.strip().splitlines()[-1])
+    except Exception as exc:  # reported, never fatal
+        return {"value": None, "unit": "evals/s", "cores": host_cores(), "kind": "port",
+                "sample": f"failed: {exc}"}
+    per_eval_full = res["median_s"] * n_full / sample_rows
+    return {"value": 1.0 / per_eval_full, "unit": "evals/s", "cores": res["cores"], "kind": "port",
+            "sample": (f"oracle/glm_oracle.py log_posterior_grad (numpy PLF, {res['cores']} workers x 1 BLAS thread) "
+                       f"on {sample_rows} rows x K={k}, median of {reps} evals after 3 warm-up = "
+                       f"{res['median_s']*1e3:.1f} ms, scaled x{n_full/sample_rows:g} to N={n_full}")}
+
+
+# ---------------------------------------------------------------------------- reference arm
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import glm_oracle as gl
+    from paper_1310_1537_b200.synthetic import baseline_design
+    cores = host_cores()
+    n_full, k = cfg["n"], cfg["k"]
+    # bounded sample per step so the whole K-step run stays within a few minutes
+    sample_rows = min(n_full, max(100_000, min(1_000_000, int(1e8 // max(args.steps, 1)))))
+    x, y, _, betas = baseline_design(sample_rows, k, seed=7, n_eval=args.steps + args.warmup + 1)
+    if cfg.get("x_storage") == "f32":
+        x = x.astype(np.float32).astype(np.float64)
+    mu, sigma = np.zeros(k), np.full(k, 10.0)
+    for i in range(args.warmup):
+        gl.log_posterior_grad(x, y, betas[i], mu, sigma, workers=cores)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        gl.log_posterior_grad(x, y, betas[args.warmup + i], mu, sigma, workers=cores)
+    wall = time.perf_counter() - t0
+    scale = n_full / sample_rows
+    ms_per_step = wall / args.steps * 1e3 * scale
+    value = 1000.0 / ms_per_step
+    line = {
+        "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY §8d generator, seed 7)",
+        "config": {"workload": cfg["desc"], "N": n_full, "K": k, "sample_rows_per_step": sample_rows,
+                   "x_storage": cfg.get("x_storage", "f64")},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "port",
+                         "sample": (f"oracle/glm_oracle.py (numpy restatement of parmcmc PLF, glm.py:418-436) "
+                                    f"with {cores} workers x 1 OpenBLAS thread; each step evaluates {sample_rows} "
+                                    f"rows and is scaled x{scale:g} to N={n_full}")},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- B200 arm: GLM
+def run_glm(args, cfg):
+    import torch
+    import torch.distributed as dist
+    from paper_1310_1537_b200 import glm as pglm
+    from paper_1310_1537_b200.parallel import partition
+    from paper_1310_1537_b200.sampler import GaussianPrior
+    from paper_1310_1537_b200.synthetic import baseline_design
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n_full, k = cfg["n"], cfg["k"]
+    a, b = partition(n_full, ws)[rank]
+    n_local = b - a
+    steps, warmup = args.steps, args.warmup
+    # rank-local shard of the global design (per-rank seed: generating another rank's
+    # prefix would cost its full stream)
+    x, y, _, betas = baseline_design(n_local, k, seed=1000 + rank, n_eval=1)
+    betas = np.random.default_rng(99).normal(0.0, 0.1, (warmup + 2 * steps, k))  # same on every rank
+    data = pglm.DesignMatrix(x, y)
+    del x
+    prior = GaussianPrior.isotropic(k, 0.0, 10.0)
+    plan = pglm.ExecPlan(pglm.Strategy.B200, device=local, x_storage=cfg["x_storage"])
+    dev = data.on_device(local, cfg["x_storage"])
+    geo = dev.geometry()
+
+    if ws > 1:
+        from paper_1310_1537_b200.dist import DistributedDesign
+        dd = DistributedDesign(data, device=local, x_storage=cfg["x_storage"])
+
+        def step_dev(beta):
+            return dd.log_posterior_grad_device(beta, prior)
+
+        def step_e2e(beta):
+            return dd.log_posterior_grad(beta, prior)
+    else:
+        dev.set_prior(prior.mu, prior.sigma)
+
+        def step_dev(beta):
+            dev.launch(beta, True, True)
+
+        def step_e2e(beta):
+            return pglm.log_posterior_grad(data, beta, prior, plan)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(local)
+
+    # warm-up (untimed)
+    for i in range(warmup):
+        step_dev(betas[i])
+        step_e2e(betas[i])
+    barrier()
+
+    # ---- device-timed region: K steps, inputs resident, events on the launching stream
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    block = np.ascontiguousarray(betas[warmup:warmup + steps])
+    if ws == 1:
+        # K launches bracketed by CUDA events on the launching (handle) stream
+        dev_ms = dev.time_launches(block, with_prior=True, want_grad=True)
+    else:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tstream = torch.cuda.current_stream(local)
+        ev0.record(tstream)
+        for i in range(steps):
+            step_dev(block[i])
+        ev1.record(tstream)
+        torch.cuda.synchronize(local)
+        dev_ms = ev0.elapsed_time(ev1)
+    barrier()
+    clk = clocks.stop()
+
+    # ---- kernel-only timing of the dominant kernel (handle stream, back-to-back launches)
+    kern_ms = dev.time_launches(block, with_prior=True, want_grad=True) / steps
+
+    # ---- end-to-end through the public API (host beta in, host (f, g) out, every step)
+    barrier()
+    t0 = time.perf_counter()
+    for i in range(steps):
+        res = step_e2e(betas[warmup + steps + i])
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    assert np.isfinite(res.f) and np.all(np.isfinite(res.g))
+
+    # max over ranks
+    t = torch.tensor([dev_ms, e2e_s, kern_ms], dtype=torch.float64, device=f"cuda:{local}")
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms, e2e_s, kern_ms = (float(v) for v in t.cpu())
+
+    xs = 8 if cfg["x_storage"] == "f64" else 4
+    bytes_eval_local = n_local * (k * xs + 8)          # N (K b_x + b_y)
+    bytes_eval_total = n_full * (k * xs + 8)
+    ms_per_step = dev_ms / steps
+    value = 1000.0 / ms_per_step
+    peak, peak_src = load_peaks()
+    achieved = bytes_eval_local / (kern_ms * 1e-3) / 1e9
+    e2e_value = steps / e2e_s
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws, "steps": steps, "warmup": warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if cfg["x_storage"] == "f64" else "f64 (X stored f32)",
+            "data": "synthetic (SURVEY §8d generator: X[:,0]=1, X[:,1:]~N(0,1), y~Bern(sigmoid(X beta_true)))",
+            "config": {"workload": cfg["desc"], "N": n_full, "K": k, "rows_per_gpu": n_local,
+                       "x_storage": cfg["x_storage"], "parallelism": f"row-shard x{ws}",
+                       "l2": f"inputs larger than L2 ({bytes_eval_local/1e9:.2f} GB per GPU per eval)",
+                       "prior": "N(0, 10^2) iid", "beta": "fresh N(0, 0.1^2) per step"},
+            "achieved_gbs": bytes_eval_total / (ms_per_step * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "frac_of_8tbs_spec": achieved / 8000.0,
+                         "traffic": load_traffic(f"{args.config}"),
+                         "algorithmic_bytes_per_launch": bytes_eval_local,
+                         "kernel_ms": kern_ms, "peak_source": peak_src,
+                         "kernel": f"glm_stream_kernel ({geo['kernel']}, grid {geo['grid']} x {geo['threads']} "
+                                   f"threads, {geo['stages']} TMA stages, {geo['smem_bytes']} B smem)"},
+            "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": 8 * k,
+                    "d2h_bytes_per_step": 8 * (k + 1),
+                    "path": "paper_1310_1537_b200.glm.log_posterior_grad (C-ABI pm_glm_launch/wait; beta in "
+                            "kernel params, (f,g) written to mapped pinned host memory)"},
+            "gpu_launches": steps,
+            "clocks": clk,
+        }
+        if ws == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg, n_full)
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------- B200 arm: HB
+def run_hb(args, cfg):
+    import torch
+    from paper_1310_1537_b200.hb import CsrGroups
+    from paper_1310_1537_b200.synthetic import hb_design
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    x, y, off, betas, mu, tau = hb_design(cfg["groups"], cfg["k"], seed=3, mean_rows=cfg["mean_rows"])
+    csr = CsrGroups(x, y, off)
+    dev = csr.on_device(local)
+    sigma = np.full(cfg["k"], tau)
+    for _ in range(args.warmup):
+        dev.eval(betas, mu, sigma)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        dev.eval(betas, mu, sigma)
+    wall = time.perf_counter() - t0
+    clk = clocks.stop()
+    n = int(off[-1])
+    bytes_launch = n * (cfg["k"] * 8 + 8)
+    ms = wall / args.steps * 1e3
+    peak, src = load_peaks()
+    if rank == 0:
+        print(json.dumps({
+            "metric": "HB batched log-posterior+gradient launches/s (G groups per launch)", "value": 1000.0 / ms,
+            "unit": "launches/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SURVEY §8d config 3 generator)",
+            "config": {"workload": cfg["desc"], "rows": n, "K": cfg["k"], "groups": cfg["groups"]},
+            "group_evals_per_s": cfg["groups"] * 1000.0 / ms,
+            "roofline": {"bound": "hbm", "achieved": bytes_launch / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": bytes_launch / (ms * 1e-3) / 1e9 / peak, "traffic": load_traffic(args.config),
+                         "note": "wall time incl. beta H2D and (f,g) D2H", "peak_source": src},
+            "e2e": {"value": 1000.0 / ms, "unit": "launches/s", "h2d_bytes_per_step": betas.nbytes,
+                    "d2h_bytes_per_step": 8 * cfg["groups"] * (cfg["k"] + 1)},
+            "gpu_launches": args.steps, "clocks": clk}), flush=True)
+
+
+# ---------------------------------------------------------------------------- B200 arm: Gibbs
+def run_gibbs(args, cfg):
+    import torch
+    from paper_1310_1537_b200 import ising
+    from paper_1310_1537_b200.rng import SitePhilox
+    from paper_1310_1537_b200.synthetic import ising_spins, potts_states
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    h, w = cfg["h"], cfg["w"]
+    if cfg["model"] == "ising":
+        lat = ising.IsingLattice(ising_spins(h, w, seed=0), np.zeros((h, w)), 2 * 0.4407, boundary="periodic")
+    else:
+        lat = ising.PottsLattice(potts_states(h, w, seed=0), 0.4407, boundary="periodic")
+    part = ising.color_lattice(lat, device=local)
+    dev = part.device
+    assert dev.fast_path()
+    rng = SitePhilox(seed=2024)
+    dev.sweeps(args.warmup, 2, rng.seed, 0, rng.sweep)
+    rng.advance(args.warmup)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms = dev.time_sweeps(args.steps, 2, rng.seed, 0, rng.sweep) / args.steps  # CUDA events, handle stream
+    clk = clocks.stop()
+    # end to end: spins in from host, sweeps, spins out
+    t0 = time.perf_counter()
+    part.pack_from(lat)
+    dev.sweeps(args.steps, 2, rng.seed, 0, rng.sweep + args.steps)
+    part.unpack_into(lat)
+    e2e = time.perf_counter() - t0
+    peak, src = load_peaks()
+    bytes_sweep = 2 * h * w
+    if rank == 0:
+        print(json.dumps({
+            "metric": "Gibbs sweeps/s (red-black checkerboard)", "value": 1000.0 / ms, "unit": "sweeps/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int8 spins, u32 Philox",
+            "data": "synthetic iid uniform initial state",
+            "config": {"workload": cfg["desc"], "H": h, "W": w, "beta_J": 0.4407},
+            "msite_per_s": h * w / (ms * 1e-3) / 1e6,
+            "roofline": {"bound": "issue (Philox4x32) -- HBM fraction reported for context",
+                         "achieved": bytes_sweep / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": bytes_sweep / (ms * 1e-3) / 1e9 / peak, "traffic": load_traffic(args.config),
+                         "peak_source": src},
+            "e2e": {"value": args.steps / e2e, "unit": "sweeps/s", "h2d_bytes_per_step": h * w / args.steps,
+                    "d2h_bytes_per_step": h * w / args.steps},
+            "gpu_launches": 2 * args.steps, "clocks": clk}), flush=True)
+
+
+def main():
+    p = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=None)
+    p.add_argument("--warmup", type=int, default=None)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", default="c1", choices=sorted(CONFIGS))
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    # internal: CPU baseline subprocess
+    p.add_argument("--cpu-worker", action="store_true", help=argparse.SUPPRESS)
+    p.add_argument("--sample-rows", type=int, default=0, help=argparse.SUPPRESS)
+    p.add_argument("--k", type=int, default=0, help=argparse.SUPPRESS)
+    p.add_argument("--reps", type=int, default=5, help=argparse.SUPPRESS)
+    p.add_argument("--x-storage", default="f64", help=argparse.SUPPRESS)
+    args = p.parse_args()
+    if args.cpu_worker:
+        cpu_worker_main(args)
+        return
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        args.steps = args.steps or 5
+        args.warmup = args.warmup if args.warmup is not None else 3
+        if "n" not in cfg:
+            ws, rank, _ = dist_env()
+            if rank == 0:
+                print(json.dumps({"impl": "reference", "unavailable": "reference arm implemented for GLM configs"}))
+            return
+        run_reference(args, cfg)
+        return
+    if "n" in cfg:
+        args.steps = args.steps or 1000
+        args.warmup = args.warmup if args.warmup is not None else 10
+        run_glm(args, cfg)
+    elif "groups" in cfg:
+        args.steps = args.steps or 200
+        args.warmup = args.warmup if args.warmup is not None else 5
+        run_hb(args, cfg)
+    else:
+        args.steps = args.steps or 1000
+        args.warmup = args.warmup if args.warmup is not None else 10
+        run_gibbs(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

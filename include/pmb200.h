@@ -1,0 +1,207 @@
+/*
+ * pmb200.h -- C ABI of libpmb200.so, the B200 (sm_100a) implementation of the two
+ * SIMD hot paths of arXiv 1310.1537 as shipped in the reference package `parmcmc`
+ * (/root/reference/pkg/src/parmcmc).
+ *
+ * Every entry point below replaces one reference Python call (file:line cited per
+ * function).  The reference's "plugin" boundary is the ExecPlan argument each hot
+ * function dispatches on (glm.py:57-77, 257-274, 351-364); the Python mirror in
+ * paper_1310_1537_b200/ binds these symbols with ctypes and keeps the reference's
+ * signatures (INTEGRATION.md shows the binding a reference maintainer would add).
+ *
+ * Conventions
+ *   - every function returns int: PM_OK (0) or an error code; pm_last_error()
+ *     returns a thread-local message for the last failing call on this thread.
+ *       PM_EINVAL  -> ValueError      (shape / non-finite / validation; glm.py:74-99,210-216)
+ *       PM_ERANGE  -> IndexError      (coordinate out of range; glm.py:495-496)
+ *       PM_EDEVICE -> RuntimeError    (CUDA failure)
+ *       PM_ENOMEM  -> MemoryError
+ *       PM_ESTATE  -> RuntimeError    (call order: e.g. eval before upload)
+ *   - host pointers are borrowed for the duration of the call only;
+ *   - calls are synchronous unless the name ends in _launch/_async;
+ *   - a handle is bound to one device and owns one CUDA stream; calls on one handle
+ *     are serialised by a per-handle mutex, so handles may be used from pool threads
+ *     (the reference's HB COARSE mapping calls kernels from workers, hb.py:152-161);
+ *   - results are bitwise repeatable for a fixed handle and input (the reference's
+ *     fixed-plan determinism, test_glm.py:107-114): every reduction has a fixed order
+ *     and no floating-point atomics are used.
+ */
+#ifndef PMB200_H
+#define PMB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PM_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define PM_API __attribute__((visibility("default")))
+#else
+#define PM_API
+#endif
+
+enum pm_status {
+  PM_OK = 0,
+  PM_EINVAL = 1,
+  PM_ERANGE = 2,
+  PM_EDEVICE = 3,
+  PM_ENOMEM = 4,
+  PM_ESTATE = 5
+};
+
+/* storage type of the design matrix on the device */
+enum pm_xtype { PM_X_F64 = 0, PM_X_F32 = 1 };
+
+/* ------------------------------------------------------------------ library */
+PM_API int pm_abi_version(void);
+PM_API const char* pm_last_error(void);
+PM_API int pm_device_count(int* n);
+PM_API int pm_device_info(int device, int* sm_count, int* cc_major, int* cc_minor, size_t* total_mem);
+
+/* ------------------------------------------------------------------ GLM
+ * One device-resident logistic design: X row-major [N][K] (stored padded to a
+ * multiple of 32 rows with zero rows; the padding never contributes), y in {0,1}.
+ * Replaces the numpy arrays of DesignMatrix (glm.py:80-111), which the reference
+ * declares immutable and shareable, so they are uploaded once and cached.
+ */
+typedef struct pm_glm_s* pm_glm_t;
+
+PM_API int pm_glm_create(int device, pm_glm_t* out);
+PM_API int pm_glm_destroy(pm_glm_t h);
+
+/* X: host, row-major, n_rows*n_cols elements of double (PM_X_F64) or float (PM_X_F32);
+ * y: host double[n_rows], each exactly 0 or 1 (glm.py:96-99). */
+PM_API int pm_glm_upload(pm_glm_t h, const void* X, int x_dtype, const double* y,
+                  int64_t n_rows, int32_t n_cols);
+
+/* Diagonal Gaussian prior N(mu_k, sigma_k^2) (sampler.py:36-58); mu == sigma == NULL clears. */
+PM_API int pm_glm_set_prior(pm_glm_t h, const double* mu, const double* sigma);
+
+/* One fused pass over X (glm.py:351-372 loglike_grad -> _block_fg; glm.py:257 loglike):
+ *   f = L(beta) [+ sum_k -0.5 ((beta_k-mu_k)/sigma_k)^2 if with_prior]
+ *   g = X'(y - sigmoid(X beta)) [- (beta-mu)/sigma^2 if with_prior]   (if want_grad)
+ * beta: host double[K]; f_out: host double*; g_out: host double[K] or NULL. */
+PM_API int pm_glm_eval(pm_glm_t h, const double* beta, int with_prior, int want_grad,
+                double* f_out, double* g_out);
+
+/* Split form of pm_glm_eval for several handles in flight (the reference's
+ * SHARDED strategy, glm.py:439-454, one shard per device): _launch enqueues the
+ * kernel on the handle's stream, _wait synchronises and returns the result. */
+PM_API int pm_glm_launch(pm_glm_t h, const double* beta, int with_prior, int want_grad);
+PM_API int pm_glm_wait(pm_glm_t h, double* f_out, double* g_out);
+
+/* Device-output form for collectives: writes (f, g[K]) as K+1 doubles to the device
+ * buffer dev_out on `stream` (a cudaStream_t, NULL = the handle's own stream) without
+ * synchronising; the caller reduces the partials across ranks (NCCL) and adds the prior. */
+PM_API int pm_glm_eval_device(pm_glm_t h, const double* beta, int want_grad, double* dev_out,
+                       void* stream);
+
+/* Benchmark helper: n back-to-back launches (beta row i of betas[n][K]) bracketed by CUDA
+ * events on the handle's stream; *total_ms = elapsed device time. */
+PM_API int pm_glm_time_launches(pm_glm_t h, const double* betas, int32_t n, int with_prior,
+                                int want_grad, float* total_ms);
+
+/* The handle's CUDA stream (cudaStream_t), for event timing by the caller. */
+PM_API int pm_glm_stream(pm_glm_t h, void** stream);
+/* Launch geometry actually used (for the bench roofline and tests). */
+PM_API int pm_glm_geometry(pm_glm_t h, int* grid, int* threads, int* stages, size_t* smem_bytes,
+                    int* kernel_kind);
+
+/* ------------------------------------------------------------------ differential update
+ * Replaces GlmWorkspace / diff_loglike / commit_update (glm.py:461-539): a
+ * device-resident xbeta[N] = X beta_current and the transposed copy xt[K][N].
+ */
+typedef struct pm_ws_s* pm_ws_t;
+
+PM_API int pm_ws_create(pm_glm_t h, const double* beta0, pm_ws_t* out);
+PM_API int pm_ws_destroy(pm_ws_t ws);
+/* f_out[m] = L(beta_current + deltas[m] e_k), m < n_deltas (glm.py:499-522), one pass
+ * over (xbeta, xt[k], y) for all deltas; never mutates the workspace. */
+PM_API int pm_ws_diff_eval(pm_ws_t ws, int32_t k, const double* deltas, int32_t n_deltas,
+                    double* f_out);
+/* xbeta += delta * xt[k] (glm.py:525-539; bit-identical to numpy's two roundings). */
+PM_API int pm_ws_commit(pm_ws_t ws, int32_t k, double delta);
+PM_API int pm_ws_read_xbeta(pm_ws_t ws, double* out);
+/* max_n |xbeta_n - (X beta_current)_n| recomputed on the device (GlmWorkspace.validate,
+ * glm.py:484-489). */
+PM_API int pm_ws_validate(pm_ws_t ws, const double* beta_current, double* max_abs_err);
+
+/* ------------------------------------------------------------------ hierarchical GLM
+ * Replaces the per-group loop of loglike_grad over HbDataset.groups (hb.py:64-86,
+ * 127-135) with one launch over CSR-batched groups sharing K.
+ */
+typedef struct pm_hb_s* pm_hb_t;
+
+PM_API int pm_hb_create(int device, pm_hb_t* out);
+PM_API int pm_hb_destroy(pm_hb_t h);
+/* X: host double[offsets[G]][K] row-major, y: host double[offsets[G]], offsets int64[G+1]
+ * (offsets[0] == 0, non-decreasing, every group non-empty). */
+PM_API int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64_t* offsets,
+                 int32_t n_groups, int32_t n_cols);
+/* betas: host double[G][K]; mu, sigma: host double[K] shared prior or NULL (no prior);
+ * f_out: host double[G]; g_out: host double[G][K] or NULL. */
+PM_API int pm_hb_eval(pm_hb_t h, const double* betas, const double* mu, const double* sigma,
+               int want_grad, double* f_out, double* g_out);
+PM_API int pm_hb_stream(pm_hb_t h, void** stream);
+
+/* ------------------------------------------------------------------ lattice Gibbs
+ * Replaces IsingLattice/ColorPartition/gibbs_sweep (ising.py:47-187) and adds the
+ * periodic boundary and the q=4 Potts model.  Colour c = (i+j)%2; colour 0 updates
+ * against frozen colour 1, then colour 1 (ising.py:175-187).
+ */
+enum pm_boundary { PM_BOUNDARY_FREE = 0, PM_BOUNDARY_PERIODIC = 1 };
+enum pm_model { PM_MODEL_ISING = 0, PM_MODEL_POTTS4 = 1 };
+enum pm_rng {
+  /* caller-supplied doubles in the reference's consumption order: per sweep, colour 0
+   * in packed (scan) order then colour 1 (ising.py:185, rng.py:115-127) */
+  PM_RNG_UNIFORMS = 0,
+  /* numpy Philox4x64-10 DeviateBuffer stream (rng.py:42-44,86-90): deviate i uses
+   * counter i/4+1, word i%4, u = (word>>11)*2^-53; key = (key0, key1) */
+  PM_RNG_NUMPY_PHILOX = 1,
+  /* Philox4x32-10 keyed by (seed, sweep, site): key = (key0 lo32, key0 hi32), counter
+   * = (s/4 lo32, s/4 hi32, sweep lo32, sweep hi32), word s%4, u = word*2^-32, where
+   * s = c*ceil(HW/2) + (i*W+j)/2 is the site's position in the sweep's stream */
+  PM_RNG_PHILOX4X32 = 2
+};
+
+typedef struct pm_lat_s* pm_lat_t;
+
+PM_API int pm_lat_create(int device, int32_t height, int32_t width, int boundary, int model,
+                  pm_lat_t* out);
+PM_API int pm_lat_destroy(pm_lat_t h);
+/* spins: host int8[H*W] row-major; Ising values +-1, Potts values 0..3. */
+PM_API int pm_lat_set_spins(pm_lat_t h, const int8_t* spins);
+PM_API int pm_lat_get_spins(pm_lat_t h, int8_t* spins);
+/* Ising field: P(s=+1) = expit(b_ij + w * sum of neighbour spins) (ising.py:11-16, 184);
+ * bias: host double[H*W] or NULL for b == 0.  The host builds the exact probability
+ * table with the reference's own arithmetic (b + w*nsum, then 1/(1+exp(-z)), as
+ * scipy.special.expit), so the device compare u < p is bit-identical. */
+PM_API int pm_lat_set_ising(pm_lat_t h, double w, const double* bias);
+/* Potts q=4: P(a) proportional to exp(coupling * n_a), n_a = neighbours in state a;
+ * a = #{a' < 3 : u >= cdf[a']} with the cdf built on the host in ascending a. */
+PM_API int pm_lat_set_potts(pm_lat_t h, double coupling);
+/* Run n_sweeps full sweeps.  stream_pos: PM_RNG_NUMPY_PHILOX -> index of the next
+ * deviate of the buffer's stream; PM_RNG_PHILOX4X32 -> sweep number of the first sweep.
+ * uniforms: host double[n_sweeps*H*W] for PM_RNG_UNIFORMS, else NULL. */
+PM_API int pm_lat_sweeps(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t key0, uint64_t key1,
+                  uint64_t stream_pos, const double* uniforms);
+/* Benchmark helper: pm_lat_sweeps for an in-kernel RNG mode, bracketed by CUDA events on the
+ * handle's stream; *total_ms = elapsed device time of the n_sweeps sweeps. */
+PM_API int pm_lat_time_sweeps(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t key0, uint64_t key1,
+                              uint64_t stream_pos, float* total_ms);
+PM_API int pm_lat_stream(pm_lat_t h, void** stream);
+/* 1 if sweeps run on the red-black packed fast path (periodic, even H and W). */
+PM_API int pm_lat_packed(pm_lat_t h, int* packed);
+
+/* Host-side table builders, exported so tests can check them against the oracle. */
+PM_API int pm_ising_prob_table(double w, double b, double* p_out /*9: nsum=-4..4*/);
+PM_API int pm_potts_cdf_table(double coupling, double* cdf_out /*625*3*/);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PMB200_H */

@@ -1,0 +1,878 @@
+// Host side of the GLM hot path: handles, geometry, dispatch and the C ABI
+// (include/pmb200.h).  Kernels live in glm_kernels.cuh / glm_aux_kernels.cuh.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "glm_aux_kernels.cuh"
+
+using namespace pm;
+
+namespace {
+
+constexpr int kNCW = 8;                      // consumer warps of the streaming kernel
+constexpr int kStreamThreads = (kNCW + 1) * 32;
+constexpr int kMaxStages = 16;
+constexpr int kHbNCW = 4;
+constexpr int kHbThreads = (kHbNCW + 1) * 32;
+constexpr int kHbMaxStages = 6;
+constexpr int kWideThreads = 256;
+constexpr int kMaxKC = 8;                    // stream kernel handles K <= 256
+
+enum KernelKind { KIND_NONE = 0, KIND_STREAM = 1, KIND_WIDE = 2 };
+
+int max_optin_smem(int device) {
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  return v;
+}
+
+bool all_finite(const double* p, int64_t n) {
+  for (int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(p[i])) return false;
+  return true;
+}
+
+template <typename T>
+__global__ void count_nonfinite(const T* __restrict__ p, int64_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    c += isfinite(p[i]) ? 0ull : 1ull;
+  for (int s = 16; s >= 1; s >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+}  // namespace
+
+struct pm_glm_s {
+  int device = 0;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  std::mutex mu;
+  // data
+  void* X = nullptr;
+  double* y = nullptr;
+  int xtype = PM_X_F64;
+  int64_t n_rows = 0, n_pad = 0, n_tiles = 0;
+  int K = 0;
+  // prior
+  double* prior_mu = nullptr;
+  double* prior_sigma = nullptr;
+  bool has_prior = false;
+  // scratch
+  double* partials = nullptr;
+  int partials_cap = 0;
+  unsigned int* counter = nullptr;
+  double* out_host = nullptr;   // mapped pinned [K+1]
+  double* out_dev = nullptr;    // device alias of out_host
+  double* beta_dev = nullptr;   // [K] (wide kernel)
+  double* beta_pinned = nullptr;
+  // geometry
+  int kind = KIND_NONE;
+  int grid = 0, threads = 0, stages = 0;
+  size_t smem = 0;
+  bool launched = false;
+  int last_want_grad = 1;
+};
+
+namespace {
+
+void free_glm_data(pm_glm_s* h) {
+  if (h->X) cudaFree(h->X);
+  if (h->y) cudaFree(h->y);
+  if (h->partials) cudaFree(h->partials);
+  if (h->beta_dev) cudaFree(h->beta_dev);
+  if (h->out_host) cudaFreeHost(h->out_host);
+  if (h->beta_pinned) cudaFreeHost(h->beta_pinned);
+  if (h->prior_mu) cudaFree(h->prior_mu);
+  if (h->prior_sigma) cudaFree(h->prior_sigma);
+  h->X = nullptr;
+  h->y = nullptr;
+  h->partials = nullptr;
+  h->beta_dev = nullptr;
+  h->out_host = nullptr;
+  h->out_dev = nullptr;
+  h->beta_pinned = nullptr;
+  h->prior_mu = h->prior_sigma = nullptr;
+  h->has_prior = false;
+  h->K = 0;
+  h->n_rows = h->n_pad = h->n_tiles = 0;
+  h->kind = KIND_NONE;
+}
+
+// ---- stream kernel dispatch table ------------------------------------------------
+using StreamLaunch = cudaError_t (*)(const GlmArgs&, const double*, int, size_t, cudaStream_t);
+
+template <typename XT, int KC, bool GRAD>
+cudaError_t launch_stream(const GlmArgs& a, const double* beta, int grid, size_t smem, cudaStream_t st) {
+  static std::atomic<uint64_t> attr{0};
+  auto kern = glm_stream_kernel<XT, KC, GRAD, kNCW>;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), attr);
+  if (e != cudaSuccess) return e;
+  BetaPack<KC> bp;
+  for (int k = 0; k < 32 * KC; ++k) bp.v[k] = (k < a.K) ? beta[k] : 0.0;
+  kern<<<grid, kStreamThreads, smem, st>>>(a, bp);
+  return cudaGetLastError();
+}
+
+template <typename XT, bool GRAD>
+StreamLaunch pick_stream(int kc) {
+  switch (kc) {
+    case 1: return launch_stream<XT, 1, GRAD>;
+    case 2: return launch_stream<XT, 2, GRAD>;
+    case 3: return launch_stream<XT, 3, GRAD>;
+    case 4: return launch_stream<XT, 4, GRAD>;
+    case 5: return launch_stream<XT, 5, GRAD>;
+    case 6: return launch_stream<XT, 6, GRAD>;
+    case 7: return launch_stream<XT, 7, GRAD>;
+    case 8: return launch_stream<XT, 8, GRAD>;
+  }
+  return nullptr;
+}
+
+StreamLaunch pick_stream_any(int xtype, int kc, bool grad) {
+  if (xtype == PM_X_F64) return grad ? pick_stream<double, true>(kc) : pick_stream<double, false>(kc);
+  return grad ? pick_stream<float, true>(kc) : pick_stream<float, false>(kc);
+}
+
+template <typename XT, bool GRAD>
+cudaError_t launch_wide(const GlmArgs& a, int grid, int threads, size_t smem, cudaStream_t st) {
+  static std::atomic<uint64_t> attr{0};
+  auto kern = glm_wide_kernel<XT, GRAD>;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), attr);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, threads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+int choose_geometry(pm_glm_s* h) {
+  const int xs = (h->xtype == PM_X_F64) ? 8 : 4;
+  const int kc = (h->K + 31) / 32;
+  const int budget = std::min(max_optin_smem(h->device), 232448) - 1024;
+  h->kind = KIND_NONE;
+  if (kc <= kMaxKC) {
+    const size_t fixed = stream_smem_bytes(h->K, xs, 0, kNCW);
+    const size_t per_stage = stream_smem_bytes(h->K, xs, 1, 0) - stream_smem_bytes(h->K, xs, 0, 0);
+    int S = int((budget - (long)fixed) / (long)per_stage);
+    S = std::min(S, kMaxStages);
+    if (S >= 2) {
+      h->kind = KIND_STREAM;
+      h->stages = S;
+      h->threads = kStreamThreads;
+      h->smem = stream_smem_bytes(h->K, xs, S, kNCW);
+      h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, h->n_tiles));
+    }
+  }
+  if (h->kind == KIND_NONE) {
+    int nw = kWideThreads / 32;
+    while (nw > 1 && stream_smem_bytes(h->K, xs, 0, nw) > (size_t)budget) --nw;
+    if (stream_smem_bytes(h->K, xs, 0, nw) > (size_t)budget)
+      return fail(PM_EINVAL, "n_cols too large for the device (K=" + std::to_string(h->K) + ")");
+    h->kind = KIND_WIDE;
+    h->stages = 0;
+    h->threads = nw * 32;
+    h->smem = stream_smem_bytes(h->K, xs, 0, nw);
+    const int64_t warps_needed = (h->n_rows + 0);
+    const int64_t blocks = (warps_needed + nw - 1) / nw;
+    h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(int64_t(h->sms) * 2, blocks));
+  }
+  return PM_OK;
+}
+
+GlmArgs make_args(pm_glm_s* h, bool with_prior, double* out) {
+  GlmArgs a;
+  a.X = h->X;
+  a.y = h->y;
+  a.n_rows = h->n_rows;
+  a.n_tiles = h->n_tiles;
+  a.K = h->K;
+  a.stages = h->stages;
+  a.with_prior = with_prior ? 1 : 0;
+  a.evict_first = 1;
+  a.prior_mu = h->prior_mu;
+  a.prior_sigma = h->prior_sigma;
+  a.partials = h->partials;
+  a.counter = h->counter;
+  a.out = out;
+  a.beta_dev = h->beta_dev;
+  return a;
+}
+
+int check_beta(pm_glm_s* h, const double* beta) {
+  if (!beta) return fail(PM_EINVAL, "beta is null");
+  if (!all_finite(beta, h->K)) return fail(PM_EINVAL, "beta contains non-finite entries");
+  return PM_OK;
+}
+
+// enqueue one evaluation writing (f, g) to `out` on stream `st` (caller holds the mutex)
+int enqueue_eval(pm_glm_s* h, const double* beta, bool with_prior, bool grad, double* out, cudaStream_t st) {
+  GlmArgs a = make_args(h, with_prior, out);
+  cudaError_t e;
+  if (h->kind == KIND_STREAM) {
+    StreamLaunch fn = pick_stream_any(h->xtype, (h->K + 31) / 32, grad);
+    e = fn(a, beta, h->grid, h->smem, st);
+  } else {
+    std::memcpy(h->beta_pinned, beta, sizeof(double) * h->K);
+    e = cudaMemcpyAsync(h->beta_dev, h->beta_pinned, sizeof(double) * h->K, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+      if (h->xtype == PM_X_F64)
+        e = grad ? launch_wide<double, true>(a, h->grid, h->threads, h->smem, st)
+                 : launch_wide<double, false>(a, h->grid, h->threads, h->smem, st);
+      else
+        e = grad ? launch_wide<float, true>(a, h->grid, h->threads, h->smem, st)
+                 : launch_wide<float, false>(a, h->grid, h->threads, h->smem, st);
+    }
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "glm kernel launch");
+  return PM_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int pm_glm_create(int device, pm_glm_t* out) {
+  if (!out) return fail(PM_EINVAL, "pm_glm_create: null output");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (device < 0 || device >= n) return fail(PM_ERANGE, "device index out of range");
+  pm_glm_s* h = new pm_glm_s();
+  h->device = device;
+  DeviceGuard g(device);
+  h->sms = sm_count(device);
+  e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaMalloc(&h->counter, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(h->counter, 0, sizeof(unsigned int));
+  if (e != cudaSuccess) {
+    delete h;
+    return cuda_fail(e, "pm_glm_create");
+  }
+  *out = h;
+  return PM_OK;
+}
+
+int pm_glm_destroy(pm_glm_t h) {
+  if (!h) return PM_OK;
+  {
+    std::lock_guard<std::mutex> lk(h->mu);
+    DeviceGuard g(h->device);
+    cudaStreamSynchronize(h->stream);
+    free_glm_data(h);
+    if (h->counter) cudaFree(h->counter);
+    if (h->ev_a) cudaEventDestroy(h->ev_a);
+    if (h->ev_b) cudaEventDestroy(h->ev_b);
+    if (h->stream) cudaStreamDestroy(h->stream);
+  }
+  delete h;
+  return PM_OK;
+}
+
+int pm_glm_upload(pm_glm_t h, const void* X, int x_dtype, const double* y, int64_t n_rows, int32_t n_cols) {
+  if (!h) return fail(PM_EINVAL, "null handle");
+  if (!X || !y) return fail(PM_EINVAL, "X and y must be non-null");
+  if (n_rows < 1 || n_cols < 1)
+    return fail(PM_EINVAL, "need N >= 1 and K >= 1, got shape (" + std::to_string(n_rows) + ", " +
+                               std::to_string(n_cols) + ")");
+  if (x_dtype != PM_X_F64 && x_dtype != PM_X_F32) return fail(PM_EINVAL, "x_dtype must be PM_X_F64 or PM_X_F32");
+  for (int64_t i = 0; i < n_rows; ++i)
+    if (!(y[i] == 0.0 || y[i] == 1.0)) return fail(PM_EINVAL, "y entries must be exactly 0 or 1");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  cudaStreamSynchronize(h->stream);
+  free_glm_data(h);
+  h->xtype = x_dtype;
+  h->n_rows = n_rows;
+  h->K = n_cols;
+  h->n_pad = (n_rows + kTileRows - 1) / kTileRows * kTileRows;
+  h->n_tiles = h->n_pad / kTileRows;
+  const size_t xs = (x_dtype == PM_X_F64) ? 8 : 4;
+  const size_t xbytes = size_t(h->n_pad) * n_cols * xs;
+  const size_t real_bytes = size_t(n_rows) * n_cols * xs;
+  PM_CUDA(cudaMalloc(&h->X, xbytes));
+  PM_CUDA(cudaMalloc(&h->y, sizeof(double) * h->n_pad));
+  PM_CUDA(cudaMemsetAsync(static_cast<char*>(h->X) + real_bytes, 0, xbytes - real_bytes, h->stream));
+  PM_CUDA(cudaMemsetAsync(h->y + n_rows, 0, sizeof(double) * (h->n_pad - n_rows), h->stream));
+  PM_CUDA(cudaMemcpyAsync(h->y, y, sizeof(double) * n_rows, cudaMemcpyHostToDevice, h->stream));
+  unsigned long long* bad = nullptr;
+  PM_CUDA(cudaMalloc(&bad, sizeof(unsigned long long)));
+  PM_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned long long), h->stream));
+  if (x_dtype == PM_X_F64) {
+    PM_CUDA(cudaMemcpyAsync(h->X, X, real_bytes, cudaMemcpyHostToDevice, h->stream));
+    count_nonfinite<double><<<h->sms * 4, 256, 0, h->stream>>>(static_cast<const double*>(h->X),
+                                                               int64_t(n_rows) * n_cols, bad);
+  } else {
+    // X arrives as float (the caller rounded the reference's float64 X, glm.py:88)
+    PM_CUDA(cudaMemcpyAsync(h->X, X, real_bytes, cudaMemcpyHostToDevice, h->stream));
+    count_nonfinite<float><<<h->sms * 4, 256, 0, h->stream>>>(static_cast<const float*>(h->X),
+                                                              int64_t(n_rows) * n_cols, bad);
+  }
+  unsigned long long nbad = 0;
+  PM_CUDA(cudaMemcpyAsync(&nbad, bad, sizeof(nbad), cudaMemcpyDeviceToHost, h->stream));
+  PM_CUDA(cudaStreamSynchronize(h->stream));
+  cudaFree(bad);
+  if (nbad) {
+    free_glm_data(h);
+    return fail(PM_EINVAL, "x contains non-finite entries");
+  }
+  int rc = choose_geometry(h);
+  if (rc != PM_OK) {
+    free_glm_data(h);
+    return rc;
+  }
+  h->partials_cap = std::max(h->grid, 1);
+  PM_CUDA(cudaMalloc(&h->partials, sizeof(double) * size_t(h->partials_cap) * (n_cols + 1)));
+  PM_CUDA(cudaMalloc(&h->beta_dev, sizeof(double) * n_cols));
+  PM_CUDA(cudaHostAlloc(&h->out_host, sizeof(double) * (n_cols + 1), cudaHostAllocMapped | cudaHostAllocPortable));
+  PM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->out_dev), h->out_host, 0));
+  PM_CUDA(cudaHostAlloc(&h->beta_pinned, sizeof(double) * n_cols, cudaHostAllocPortable));
+  return PM_OK;
+}
+
+int pm_glm_set_prior(pm_glm_t h, const double* mu, const double* sigma) {
+  if (!h) return fail(PM_EINVAL, "null handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  if (h->K == 0) return fail(PM_ESTATE, "upload data before setting the prior");
+  if (!mu && !sigma) {
+    h->has_prior = false;
+    return PM_OK;
+  }
+  if (!mu || !sigma) return fail(PM_EINVAL, "mu and sigma must both be given");
+  for (int k = 0; k < h->K; ++k) {
+    if (!std::isfinite(mu[k]) || !std::isfinite(sigma[k])) return fail(PM_EINVAL, "prior must be finite");
+    if (!(sigma[k] > 0)) return fail(PM_EINVAL, "all prior sigmas must be > 0");
+  }
+  cudaStreamSynchronize(h->stream);
+  if (!h->prior_mu) PM_CUDA(cudaMalloc(&h->prior_mu, sizeof(double) * h->K));
+  if (!h->prior_sigma) PM_CUDA(cudaMalloc(&h->prior_sigma, sizeof(double) * h->K));
+  PM_CUDA(cudaMemcpy(h->prior_mu, mu, sizeof(double) * h->K, cudaMemcpyHostToDevice));
+  PM_CUDA(cudaMemcpy(h->prior_sigma, sigma, sizeof(double) * h->K, cudaMemcpyHostToDevice));
+  h->has_prior = true;
+  return PM_OK;
+}
+
+int pm_glm_launch(pm_glm_t h, const double* beta, int with_prior, int want_grad) {
+  if (!h) return fail(PM_EINVAL, "null handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->K == 0) return fail(PM_ESTATE, "no data uploaded");
+  if (with_prior && !h->has_prior) return fail(PM_ESTATE, "with_prior set but no prior configured");
+  int rc = check_beta(h, beta);
+  if (rc) return rc;
+  DeviceGuard g(h->device);
+  rc = enqueue_eval(h, beta, with_prior != 0, want_grad != 0, h->out_dev, h->stream);
+  if (rc) return rc;
+  h->launched = true;
+  h->last_want_grad = want_grad;
+  return PM_OK;
+}
+
+int pm_glm_wait(pm_glm_t h, double* f_out, double* g_out) {
+  if (!h) return fail(PM_EINVAL, "null handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (!h->launched) return fail(PM_ESTATE, "pm_glm_wait without a launch");
+  DeviceGuard g(h->device);
+  PM_CUDA(cudaStreamSynchronize(h->stream));
+  h->launched = false;
+  if (f_out) *f_out = h->out_host[0];
+  if (g_out && h->last_want_grad) std::memcpy(g_out, h->out_host + 1, sizeof(double) * h->K);
+  return PM_OK;
+}
+
+int pm_glm_eval(pm_glm_t h, const double* beta, int with_prior, int want_grad, double* f_out, double* g_out) {
+  int rc = pm_glm_launch(h, beta, with_prior, want_grad);
+  if (rc) return rc;
+  return pm_glm_wait(h, f_out, g_out);
+}
+
+int pm_glm_eval_device(pm_glm_t h, const double* beta, int want_grad, double* dev_out, void* stream) {
+  if (!h) return fail(PM_EINVAL, "null handle");
+  if (!dev_out) return fail(PM_EINVAL, "dev_out is null");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->K == 0) return fail(PM_ESTATE, "no data uploaded");
+  int rc = check_beta(h, beta);
+  if (rc) return rc;
+  DeviceGuard g(h->device);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+  if (st != h->stream) {  // order against earlier work on the handle (shared scratch)
+    PM_CUDA(cudaEventRecord(h->ev_a, h->stream));
+    PM_CUDA(cudaStreamWaitEvent(st, h->ev_a, 0));
+  }
+  rc = enqueue_eval(h, beta, false, want_grad != 0, dev_out, st);
+  if (rc) return rc;
+  if (st != h->stream) {
+    PM_CUDA(cudaEventRecord(h->ev_b, st));
+    PM_CUDA(cudaStreamWaitEvent(h->stream, h->ev_b, 0));
+  }
+  return PM_OK;
+}
+
+int pm_glm_time_launches(pm_glm_t h, const double* betas, int32_t n, int with_prior, int want_grad,
+                         float* total_ms) {
+  if (!h || !betas || !total_ms) return fail(PM_EINVAL, "null argument");
+  if (n < 1) return fail(PM_EINVAL, "n must be >= 1");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->K == 0) return fail(PM_ESTATE, "no data uploaded");
+  if (with_prior && !h->has_prior) return fail(PM_ESTATE, "with_prior set but no prior configured");
+  for (int i = 0; i < n; ++i) {
+    int rc = check_beta(h, betas + size_t(i) * h->K);
+    if (rc) return rc;
+  }
+  DeviceGuard g(h->device);
+  cudaEvent_t e0, e1;
+  PM_CUDA(cudaEventCreate(&e0));
+  PM_CUDA(cudaEventCreate(&e1));
+  PM_CUDA(cudaStreamSynchronize(h->stream));
+  PM_CUDA(cudaEventRecord(e0, h->stream));
+  for (int i = 0; i < n; ++i) {
+    int rc = enqueue_eval(h, betas + size_t(i) * h->K, with_prior != 0, want_grad != 0, h->out_dev, h->stream);
+    if (rc) return rc;
+  }
+  PM_CUDA(cudaEventRecord(e1, h->stream));
+  PM_CUDA(cudaEventSynchronize(e1));
+  PM_CUDA(cudaEventElapsedTime(total_ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  h->last_want_grad = want_grad;
+  return PM_OK;
+}
+
+int pm_glm_stream(pm_glm_t h, void** stream) {
+  if (!h || !stream) return fail(PM_EINVAL, "null argument");
+  *stream = h->stream;
+  return PM_OK;
+}
+
+int pm_glm_geometry(pm_glm_t h, int* grid, int* threads, int* stages, size_t* smem_bytes, int* kernel_kind) {
+  if (!h) return fail(PM_EINVAL, "null handle");
+  if (grid) *grid = h->grid;
+  if (threads) *threads = h->threads;
+  if (stages) *stages = h->stages;
+  if (smem_bytes) *smem_bytes = h->smem;
+  if (kernel_kind) *kernel_kind = h->kind;
+  return PM_OK;
+}
+
+}  // extern "C"
+
+// ====================================================================== workspace
+struct pm_ws_s {
+  pm_glm_s* h = nullptr;
+  double* xbeta = nullptr;
+  double* xt = nullptr;
+  double* tmp = nullptr;
+  double* beta_dev = nullptr;
+  double* partials = nullptr;
+  unsigned int* counter = nullptr;
+  unsigned long long* maxbits = nullptr;
+  double* out_host = nullptr;
+  double* out_dev = nullptr;
+  int grid = 0;
+  std::mutex mu;
+};
+
+namespace {
+
+template <int M>
+cudaError_t launch_diff(const DiffArgs& a, const DeltaPack& dp, int grid, cudaStream_t st) {
+  diff_eval_kernel<M><<<grid, 256, 0, st>>>(a, dp);
+  return cudaGetLastError();
+}
+
+void free_ws(pm_ws_s* w) {
+  if (w->xbeta) cudaFree(w->xbeta);
+  if (w->xt) cudaFree(w->xt);
+  if (w->tmp) cudaFree(w->tmp);
+  if (w->beta_dev) cudaFree(w->beta_dev);
+  if (w->partials) cudaFree(w->partials);
+  if (w->counter) cudaFree(w->counter);
+  if (w->maxbits) cudaFree(w->maxbits);
+  if (w->out_host) cudaFreeHost(w->out_host);
+}
+
+cudaError_t launch_xbeta(pm_glm_s* h, const double* beta_dev, double* out) {
+  const int grid = std::max(1, std::min(h->sms * 8, int((h->n_rows * 32 + 255) / 256)));
+  if (h->xtype == PM_X_F64)
+    xbeta_kernel<double><<<grid, 256, 0, h->stream>>>(static_cast<const double*>(h->X), beta_dev, h->K, h->n_rows,
+                                                      out);
+  else
+    xbeta_kernel<float><<<grid, 256, 0, h->stream>>>(static_cast<const float*>(h->X), beta_dev, h->K, h->n_rows, out);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" {
+
+int pm_ws_create(pm_glm_t h, const double* beta0, pm_ws_t* out) {
+  if (!h || !out) return fail(PM_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->K == 0) return fail(PM_ESTATE, "no data uploaded");
+  int rc = check_beta(h, beta0);
+  if (rc) return rc;
+  DeviceGuard g(h->device);
+  pm_ws_s* w = new pm_ws_s();
+  w->h = h;
+  const int64_t n = h->n_rows, np = h->n_pad;
+  const int K = h->K;
+  cudaError_t e = cudaSuccess;
+  auto chk = [&](cudaError_t x) {
+    if (e == cudaSuccess) e = x;
+  };
+  chk(cudaMalloc(&w->xbeta, sizeof(double) * np));
+  chk(cudaMalloc(&w->tmp, sizeof(double) * np));
+  chk(cudaMalloc(&w->xt, sizeof(double) * size_t(K) * np));
+  chk(cudaMalloc(&w->beta_dev, sizeof(double) * K));
+  w->grid = (int)std::max<int64_t>(1, std::min<int64_t>(int64_t(h->sms) * 4, (n + 255) / 256));
+  chk(cudaMalloc(&w->partials, sizeof(double) * size_t(w->grid) * kMaxDeltas));
+  chk(cudaMalloc(&w->counter, sizeof(unsigned int)));
+  chk(cudaMalloc(&w->maxbits, sizeof(unsigned long long)));
+  chk(cudaHostAlloc(&w->out_host, sizeof(double) * kMaxDeltas, cudaHostAllocMapped | cudaHostAllocPortable));
+  if (e != cudaSuccess) {
+    free_ws(w);
+    delete w;
+    return cuda_fail(e, "pm_ws_create alloc");
+  }
+  cudaHostGetDevicePointer(reinterpret_cast<void**>(&w->out_dev), w->out_host, 0);
+  chk(cudaMemsetAsync(w->counter, 0, sizeof(unsigned int), h->stream));
+  chk(cudaMemsetAsync(w->xbeta, 0, sizeof(double) * np, h->stream));
+  chk(cudaMemcpyAsync(w->beta_dev, beta0, sizeof(double) * K, cudaMemcpyHostToDevice, h->stream));
+  chk(launch_xbeta(h, w->beta_dev, w->xbeta));
+  dim3 tg(unsigned((n + 31) / 32), unsigned((K + 31) / 32));
+  if (h->xtype == PM_X_F64)
+    transpose_kernel<double><<<tg, 256, 0, h->stream>>>(static_cast<const double*>(h->X), n, K, w->xt, np);
+  else
+    transpose_kernel<float><<<tg, 256, 0, h->stream>>>(static_cast<const float*>(h->X), n, K, w->xt, np);
+  chk(cudaGetLastError());
+  chk(cudaStreamSynchronize(h->stream));
+  if (e != cudaSuccess) {
+    free_ws(w);
+    delete w;
+    return cuda_fail(e, "pm_ws_create init");
+  }
+  *out = w;
+  return PM_OK;
+}
+
+int pm_ws_destroy(pm_ws_t w) {
+  if (!w) return PM_OK;
+  {
+    std::lock_guard<std::mutex> lk(w->h->mu);
+    DeviceGuard g(w->h->device);
+    cudaStreamSynchronize(w->h->stream);
+    free_ws(w);
+  }
+  delete w;
+  return PM_OK;
+}
+
+int pm_ws_diff_eval(pm_ws_t w, int32_t k, const double* deltas, int32_t n_deltas, double* f_out) {
+  if (!w || !deltas || !f_out) return fail(PM_EINVAL, "null argument");
+  pm_glm_s* h = w->h;
+  if (k < 0 || k >= h->K)
+    return fail(PM_ERANGE, "coordinate " + std::to_string(k) + " out of range [0, " + std::to_string(h->K) + ")");
+  if (n_deltas < 1 || n_deltas > kMaxDeltas)
+    return fail(PM_EINVAL, "n_deltas must be in [1, " + std::to_string(kMaxDeltas) + "]");
+  if (!all_finite(deltas, n_deltas)) return fail(PM_EINVAL, "delta_beta_k must be finite");
+  std::lock_guard<std::mutex> lk(w->mu);
+  std::lock_guard<std::mutex> lk2(h->mu);
+  DeviceGuard g(h->device);
+  DiffArgs a;
+  a.xbeta = w->xbeta;
+  a.xk = w->xt + size_t(k) * h->n_pad;
+  a.y = h->y;
+  a.n = h->n_rows;
+  a.partials = w->partials;
+  a.counter = w->counter;
+  a.out = w->out_dev;
+  DeltaPack dp;
+  for (int m = 0; m < kMaxDeltas; ++m) dp.d[m] = m < n_deltas ? deltas[m] : 0.0;
+  cudaError_t e;
+  if (n_deltas == 1) e = launch_diff<1>(a, dp, w->grid, h->stream);
+  else if (n_deltas == 2) e = launch_diff<2>(a, dp, w->grid, h->stream);
+  else if (n_deltas <= 4) e = launch_diff<4>(a, dp, w->grid, h->stream);
+  else if (n_deltas <= 8) e = launch_diff<8>(a, dp, w->grid, h->stream);
+  else e = launch_diff<16>(a, dp, w->grid, h->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "diff_eval launch");
+  PM_CUDA(cudaStreamSynchronize(h->stream));
+  std::memcpy(f_out, w->out_host, sizeof(double) * n_deltas);
+  return PM_OK;
+}
+
+int pm_ws_commit(pm_ws_t w, int32_t k, double delta) {
+  if (!w) return fail(PM_EINVAL, "null workspace");
+  pm_glm_s* h = w->h;
+  if (k < 0 || k >= h->K)
+    return fail(PM_ERANGE, "coordinate " + std::to_string(k) + " out of range [0, " + std::to_string(h->K) + ")");
+  if (!std::isfinite(delta)) return fail(PM_EINVAL, "delta_beta_k must be finite");
+  if (delta == 0.0) return PM_OK;  // glm.py:536
+  std::lock_guard<std::mutex> lk(w->mu);
+  std::lock_guard<std::mutex> lk2(h->mu);
+  DeviceGuard g(h->device);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(int64_t(h->sms) * 4, (h->n_rows + 255) / 256));
+  commit_kernel<<<grid, 256, 0, h->stream>>>(w->xbeta, w->xt + size_t(k) * h->n_pad, delta, h->n_rows);
+  PM_CUDA(cudaGetLastError());
+  return PM_OK;
+}
+
+int pm_ws_read_xbeta(pm_ws_t w, double* out) {
+  if (!w || !out) return fail(PM_EINVAL, "null argument");
+  pm_glm_s* h = w->h;
+  std::lock_guard<std::mutex> lk(w->mu);
+  std::lock_guard<std::mutex> lk2(h->mu);
+  DeviceGuard g(h->device);
+  PM_CUDA(cudaMemcpyAsync(out, w->xbeta, sizeof(double) * h->n_rows, cudaMemcpyDeviceToHost, h->stream));
+  PM_CUDA(cudaStreamSynchronize(h->stream));
+  return PM_OK;
+}
+
+int pm_ws_validate(pm_ws_t w, const double* beta_current, double* max_abs_err) {
+  if (!w || !beta_current || !max_abs_err) return fail(PM_EINVAL, "null argument");
+  pm_glm_s* h = w->h;
+  std::lock_guard<std::mutex> lk(w->mu);
+  std::lock_guard<std::mutex> lk2(h->mu);
+  DeviceGuard g(h->device);
+  PM_CUDA(cudaMemcpyAsync(w->beta_dev, beta_current, sizeof(double) * h->K, cudaMemcpyHostToDevice, h->stream));
+  PM_CUDA(launch_xbeta(h, w->beta_dev, w->tmp));
+  PM_CUDA(cudaMemsetAsync(w->maxbits, 0, sizeof(unsigned long long), h->stream));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(int64_t(h->sms) * 4, (h->n_rows + 255) / 256));
+  maxabs_diff_kernel<<<grid, 256, 0, h->stream>>>(w->xbeta, w->tmp, h->n_rows, w->maxbits);
+  PM_CUDA(cudaGetLastError());
+  unsigned long long bits = 0;
+  PM_CUDA(cudaMemcpyAsync(&bits, w->maxbits, sizeof(bits), cudaMemcpyDeviceToHost, h->stream));
+  PM_CUDA(cudaStreamSynchronize(h->stream));
+  double v;
+  std::memcpy(&v, &bits, sizeof(v));
+  *max_abs_err = v;
+  return PM_OK;
+}
+
+}  // extern "C"
+
+// ====================================================================== hierarchical
+struct pm_hb_s {
+  int device = 0;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  double* X = nullptr;
+  double* y = nullptr;
+  int64_t* poff = nullptr;
+  int64_t* nrows = nullptr;
+  int G = 0, K = 0;
+  int stages = 0;
+  size_t smem = 0;
+  double* betas = nullptr;
+  double* mu_dev = nullptr;
+  double* sigma_dev = nullptr;
+  double* out_f = nullptr;
+  double* out_g = nullptr;
+  double* pin_in = nullptr;    // G*K + 2K
+  double* pin_out = nullptr;   // G + G*K
+};
+
+namespace {
+
+void free_hb(pm_hb_s* h) {
+  for (void* p : {(void*)h->X, (void*)h->y, (void*)h->poff, (void*)h->nrows, (void*)h->betas, (void*)h->mu_dev,
+                  (void*)h->sigma_dev, (void*)h->out_f, (void*)h->out_g})
+    if (p) cudaFree(p);
+  if (h->pin_in) cudaFreeHost(h->pin_in);
+  if (h->pin_out) cudaFreeHost(h->pin_out);
+  h->X = h->y = nullptr;
+  h->poff = h->nrows = nullptr;
+  h->betas = h->mu_dev = h->sigma_dev = h->out_f = h->out_g = nullptr;
+  h->pin_in = h->pin_out = nullptr;
+  h->G = h->K = 0;
+}
+
+using HbLaunch = cudaError_t (*)(const HbArgs&, int, size_t, cudaStream_t);
+
+template <int KC, bool GRAD>
+cudaError_t launch_hb(const HbArgs& a, int grid, size_t smem, cudaStream_t st) {
+  static std::atomic<uint64_t> attr{0};
+  auto kern = hb_kernel<KC, GRAD, kHbNCW>;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), attr);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kHbThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <bool GRAD>
+HbLaunch pick_hb(int kc) {
+  switch (kc) {
+    case 1: return launch_hb<1, GRAD>;
+    case 2: return launch_hb<2, GRAD>;
+    case 3: return launch_hb<3, GRAD>;
+    case 4: return launch_hb<4, GRAD>;
+    case 5: return launch_hb<5, GRAD>;
+    case 6: return launch_hb<6, GRAD>;
+    case 7: return launch_hb<7, GRAD>;
+    case 8: return launch_hb<8, GRAD>;
+  }
+  return nullptr;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pm_hb_create(int device, pm_hb_t* out) {
+  if (!out) return fail(PM_EINVAL, "null output");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (device < 0 || device >= n) return fail(PM_ERANGE, "device index out of range");
+  pm_hb_s* h = new pm_hb_s();
+  h->device = device;
+  DeviceGuard g(device);
+  h->sms = sm_count(device);
+  e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete h;
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+  *out = h;
+  return PM_OK;
+}
+
+int pm_hb_destroy(pm_hb_t h) {
+  if (!h) return PM_OK;
+  {
+    std::lock_guard<std::mutex> lk(h->mu);
+    DeviceGuard g(h->device);
+    cudaStreamSynchronize(h->stream);
+    free_hb(h);
+    cudaStreamDestroy(h->stream);
+  }
+  delete h;
+  return PM_OK;
+}
+
+int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64_t* offsets, int32_t G, int32_t K) {
+  if (!h || !X || !y || !offsets) return fail(PM_EINVAL, "null argument");
+  if (G < 1) return fail(PM_EINVAL, "need at least one group");
+  if (K < 1) return fail(PM_EINVAL, "need K >= 1");
+  if ((K + 31) / 32 > kMaxKC) return fail(PM_EINVAL, "hierarchical path supports K <= 256");
+  if (offsets[0] != 0) return fail(PM_EINVAL, "offsets[0] must be 0");
+  for (int g = 0; g < G; ++g)
+    if (offsets[g + 1] <= offsets[g]) return fail(PM_EINVAL, "every group needs >= 1 row (group " + std::to_string(g) + ")");
+  const int64_t N = offsets[G];
+  for (int64_t i = 0; i < N; ++i)
+    if (!(y[i] == 0.0 || y[i] == 1.0)) return fail(PM_EINVAL, "y entries must be exactly 0 or 1");
+  for (int64_t i = 0; i < N * K; ++i)
+    if (!std::isfinite(X[i])) return fail(PM_EINVAL, "x contains non-finite entries");
+  std::vector<int64_t> poff(G + 1), nr(G);
+  poff[0] = 0;
+  for (int g = 0; g < G; ++g) {
+    nr[g] = offsets[g + 1] - offsets[g];
+    poff[g + 1] = poff[g] + (nr[g] + kTileRows - 1) / kTileRows * kTileRows;
+  }
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard gd(h->device);
+  cudaStreamSynchronize(h->stream);
+  free_hb(h);
+  h->G = G;
+  h->K = K;
+  const int64_t NP = poff[G];
+  PM_CUDA(cudaMalloc(&h->X, sizeof(double) * size_t(NP) * K));
+  PM_CUDA(cudaMalloc(&h->y, sizeof(double) * NP));
+  PM_CUDA(cudaMemsetAsync(h->X, 0, sizeof(double) * size_t(NP) * K, h->stream));
+  PM_CUDA(cudaMemsetAsync(h->y, 0, sizeof(double) * NP, h->stream));
+  for (int g = 0; g < G; ++g) {
+    PM_CUDA(cudaMemcpyAsync(h->X + size_t(poff[g]) * K, X + size_t(offsets[g]) * K, sizeof(double) * nr[g] * K,
+                            cudaMemcpyHostToDevice, h->stream));
+    PM_CUDA(cudaMemcpyAsync(h->y + poff[g], y + offsets[g], sizeof(double) * nr[g], cudaMemcpyHostToDevice,
+                            h->stream));
+  }
+  PM_CUDA(cudaMalloc(&h->poff, sizeof(int64_t) * (G + 1)));
+  PM_CUDA(cudaMalloc(&h->nrows, sizeof(int64_t) * G));
+  PM_CUDA(cudaMemcpyAsync(h->poff, poff.data(), sizeof(int64_t) * (G + 1), cudaMemcpyHostToDevice, h->stream));
+  PM_CUDA(cudaMemcpyAsync(h->nrows, nr.data(), sizeof(int64_t) * G, cudaMemcpyHostToDevice, h->stream));
+  PM_CUDA(cudaMalloc(&h->betas, sizeof(double) * size_t(G) * K));
+  PM_CUDA(cudaMalloc(&h->mu_dev, sizeof(double) * K));
+  PM_CUDA(cudaMalloc(&h->sigma_dev, sizeof(double) * K));
+  PM_CUDA(cudaMalloc(&h->out_f, sizeof(double) * G));
+  PM_CUDA(cudaMalloc(&h->out_g, sizeof(double) * size_t(G) * K));
+  PM_CUDA(cudaHostAlloc(&h->pin_in, sizeof(double) * (size_t(G) * K + 2 * K), cudaHostAllocPortable));
+  PM_CUDA(cudaHostAlloc(&h->pin_out, sizeof(double) * (size_t(G) + size_t(G) * K), cudaHostAllocPortable));
+  PM_CUDA(cudaStreamSynchronize(h->stream));
+  const size_t fixed = stream_smem_bytes(K, 8, 0, kHbNCW);
+  const size_t per_stage = stream_smem_bytes(K, 8, 1, 0) - stream_smem_bytes(K, 8, 0, 0);
+  int S = kHbMaxStages;
+  const size_t cap = 60 * 1024;
+  while (S > 2 && fixed + S * per_stage > cap) --S;
+  h->stages = S;
+  h->smem = stream_smem_bytes(K, 8, S, kHbNCW);
+  return PM_OK;
+}
+
+int pm_hb_eval(pm_hb_t h, const double* betas, const double* mu, const double* sigma, int want_grad, double* f_out,
+               double* g_out) {
+  if (!h || !betas || !f_out) return fail(PM_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->G == 0) return fail(PM_ESTATE, "no data uploaded");
+  const int G = h->G, K = h->K;
+  if (!all_finite(betas, int64_t(G) * K)) return fail(PM_EINVAL, "betas contain non-finite entries");
+  const bool prior = mu != nullptr;
+  if (prior != (sigma != nullptr)) return fail(PM_EINVAL, "mu and sigma must both be given");
+  if (prior) {
+    for (int k = 0; k < K; ++k)
+      if (!(sigma[k] > 0) || !std::isfinite(mu[k]) || !std::isfinite(sigma[k]))
+        return fail(PM_EINVAL, "prior must be finite with sigma > 0");
+  }
+  DeviceGuard gd(h->device);
+  std::memcpy(h->pin_in, betas, sizeof(double) * size_t(G) * K);
+  if (prior) {
+    std::memcpy(h->pin_in + size_t(G) * K, mu, sizeof(double) * K);
+    std::memcpy(h->pin_in + size_t(G) * K + K, sigma, sizeof(double) * K);
+  }
+  PM_CUDA(cudaMemcpyAsync(h->betas, h->pin_in, sizeof(double) * size_t(G) * K, cudaMemcpyHostToDevice, h->stream));
+  if (prior) {
+    PM_CUDA(cudaMemcpyAsync(h->mu_dev, h->pin_in + size_t(G) * K, sizeof(double) * K, cudaMemcpyHostToDevice,
+                            h->stream));
+    PM_CUDA(cudaMemcpyAsync(h->sigma_dev, h->pin_in + size_t(G) * K + K, sizeof(double) * K,
+                            cudaMemcpyHostToDevice, h->stream));
+  }
+  HbArgs a;
+  a.X = h->X;
+  a.y = h->y;
+  a.poff = h->poff;
+  a.nrows = h->nrows;
+  a.K = K;
+  a.stages = h->stages;
+  a.betas = h->betas;
+  a.mu = prior ? h->mu_dev : nullptr;
+  a.sigma = prior ? h->sigma_dev : nullptr;
+  a.out_f = h->out_f;
+  a.out_g = h->out_g;
+  const bool grad = want_grad != 0 && g_out != nullptr;
+  HbLaunch fn = grad ? pick_hb<true>((K + 31) / 32) : pick_hb<false>((K + 31) / 32);
+  cudaError_t e = fn(a, G, h->smem, h->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "hb kernel launch");
+  PM_CUDA(cudaMemcpyAsync(h->pin_out, h->out_f, sizeof(double) * G, cudaMemcpyDeviceToHost, h->stream));
+  if (grad)
+    PM_CUDA(cudaMemcpyAsync(h->pin_out + G, h->out_g, sizeof(double) * size_t(G) * K, cudaMemcpyDeviceToHost,
+                            h->stream));
+  PM_CUDA(cudaStreamSynchronize(h->stream));
+  std::memcpy(f_out, h->pin_out, sizeof(double) * G);
+  if (grad) std::memcpy(g_out, h->pin_out + G, sizeof(double) * size_t(G) * K);
+  return PM_OK;
+}
+
+int pm_hb_stream(pm_hb_t h, void** stream) {
+  if (!h || !stream) return fail(PM_EINVAL, "null argument");
+  *stream = h->stream;
+  return PM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,234 @@
+// Device code for the callers of the GLM hot path:
+//   K3 diff_eval   (glm.py:499-522)  multi-delta conditional log-likelihood, one pass
+//   K4 commit      (glm.py:525-539)  xbeta += delta * xt[k]
+//   workspace init (glm.py:469-474)  xbeta = X beta0, xt = X^T
+//   K5 hb segmented (hb.py:64-86, 127-135) one CTA per group over CSR-batched groups
+#pragma once
+
+#include "glm_kernels.cuh"
+
+namespace pm {
+
+constexpr int kMaxDeltas = 16;
+
+struct DeltaPack {
+  double d[kMaxDeltas];
+};
+
+struct DiffArgs {
+  const double* xbeta;
+  const double* xk;   // xt + k*n_pad
+  const double* y;
+  int64_t n;
+  double* partials;   // [grid][kMaxDeltas]
+  unsigned int* counter;
+  double* out;        // [M]
+};
+
+// Rounding identical to numpy's `xbeta + delta*xk` (glm.py:517): product rounded, then sum.
+__device__ __forceinline__ double shifted_t(double xb, double d, double xk) {
+  return __dadd_rn(xb, __dmul_rn(d, xk));
+}
+
+__device__ __forceinline__ double row_nll(double t, double y) {
+  const double e = exp(-fabs(t));
+  return (1.0 - y) * t + fmax(-t, 0.0) + log1p(e);
+}
+
+// Grid-stride over elements; per-thread sums for each delta in the same order for every M,
+// so f for a given delta is bit-identical whether it is evaluated alone or in a batch.
+template <int M>
+__global__ void __launch_bounds__(256) diff_eval_kernel(DiffArgs a, DeltaPack dp) {
+  __shared__ double red[8][M];
+  __shared__ int flag;
+  double acc[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) acc[m] = 0.0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+    const double xb = __ldg(a.xbeta + i);
+    const double xk = __ldg(a.xk + i);
+    const double yy = __ldg(a.y + i);
+#pragma unroll
+    for (int m = 0; m < M; ++m) acc[m] += row_nll(shifted_t(xb, dp.d[m], xk), yy);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const double s = warp_sum(acc[m]);
+    if (lane == 0) red[warp][m] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < M) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w][threadIdx.x];
+    a.partials[size_t(blockIdx.x) * kMaxDeltas + threadIdx.x] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) flag = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!flag) return;
+  __threadfence();
+  if (threadIdx.x < M) {
+    double s0 = 0.0, s1 = 0.0;
+    int b = 0;
+    for (; b + 2 <= (int)gridDim.x; b += 2) {
+      s0 += __ldcg(a.partials + size_t(b) * kMaxDeltas + threadIdx.x);
+      s1 += __ldcg(a.partials + size_t(b + 1) * kMaxDeltas + threadIdx.x);
+    }
+    if (b < (int)gridDim.x) s0 += __ldcg(a.partials + size_t(b) * kMaxDeltas + threadIdx.x);
+    a.out[threadIdx.x] = -(s0 + s1);
+  }
+  if (threadIdx.x == 0) *a.counter = 0u;
+}
+
+__global__ void __launch_bounds__(256) commit_kernel(double* __restrict__ xbeta, const double* __restrict__ xk,
+                                                     double d, int64_t n) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    xbeta[i] = __dadd_rn(xbeta[i], __dmul_rn(d, xk[i]));
+}
+
+// xbeta[r] = X[r,:] . beta  (one warp per row; GlmWorkspace construction and validate)
+template <typename XT>
+__global__ void __launch_bounds__(256) xbeta_kernel(const XT* __restrict__ X, const double* __restrict__ beta,
+                                                    int K, int64_t n, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = w0; r < n; r += nw) {
+    double acc = 0.0;
+    for (int k = lane; k < K; k += 32) acc = fma(ld_x(X + r * K + k), __ldg(beta + k), acc);
+    acc = warp_sum(acc);
+    if (lane == 0) out[r] = acc;
+  }
+}
+
+// max |a - b| over n (validate, glm.py:484-489): per-block max then single atomicMax on bits
+// (non-negative doubles order like their bit patterns, so this is exact and order-free).
+__global__ void __launch_bounds__(256) maxabs_diff_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                                          int64_t n, unsigned long long* out_bits) {
+  double m = 0.0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    m = fmax(m, fabs(a[i] - b[i]));
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, s));
+  if ((threadIdx.x & 31) == 0) atomicMax(out_bits, (unsigned long long)__double_as_longlong(m));
+}
+
+// X [n][K] (row-major, XT) -> xt [K][ld] f64, 32x32 tiles through shared memory.
+template <typename XT>
+__global__ void __launch_bounds__(256) transpose_kernel(const XT* __restrict__ X, int64_t n, int K,
+                                                        double* __restrict__ xt, int64_t ld) {
+  __shared__ double tile[32][33];
+  const int64_t r0 = int64_t(blockIdx.x) * 32;
+  const int c0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t r = r0 + i;
+    const int c = c0 + tx;
+    tile[i][tx] = (r < n && c < K) ? ld_x(X + r * K + c) : 0.0;
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const int c = c0 + i;
+    const int64_t r = r0 + tx;
+    if (c < K && r < n) xt[int64_t(c) * ld + r] = tile[tx][i];
+  }
+}
+
+__global__ void __launch_bounds__(256) f64_to_f32_kernel(const double* __restrict__ src, float* __restrict__ dst,
+                                                         int64_t n) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = __double2float_rn(src[i]);
+}
+
+// ---------------------------------------------------------------- K5 hierarchical
+struct HbArgs {
+  const double* X;        // padded per group: group g occupies rows [poff[g], poff[g+1])
+  const double* y;
+  const int64_t* poff;    // [G+1] padded row offsets (multiples of 32)
+  const int64_t* nrows;   // [G] real rows per group
+  int K;
+  int stages;
+  const double* betas;    // [G][K]
+  const double* mu;       // [K] or null
+  const double* sigma;    // [K] or null
+  double* out_f;          // [G]
+  double* out_g;          // [G][K]
+};
+
+// One CTA per group: the group's tiles stream through the same TMA ring as K1; the CTA
+// reduces its warps in fixed order and adds the shared group prior.  No cross-CTA step.
+template <int KC, bool GRAD, int NCW>
+__global__ void __launch_bounds__((NCW + 1) * 32) hb_kernel(HbArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int K = a.K;
+  const int S = a.stages;
+  const StreamSmem sm = carve_stream_smem(smem_raw, K, sizeof(double), S, NCW);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int grp = blockIdx.x;
+  const double* bg = a.betas + size_t(grp) * K;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  for (int k = threadIdx.x; k < K; k += blockDim.x) sm.sbeta[k] = bg[k];
+  __syncthreads();
+  double breg[KC], g[KC];
+#pragma unroll
+  for (int j = 0; j < KC; ++j) {
+    const int c = lane + 32 * j;
+    breg[j] = (c < K) ? sm.sbeta[c] : 0.0;
+    g[j] = 0.0;
+  }
+  double nll = 0.0;
+  const int64_t p0 = a.poff[grp], p1 = a.poff[grp + 1];
+  stream_tiles<double, KC, GRAD, NCW>(a.X, a.y, K, p0 / kTileRows, p1 / kTileRows, 1, p0 + a.nrows[grp], S, sm,
+                                      breg, g, nll, false);
+  if (warp > 0) {
+    const int cw = warp - 1;
+    const double wsum = warp_sum(nll);
+    if (lane == 0) sm.wf[cw] = -wsum;
+    if (GRAD) {
+#pragma unroll
+      for (int j = 0; j < KC; ++j) {
+        const int c = lane + 32 * j;
+        if (c < K) sm.wg[size_t(cw) * K + c] = g[j];
+      }
+    }
+  }
+  __syncthreads();
+  const bool prior = a.mu != nullptr;
+  for (int c = threadIdx.x; c <= K; c += blockDim.x) {
+    if (c == 0) {
+      double f = 0.0;
+      for (int w = 0; w < NCW; ++w) f += sm.wf[w];
+      if (prior) {
+        for (int k = 0; k < K; ++k) {
+          const double z = (sm.sbeta[k] - a.mu[k]) / a.sigma[k];
+          f += -0.5 * z * z;
+        }
+      }
+      a.out_f[grp] = f;
+    } else if (GRAD) {
+      const int k = c - 1;
+      double gk = 0.0;
+      for (int w = 0; w < NCW; ++w) gk += sm.wg[size_t(w) * K + k];
+      if (prior) {
+        const double sg = a.sigma[k];
+        gk -= (sm.sbeta[k] - a.mu[k]) / (sg * sg);
+      }
+      a.out_g[size_t(grp) * K + k] = gk;
+    }
+  }
+}
+
+}  // namespace pm

@@ -1,0 +1,355 @@
+// Device code of the logistic-GLM hot path, sm_100a.
+//
+// Reference semantics (all /root/reference/pkg/src/parmcmc):
+//   _block_fg            glm.py:367-372   t = x@beta; f = _nll_sum(t,y); gf = y - expit(t); g = x.T@gf
+//   _nll_sum             glm.py:179-192   -sum[(1-y)t + max(-t,0) + log1p(exp(-|t|))]
+//   _merge_grad          glm.py:243-250   fixed-order sum of partials
+//   GaussianPrior        sampler.py:55-58 -0.5*((v-mu)/sigma)^2, constants dropped
+//   diff_loglike         glm.py:499-522   _nll_sum(xbeta + delta*xt[k], y)
+//   commit_update        glm.py:525-539   xbeta += delta*xt[k]
+//
+// Layout in HBM: X row-major [n_pad][K] with n_pad = roundup(N, 32) (zero rows), y f64 [n_pad].
+// One tile = 32 consecutive rows = 32*K*sizeof(XT) contiguous bytes, moved by one TMA bulk
+// copy (cp.async.bulk -> SASS UBLKCP) into a shared-memory ring guarded by mbarriers.
+// X is read from HBM exactly once per evaluation.
+#pragma once
+
+#include "pm_internal.cuh"
+
+namespace pm {
+
+constexpr int kTileRows = 32;
+
+template <int KC>
+struct BetaPack {
+  double v[32 * KC];
+};
+
+// Per-row stable terms, identical algebra to _nll_sum (glm.py:186-192) and expit.
+//   nll = (1-y) t + max(-t,0) + log1p(exp(-|t|))       (the reference's f is -sum nll)
+//   w   = y - sigmoid(t)                                (glm.py:371)
+__device__ __forceinline__ void row_terms(double t, double y, double& nll, double& w) {
+  const double e = exp(-fabs(t));
+  nll = (1.0 - y) * t + fmax(-t, 0.0) + log1p(e);
+  const double inv = 1.0 / (1.0 + e);
+  const double sig = (t >= 0.0) ? inv : e * inv;
+  w = y - sig;
+}
+
+// v[r] holds this lane's partial dot product for tile row r.  Returns, in lane l, the full
+// (all-lane) dot product of row l: a 5-level transpose-reduce, 31 shuffles per 32 rows.
+__device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool upper = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const double send = upper ? v[i] : v[i + s];
+      const double keep = upper ? v[i + s] : v[i];
+      v[i] = keep + shfl_xor_d(send, s);
+    }
+  }
+  return v[0];
+}
+
+template <typename XT>
+__device__ __forceinline__ double ld_x(const XT* p) {
+  return static_cast<double>(*p);
+}
+
+// One warp consumes one 32-row tile resident in shared memory.
+// Lane l owns columns l + 32 j (j < KC): beta and the gradient accumulators live in
+// registers, so the tile is read from shared memory twice (dot pass, gradient pass)
+// and from HBM once.
+template <typename XT, int KC, bool GRAD>
+__device__ __forceinline__ void consume_tile(const XT* xs, const double* ys,
+                                             int K, int lane, bool valid, const double (&breg)[KC],
+                                             double (&g)[KC], double& nll_acc) {
+  double v[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    const XT* xr = xs + r * K + lane;
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < KC; ++j) {
+      if (j < KC - 1 || lane + 32 * j < K) acc = fma(ld_x(xr + 32 * j), breg[j], acc);
+    }
+    v[r] = acc;
+  }
+  const double t = transpose_reduce32(v, lane);
+  // Force the gradient pass to re-read the tile from shared memory: without this the
+  // compiler keeps all 32*KC tile values of the dot pass live in registers and spills.
+  asm volatile("" ::: "memory");
+  double nll, w;
+  row_terms(t, ys[lane], nll, w);
+  nll_acc += valid ? nll : 0.0;
+  if (GRAD) {
+    w = valid ? w : 0.0;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const double wr = shfl_d(w, r);
+      const XT* xr = xs + r * K + lane;
+#pragma unroll
+      for (int j = 0; j < KC; ++j) {
+        if (j < KC - 1 || lane + 32 * j < K) g[j] = fma(wr, ld_x(xr + 32 * j), g[j]);
+      }
+    }
+  }
+}
+
+// Shared-memory carve-up of the streaming kernels.
+struct StreamSmem {
+  unsigned char* xs;  // [S][tile_bytes]
+  double* ys;         // [S][32]
+  uint64_t* full;     // [S]
+  uint64_t* empty;    // [S]
+  double* sbeta;      // [K]
+  double* wg;         // [nw][K]
+  double* wf;         // [nw]
+  int* flag;
+};
+
+__host__ __device__ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+__host__ __device__ inline size_t stream_smem_bytes(int K, int xsize, int S, int nw) {
+  size_t tile = size_t(kTileRows) * K * xsize;
+  size_t b = align_up(tile, 128) * S;
+  b += size_t(S) * 32 * sizeof(double);
+  b += size_t(2 * S) * sizeof(uint64_t);
+  b += align_up(size_t(K) * sizeof(double), 16);
+  b += size_t(nw) * K * sizeof(double);
+  b += align_up(size_t(nw) * sizeof(double), 16) + 16;
+  return b;
+}
+
+__device__ inline StreamSmem carve_stream_smem(unsigned char* base, int K, int xsize, int S, int nw) {
+  StreamSmem s;
+  size_t tile = align_up(size_t(kTileRows) * K * xsize, 128);
+  unsigned char* p = base;
+  s.xs = p;
+  p += tile * S;
+  s.ys = reinterpret_cast<double*>(p);
+  p += size_t(S) * 32 * sizeof(double);
+  s.full = reinterpret_cast<uint64_t*>(p);
+  p += size_t(S) * sizeof(uint64_t);
+  s.empty = reinterpret_cast<uint64_t*>(p);
+  p += size_t(S) * sizeof(uint64_t);
+  s.sbeta = reinterpret_cast<double*>(p);
+  p += align_up(size_t(K) * sizeof(double), 16);
+  s.wg = reinterpret_cast<double*>(p);
+  p += size_t(nw) * K * sizeof(double);
+  s.wf = reinterpret_cast<double*>(p);
+  p += align_up(size_t(nw) * sizeof(double), 16);
+  s.flag = reinterpret_cast<int*>(p);
+  return s;
+}
+
+// Producer/consumer ring over the tiles tile_begin, tile_begin+stride, ... < tile_end.
+// Warp 0 lane 0 issues TMA bulk copies; warps 1..NCW consume tiles round-robin.
+// Rows with global (padded) index >= row_limit are masked (padding).
+template <typename XT, int KC, bool GRAD, int NCW>
+__device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const double* __restrict__ y, int K,
+                                             int64_t tile_begin, int64_t tile_end, int64_t stride,
+                                             int64_t row_limit, int S, const StreamSmem& sm,
+                                             const double (&breg)[KC], double (&g)[KC], double& nll_acc,
+                                             bool evict_first) {
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t tile_elems = uint32_t(kTileRows) * K;
+  const uint32_t tile_bytes = tile_elems * sizeof(XT);
+  const size_t tile_pitch = align_up(tile_bytes, 128);
+  if (tile_begin >= tile_end) return;
+  const int64_t n_mine = (tile_end - tile_begin + stride - 1) / stride;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_first();
+      for (int64_t i = 0; i < n_mine; ++i) {
+        const int s = int(i % S);
+        const uint32_t n = uint32_t(i / S);
+        if (n > 0) mbar_wait(&sm.empty[s], (n - 1) & 1);
+        const int64_t tile = tile_begin + i * stride;
+        mbar_arrive_expect_tx(&sm.full[s], tile_bytes + 32 * sizeof(double));
+        const XT* src = X + tile * int64_t(tile_elems);
+        if (evict_first) {
+          bulk_g2s_hint(sm.xs + size_t(s) * tile_pitch, src, tile_bytes, &sm.full[s], pol);
+        } else {
+          bulk_g2s(sm.xs + size_t(s) * tile_pitch, src, tile_bytes, &sm.full[s]);
+        }
+        bulk_g2s(sm.ys + size_t(s) * 32, y + tile * kTileRows, 32 * sizeof(double), &sm.full[s]);
+      }
+    }
+    return;
+  }
+  const int cw = warp - 1;
+  for (int64_t i = cw; i < n_mine; i += NCW) {
+    const int s = int(i % S);
+    const uint32_t n = uint32_t(i / S);
+    mbar_wait(&sm.full[s], n & 1);
+    const int64_t tile = tile_begin + i * stride;
+    const bool valid = tile * kTileRows + lane < row_limit;
+    consume_tile<XT, KC, GRAD>(reinterpret_cast<const XT*>(sm.xs + size_t(s) * tile_pitch),
+                               sm.ys + size_t(s) * 32, K, lane, valid, breg, g, nll_acc);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[s]);
+  }
+}
+
+struct GlmArgs {
+  const void* X;
+  const double* y;
+  int64_t n_rows;
+  int64_t n_tiles;
+  int K;
+  int stages;
+  int with_prior;
+  int evict_first;
+  const double* prior_mu;     // device [K]
+  const double* prior_sigma;  // device [K]
+  double* partials;           // [grid][K+1]
+  unsigned int* counter;      // zero between launches
+  double* out;                // [K+1]  (f, g)
+  const double* beta_dev;     // wide kernel only
+};
+
+// Deterministic cross-CTA finish: CTA partial -> partials[blockIdx]; the last CTA to
+// arrive sums all partials in ascending CTA order (the reference's ascending-worker merge,
+// glm.py:243-250), adds the prior (sampler.py:55-58) and writes (f, g).
+__device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& sm, int nw, bool grad) {
+  const int K = a.K;
+  const int tid = threadIdx.x;
+  __syncthreads();
+  double* mine = a.partials + size_t(blockIdx.x) * (K + 1);
+  for (int c = tid; c <= K; c += blockDim.x) {
+    double acc = 0.0;
+    if (c == 0) {
+      for (int w = 0; w < nw; ++w) acc += sm.wf[w];
+    } else if (grad) {
+      for (int w = 0; w < nw; ++w) acc += sm.wg[size_t(w) * K + (c - 1)];
+    }
+    mine[c] = acc;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned t = atomicAdd(a.counter, 1u);
+    *sm.flag = (t == gridDim.x - 1) ? 1 : 0;
+  }
+  __syncthreads();
+  if (*sm.flag == 0) return;
+  __threadfence();
+  const int G = gridDim.x;
+  // column totals in fixed order (4 interleaved accumulators, combined pairwise)
+  for (int c = tid; c <= K; c += blockDim.x) {
+    if (c > 0 && !grad) break;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int b = 0;
+    for (; b + 4 <= G; b += 4) {
+      s0 += __ldcg(a.partials + size_t(b) * (K + 1) + c);
+      s1 += __ldcg(a.partials + size_t(b + 1) * (K + 1) + c);
+      s2 += __ldcg(a.partials + size_t(b + 2) * (K + 1) + c);
+      s3 += __ldcg(a.partials + size_t(b + 3) * (K + 1) + c);
+    }
+    for (; b < G; ++b) s0 += __ldcg(a.partials + size_t(b) * (K + 1) + c);
+    const double tot = (s0 + s1) + (s2 + s3);
+    if (c == 0) {
+      double f = -tot;
+      if (a.with_prior) {
+        for (int k = 0; k < K; ++k) {
+          const double z = (sm.sbeta[k] - a.prior_mu[k]) / a.prior_sigma[k];
+          f += -0.5 * z * z;
+        }
+      }
+      a.out[0] = f;
+    } else {
+      const int k = c - 1;
+      double gk = tot;
+      if (a.with_prior) {
+        const double sg = a.prior_sigma[k];
+        gk -= (sm.sbeta[k] - a.prior_mu[k]) / (sg * sg);
+      }
+      a.out[c] = gk;
+    }
+  }
+  if (tid == 0) *a.counter = 0u;  // re-arm for the next launch (kernel boundary orders it)
+}
+
+// K1 + K2: persistent fused single-pass kernel, one CTA per SM.
+template <typename XT, int KC, bool GRAD, int NCW>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1)
+    glm_stream_kernel(GlmArgs a, BetaPack<KC> beta) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int K = a.K;
+  const int S = a.stages;
+  const StreamSmem sm = carve_stream_smem(smem_raw, K, sizeof(XT), S, NCW);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  for (int k = threadIdx.x; k < K; k += blockDim.x) sm.sbeta[k] = beta.v[k];
+  __syncthreads();
+
+  double breg[KC], g[KC];
+#pragma unroll
+  for (int j = 0; j < KC; ++j) {
+    const int c = lane + 32 * j;
+    breg[j] = (c < K) ? beta.v[c] : 0.0;
+    g[j] = 0.0;
+  }
+  double nll = 0.0;
+  stream_tiles<XT, KC, GRAD, NCW>(static_cast<const XT*>(a.X), a.y, K, blockIdx.x, a.n_tiles, gridDim.x,
+                                  a.n_rows, S, sm, breg, g, nll, a.evict_first != 0);
+  if (warp > 0) {
+    const int cw = warp - 1;
+    const double wsum = warp_sum(nll);
+    if (lane == 0) sm.wf[cw] = -wsum;
+    if (GRAD) {
+#pragma unroll
+      for (int j = 0; j < KC; ++j) {
+        const int c = lane + 32 * j;
+        if (c < K) sm.wg[size_t(cw) * K + c] = g[j];
+      }
+    }
+  }
+  cta_reduce_finalize(a, sm, NCW, GRAD);
+}
+
+// Wide-K kernel (K > 256): one warp per row, lanes stride the columns, X read once from
+// HBM (the gradient pass re-reads the row from L1), per-warp gradient accumulators in smem.
+template <typename XT, bool GRAD>
+__global__ void __launch_bounds__(256) glm_wide_kernel(GlmArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int K = a.K;
+  const int nw = blockDim.x >> 5;
+  StreamSmem sm = carve_stream_smem(smem_raw, K, sizeof(XT), 0, nw);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) sm.sbeta[k] = a.beta_dev[k];
+  double* ga = sm.wg + size_t(warp) * K;
+  for (int k = lane; k < K; k += 32) ga[k] = 0.0;
+  __syncthreads();
+  const XT* X = static_cast<const XT*>(a.X);
+  double nll = 0.0;
+  const int64_t total_warps = int64_t(gridDim.x) * nw;
+  for (int64_t row = int64_t(blockIdx.x) * nw + warp; row < a.n_rows; row += total_warps) {
+    const XT* xr = X + row * K;
+    double acc = 0.0;
+    for (int k = lane; k < K; k += 32) acc = fma(ld_x(xr + k), sm.sbeta[k], acc);
+    const double t = warp_sum(acc);
+    double r_nll, w;
+    row_terms(t, __ldg(a.y + row), r_nll, w);
+    nll += r_nll;  // identical in every lane
+    if (GRAD) {
+      for (int k = lane; k < K; k += 32) ga[k] = fma(w, ld_x(xr + k), ga[k]);
+    }
+  }
+  if (lane == 0) sm.wf[warp] = -nll;
+  cta_reduce_finalize(a, sm, nw, GRAD);
+}
+
+}  // namespace pm

@@ -1,0 +1,599 @@
+// Red-black (checkerboard) Gibbs sweeps for Ising and q=4 Potts lattices.
+//
+// Reference semantics (ising.py):
+//   colour c = (i+j)%2; packed index = scan order within the colour          ising.py:101-131
+//   z = b + w * sum(neighbour spins), missing free-boundary neighbours = 0    ising.py:119-131,184
+//   s = +1 iff u < expit(z), u pre-assigned by packed index                   ising.py:158-172,185
+//   colour 0 against frozen colour 1, then colour 1                           ising.py:183-187
+// The host builds exact probability tables with the reference's arithmetic, so the device does
+// only integer neighbour sums and an exact compare (double compare, or the equivalent integer
+// compare word < ceil(p * 2^32) on the packed fast path).
+//
+// Layouts in HBM:
+//   W even : red-black packed, two int8 arrays [H][W/2]; colour c of row i sits at column
+//            j = 2q + ((i+c)&1).  A half-sweep reads the other colour and writes its own.
+//   W odd  : plain int8 grid [H][W] (colours are the parity of the flat index).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "philox.cuh"
+#include "pm_internal.cuh"
+
+using namespace pm;
+
+namespace {
+
+constexpr int kPottsIdx = 625;  // n0 + 5 n1 + 25 n2 + 125 n3, n_a in 0..4
+
+struct LatView {
+  int8_t* pk0;  // packed colour 0  (W even) or grid (W odd)
+  int8_t* pk1;  // packed colour 1  (W even)
+  int H, W, W2;
+  int packed;
+
+  __device__ __forceinline__ int8_t get(int i, int j) const {
+    if (packed) return ((i + j) & 1 ? pk1 : pk0)[int64_t(i) * W2 + (j >> 1)];
+    return pk0[int64_t(i) * W + j];
+  }
+  __device__ __forceinline__ void set(int i, int j, int8_t v) const {
+    if (packed)
+      ((i + j) & 1 ? pk1 : pk0)[int64_t(i) * W2 + (j >> 1)] = v;
+    else
+      pk0[int64_t(i) * W + j] = v;
+  }
+};
+
+struct GenericArgs {
+  LatView lat;
+  int periodic;
+  int model;            // PM_MODEL_*
+  int rng;              // PM_RNG_*
+  int colour;
+  int64_t n0;           // ceil(HW/2): sites of colour 0
+  int64_t n_c;          // sites of this colour
+  const int32_t* cls;   // [H*W] class per site, or null (class 0)
+  const double* ptab;   // Ising: [n_class][9] P(+1) for nsum = -4..4
+  const double* cdf;    // Potts: [625][3]
+  uint64_t key0, key1;
+  uint64_t base;        // numpy: stream index of this half-sweep's first deviate
+  uint64_t sweep;       // philox4x32: sweep number
+  const double* uni;    // uniforms of this half-sweep (n_c), PM_RNG_UNIFORMS
+};
+
+__device__ __forceinline__ double uniform_for(const GenericArgs& a, int64_t p) {
+  if (a.rng == PM_RNG_UNIFORMS) return a.uni[p];
+  if (a.rng == PM_RNG_NUMPY_PHILOX) {
+    const uint64_t w = numpy_philox_word(a.base + uint64_t(p), a.key0, a.key1);
+    return double(w >> 11) * 0x1p-53;
+  }
+  const uint64_t s = uint64_t(a.colour) * uint64_t(a.n0) + uint64_t(p);
+  const U32x4 blk = site_philox_block(s >> 2, a.sweep, a.key0);
+  return double(blk.v[s & 3]) * 0x1p-32;
+}
+
+// One thread per site of colour c, any shape / boundary / model / RNG mode.
+__global__ void __launch_bounds__(256) gibbs_generic_kernel(GenericArgs a) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int H = a.lat.H, W = a.lat.W;
+  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < a.n_c; p += stride) {
+    int i, j;
+    if ((W & 1) == 0) {
+      const int W2 = W >> 1;
+      i = int(p / W2);
+      j = 2 * int(p % W2) + ((i + a.colour) & 1);
+    } else {
+      const int64_t f = 2 * p + a.colour;
+      i = int(f / W);
+      j = int(f % W);
+    }
+    const int di[4] = {-1, 1, 0, 0};
+    const int dj[4] = {0, 0, -1, 1};
+    int nsum = 0, pidx = 0;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      int ni = i + di[d], nj = j + dj[d];
+      if (a.periodic) {
+        ni = (ni + H) % H;
+        nj = (nj + W) % W;
+      } else if (ni < 0 || ni >= H || nj < 0 || nj >= W) {
+        continue;  // free boundary: sentinel 0 (ising.py:121-131)
+      }
+      const int v = a.lat.get(ni, nj);
+      if (a.model == PM_MODEL_ISING) {
+        nsum += v;
+      } else {
+        pidx += (v == 0) ? 1 : (v == 1) ? 5 : (v == 2) ? 25 : 125;
+      }
+    }
+    const double u = uniform_for(a, p);
+    int8_t ns;
+    if (a.model == PM_MODEL_ISING) {
+      const int cl = a.cls ? a.cls[int64_t(i) * W + j] : 0;
+      const double pp = a.ptab[cl * 9 + nsum + 4];
+      ns = (u < pp) ? int8_t(1) : int8_t(-1);
+    } else {
+      const double* c3 = a.cdf + pidx * 3;
+      ns = int8_t((u >= c3[0]) + (u >= c3[1]) + (u >= c3[2]));
+    }
+    a.lat.set(i, j, ns);
+  }
+}
+
+// ---------------------------------------------------------------- packed fast path
+// Periodic, even H and W, W/2 % 16 == 0, uniform bias, Philox4x32 (seed, sweep, site).
+// Thread = 16 consecutive packed sites of one row: 3 x 16-byte loads of the other colour
+// (rows i-1, i, i+1) + 2 edge bytes, 4 Philox4x32 blocks, one 16-byte store.
+struct PackedArgs {
+  const int8_t* other;
+  int8_t* mine;
+  int H, W2;
+  int colour;
+  int64_t n0;
+  uint64_t sweep;
+  uint64_t seed;
+  unsigned long long thr[9];  // Ising: ceil(P(+1 | nsum) * 2^32), nsum = -4..4
+};
+
+__device__ __forceinline__ void load16(const int8_t* p, int8_t (&b)[16]) {
+  const int4 v = __ldg(reinterpret_cast<const int4*>(p));
+  memcpy(b, &v, 16);
+}
+
+template <int MODEL>
+__global__ void __launch_bounds__(256) gibbs_packed_kernel(PackedArgs a, const unsigned long long* __restrict__ pthr) {
+  __shared__ unsigned long long s_thr[MODEL == PM_MODEL_ISING ? 9 : kPottsIdx * 3];
+  if (MODEL == PM_MODEL_ISING) {
+    if (threadIdx.x < 9) s_thr[threadIdx.x] = a.thr[threadIdx.x];
+  } else {
+    for (int t = threadIdx.x; t < kPottsIdx * 3; t += blockDim.x) s_thr[t] = pthr[t];
+  }
+  __syncthreads();
+  const int per_row = a.W2 >> 4;
+  const int64_t gt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (gt >= int64_t(a.H) * per_row) return;
+  const int i = int(gt / per_row);
+  const int q0 = int(gt % per_row) << 4;
+  const int iu = (i == 0) ? a.H - 1 : i - 1;
+  const int id = (i == a.H - 1) ? 0 : i + 1;
+  int8_t up[16], dn[16], mid[16];
+  load16(a.other + int64_t(iu) * a.W2 + q0, up);
+  load16(a.other + int64_t(id) * a.W2 + q0, dn);
+  load16(a.other + int64_t(i) * a.W2 + q0, mid);
+  const int o = (i + a.colour) & 1;
+  // o = 0: horizontal neighbours are packed q-1 and q; o = 1: q and q+1
+  const int8_t edge = o ? __ldg(a.other + int64_t(i) * a.W2 + ((q0 + 16 == a.W2) ? 0 : q0 + 16))
+                        : __ldg(a.other + int64_t(i) * a.W2 + ((q0 == 0) ? a.W2 - 1 : q0 - 1));
+  const uint64_t s0 = uint64_t(a.colour) * uint64_t(a.n0) + uint64_t(i) * a.W2 + q0;
+  int8_t res[16];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const U32x4 blk = site_philox_block((s0 >> 2) + g, a.sweep, a.seed);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int q = 4 * g + t;
+      int8_t l, r;
+      if (o == 0) {
+        l = (q == 0) ? edge : mid[q - 1];
+        r = mid[q];
+      } else {
+        l = mid[q];
+        r = (q == 15) ? edge : mid[q + 1];
+      }
+      const uint32_t w = blk.v[t];
+      if (MODEL == PM_MODEL_ISING) {
+        const int nsum = up[q] + dn[q] + l + r;
+        res[q] = (uint64_t(w) < s_thr[nsum + 4]) ? int8_t(1) : int8_t(-1);
+      } else {
+        const int pw[4] = {1, 5, 25, 125};
+        const int idx = pw[up[q]] + pw[dn[q]] + pw[l] + pw[r];
+        const unsigned long long* t3 = s_thr + idx * 3;
+        res[q] = int8_t((w >= t3[0]) + (w >= t3[1]) + (w >= t3[2]));
+      }
+    }
+  }
+  int4 outv;
+  memcpy(&outv, res, 16);
+  *reinterpret_cast<int4*>(a.mine + int64_t(i) * a.W2 + q0) = outv;
+}
+
+// ---------------------------------------------------------------- layout conversion
+__global__ void pack_kernel(const int8_t* __restrict__ grid, int H, int W, int8_t* pk0, int8_t* pk1) {
+  const int64_t n = int64_t(H) * W;
+  for (int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < n; f += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(f / W), j = int(f % W);
+    ((i + j) & 1 ? pk1 : pk0)[int64_t(i) * (W >> 1) + (j >> 1)] = grid[f];
+  }
+}
+__global__ void unpack_kernel(int8_t* __restrict__ grid, int H, int W, const int8_t* pk0, const int8_t* pk1) {
+  const int64_t n = int64_t(H) * W;
+  for (int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < n; f += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(f / W), j = int(f % W);
+    grid[f] = ((i + j) & 1 ? pk1 : pk0)[int64_t(i) * (W >> 1) + (j >> 1)];
+  }
+}
+
+// ---------------------------------------------------------------- host tables
+// P(+1) = expit(b + w*nsum) with the reference's two roundings (ising.py:184: numpy computes
+// w*nsum, then adds b) and scipy's expit 1/(1+exp(-z)).  Compiled with -ffp-contract=off.
+void ising_probs(double w, double b, double* p) {
+  for (int n = -4; n <= 4; ++n) {
+    volatile double wn = w * double(n);
+    volatile double z = b + wn;
+    p[n + 4] = 1.0 / (1.0 + std::exp(-z));
+  }
+}
+
+void potts_cdf(double coupling, double* cdf) {
+  for (int idx = 0; idx < kPottsIdx; ++idx) {
+    int n[4] = {idx % 5, (idx / 5) % 5, (idx / 25) % 5, (idx / 125) % 5};
+    double e[4];
+    for (int a = 0; a < 4; ++a) {
+      volatile double x = coupling * double(n[a]);
+      e[a] = std::exp(x);
+    }
+    volatile double s0 = e[0];
+    volatile double s1 = s0 + e[1];
+    volatile double s2 = s1 + e[2];
+    volatile double z = s2 + e[3];
+    cdf[idx * 3 + 0] = s0 / z;
+    cdf[idx * 3 + 1] = s1 / z;
+    cdf[idx * 3 + 2] = s2 / z;
+  }
+}
+
+// u = w * 2^-32 < p  <=>  w < ceil(p * 2^32)   (p * 2^32 is exact; w integer)
+unsigned long long thr32(double p) {
+  const double t = std::ceil(p * 4294967296.0);
+  if (t <= 0.0) return 0ull;
+  if (t >= 4294967296.0) return 4294967296ull;
+  return (unsigned long long)t;
+}
+
+}  // namespace
+
+struct pm_lat_s {
+  int device = 0;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  int H = 0, W = 0, boundary = 0, model = 0;
+  int packed = 0;
+  int8_t* pk0 = nullptr;
+  int8_t* pk1 = nullptr;
+  int8_t* scratch = nullptr;  // H*W staging for set/get
+  // Ising
+  bool has_field = false;
+  double w = 0.0;
+  int n_class = 0;
+  int32_t* cls = nullptr;
+  double* ptab = nullptr;
+  unsigned long long thr[9] = {0};
+  // Potts
+  bool has_potts = false;
+  double* cdf = nullptr;
+  unsigned long long* pthr = nullptr;
+  // uniforms staging
+  double* uni = nullptr;
+  size_t uni_cap = 0;
+};
+
+namespace {
+
+void free_lat(pm_lat_s* h) {
+  for (void* p : {(void*)h->pk0, (void*)h->pk1, (void*)h->scratch, (void*)h->cls, (void*)h->ptab, (void*)h->cdf,
+                  (void*)h->pthr, (void*)h->uni})
+    if (p) cudaFree(p);
+  h->pk0 = h->pk1 = h->scratch = nullptr;
+  h->cls = nullptr;
+  h->ptab = h->cdf = h->uni = nullptr;
+  h->pthr = nullptr;
+  h->uni_cap = 0;
+}
+
+LatView view_of(pm_lat_s* h) {
+  LatView v;
+  v.pk0 = h->pk0;
+  v.pk1 = h->pk1;
+  v.H = h->H;
+  v.W = h->W;
+  v.W2 = h->W / 2;
+  v.packed = h->packed;
+  return v;
+}
+
+bool fast_path_ok(pm_lat_s* h) {
+  return h->packed && h->boundary == PM_BOUNDARY_PERIODIC && (h->H % 2 == 0) && ((h->W / 2) % 16 == 0) &&
+         (h->model == PM_MODEL_POTTS4 || h->n_class == 1);
+}
+
+int grid_for(pm_lat_s* h, int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(int64_t(h->sms) * 16, (n + 255) / 256));
+}
+
+}  // namespace
+
+extern "C" {
+
+int pm_ising_prob_table(double w, double b, double* p_out) {
+  if (!p_out) return fail(PM_EINVAL, "null output");
+  ising_probs(w, b, p_out);
+  return PM_OK;
+}
+
+int pm_potts_cdf_table(double coupling, double* cdf_out) {
+  if (!cdf_out) return fail(PM_EINVAL, "null output");
+  potts_cdf(coupling, cdf_out);
+  return PM_OK;
+}
+
+int pm_lat_create(int device, int32_t H, int32_t W, int boundary, int model, pm_lat_t* out) {
+  if (!out) return fail(PM_EINVAL, "null output");
+  if (H < 1 || W < 1) return fail(PM_EINVAL, "spin grid must be non-empty 2-D");
+  if (boundary != PM_BOUNDARY_FREE && boundary != PM_BOUNDARY_PERIODIC) return fail(PM_EINVAL, "bad boundary");
+  if (model != PM_MODEL_ISING && model != PM_MODEL_POTTS4) return fail(PM_EINVAL, "bad model");
+  if (boundary == PM_BOUNDARY_PERIODIC && ((H % 2) || (W % 2)))
+    return fail(PM_EINVAL, "periodic checkerboard needs even height and width");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (device < 0 || device >= n) return fail(PM_ERANGE, "device index out of range");
+  pm_lat_s* h = new pm_lat_s();
+  h->device = device;
+  h->H = H;
+  h->W = W;
+  h->boundary = boundary;
+  h->model = model;
+  h->packed = (W % 2 == 0) ? 1 : 0;
+  DeviceGuard g(device);
+  h->sms = sm_count(device);
+  const size_t n_sites = size_t(H) * W;
+  e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) {
+    if (h->packed) {
+      e = cudaMalloc(&h->pk0, n_sites / 2 + 16);
+      if (e == cudaSuccess) e = cudaMalloc(&h->pk1, n_sites / 2 + 16);
+    } else {
+      e = cudaMalloc(&h->pk0, n_sites + 16);
+    }
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&h->scratch, n_sites + 16);
+  if (e != cudaSuccess) {
+    free_lat(h);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return cuda_fail(e, "pm_lat_create");
+  }
+  *out = h;
+  return PM_OK;
+}
+
+int pm_lat_destroy(pm_lat_t h) {
+  if (!h) return PM_OK;
+  {
+    std::lock_guard<std::mutex> lk(h->mu);
+    DeviceGuard g(h->device);
+    cudaStreamSynchronize(h->stream);
+    free_lat(h);
+    cudaStreamDestroy(h->stream);
+  }
+  delete h;
+  return PM_OK;
+}
+
+int pm_lat_set_spins(pm_lat_t h, const int8_t* s) {
+  if (!h || !s) return fail(PM_EINVAL, "null argument");
+  const int64_t n = int64_t(h->H) * h->W;
+  for (int64_t f = 0; f < n; ++f) {
+    if (h->model == PM_MODEL_ISING ? !(s[f] == 1 || s[f] == -1) : !(s[f] >= 0 && s[f] <= 3))
+      return fail(PM_EINVAL, h->model == PM_MODEL_ISING ? "spins must be -1 or +1" : "Potts states must be 0..3");
+  }
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  if (h->packed) {
+    PM_CUDA(cudaMemcpyAsync(h->scratch, s, n, cudaMemcpyHostToDevice, h->stream));
+    pack_kernel<<<grid_for(h, n), 256, 0, h->stream>>>(h->scratch, h->H, h->W, h->pk0, h->pk1);
+    PM_CUDA(cudaGetLastError());
+  } else {
+    PM_CUDA(cudaMemcpyAsync(h->pk0, s, n, cudaMemcpyHostToDevice, h->stream));
+  }
+  PM_CUDA(cudaStreamSynchronize(h->stream));
+  return PM_OK;
+}
+
+int pm_lat_get_spins(pm_lat_t h, int8_t* s) {
+  if (!h || !s) return fail(PM_EINVAL, "null argument");
+  const int64_t n = int64_t(h->H) * h->W;
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  if (h->packed) {
+    unpack_kernel<<<grid_for(h, n), 256, 0, h->stream>>>(h->scratch, h->H, h->W, h->pk0, h->pk1);
+    PM_CUDA(cudaGetLastError());
+    PM_CUDA(cudaMemcpyAsync(s, h->scratch, n, cudaMemcpyDeviceToHost, h->stream));
+  } else {
+    PM_CUDA(cudaMemcpyAsync(s, h->pk0, n, cudaMemcpyDeviceToHost, h->stream));
+  }
+  PM_CUDA(cudaStreamSynchronize(h->stream));
+  return PM_OK;
+}
+
+int pm_lat_set_ising(pm_lat_t h, double w, const double* bias) {
+  if (!h) return fail(PM_EINVAL, "null handle");
+  if (h->model != PM_MODEL_ISING) return fail(PM_ESTATE, "lattice is not an Ising model");
+  if (!std::isfinite(w)) return fail(PM_EINVAL, "bias and coupling must be finite");
+  const int64_t n = int64_t(h->H) * h->W;
+  std::vector<double> uniq;
+  std::vector<int32_t> cls;
+  if (bias) {
+    for (int64_t f = 0; f < n; ++f)
+      if (!std::isfinite(bias[f])) return fail(PM_EINVAL, "bias and coupling must be finite");
+    uniq.assign(bias, bias + n);
+    std::sort(uniq.begin(), uniq.end());
+    // -0.0 and +0.0 merge: both give the same z and the same expit
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    if (uniq.size() > 1) {
+      cls.resize(n);
+      for (int64_t f = 0; f < n; ++f)
+        cls[f] = int32_t(std::lower_bound(uniq.begin(), uniq.end(), bias[f]) - uniq.begin());
+    }
+  } else {
+    uniq.push_back(0.0);
+  }
+  std::vector<double> tab(uniq.size() * 9);
+  for (size_t c = 0; c < uniq.size(); ++c) ising_probs(w, uniq[c], tab.data() + 9 * c);
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  cudaStreamSynchronize(h->stream);
+  if (h->cls) cudaFree(h->cls);
+  if (h->ptab) cudaFree(h->ptab);
+  h->cls = nullptr;
+  h->ptab = nullptr;
+  PM_CUDA(cudaMalloc(&h->ptab, sizeof(double) * tab.size()));
+  PM_CUDA(cudaMemcpy(h->ptab, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice));
+  if (!cls.empty()) {
+    PM_CUDA(cudaMalloc(&h->cls, sizeof(int32_t) * n));
+    PM_CUDA(cudaMemcpy(h->cls, cls.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  }
+  h->n_class = int(cls.empty() ? 1 : uniq.size());
+  h->w = w;
+  for (int t = 0; t < 9; ++t) h->thr[t] = thr32(tab[t]);
+  h->has_field = true;
+  return PM_OK;
+}
+
+int pm_lat_set_potts(pm_lat_t h, double coupling) {
+  if (!h) return fail(PM_EINVAL, "null handle");
+  if (h->model != PM_MODEL_POTTS4) return fail(PM_ESTATE, "lattice is not a Potts model");
+  if (!std::isfinite(coupling)) return fail(PM_EINVAL, "coupling must be finite");
+  std::vector<double> cdf(kPottsIdx * 3);
+  potts_cdf(coupling, cdf.data());
+  std::vector<unsigned long long> thr(kPottsIdx * 3);
+  for (int t = 0; t < kPottsIdx * 3; ++t) thr[t] = thr32(cdf[t]);
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  cudaStreamSynchronize(h->stream);
+  if (!h->cdf) PM_CUDA(cudaMalloc(&h->cdf, sizeof(double) * kPottsIdx * 3));
+  if (!h->pthr) PM_CUDA(cudaMalloc(&h->pthr, sizeof(unsigned long long) * kPottsIdx * 3));
+  PM_CUDA(cudaMemcpy(h->cdf, cdf.data(), sizeof(double) * kPottsIdx * 3, cudaMemcpyHostToDevice));
+  PM_CUDA(cudaMemcpy(h->pthr, thr.data(), sizeof(unsigned long long) * kPottsIdx * 3, cudaMemcpyHostToDevice));
+  h->has_potts = true;
+  return PM_OK;
+}
+
+static int lat_sweeps_impl(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t key0, uint64_t key1,
+                           uint64_t stream_pos, const double* uniforms, float* total_ms);
+
+int pm_lat_sweeps(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t key0, uint64_t key1, uint64_t stream_pos,
+                  const double* uniforms) {
+  return lat_sweeps_impl(h, n_sweeps, rng_mode, key0, key1, stream_pos, uniforms, nullptr);
+}
+
+int pm_lat_time_sweeps(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t key0, uint64_t key1,
+                       uint64_t stream_pos, float* total_ms) {
+  if (!total_ms) return fail(PM_EINVAL, "null argument");
+  if (rng_mode == PM_RNG_UNIFORMS) return fail(PM_EINVAL, "timing needs an in-kernel RNG mode");
+  return lat_sweeps_impl(h, n_sweeps, rng_mode, key0, key1, stream_pos, nullptr, total_ms);
+}
+
+static int lat_sweeps_impl(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t key0, uint64_t key1,
+                           uint64_t stream_pos, const double* uniforms, float* total_ms) {
+  if (!h) return fail(PM_EINVAL, "null handle");
+  if (n_sweeps < 0) return fail(PM_EINVAL, "n_sweeps must be >= 0");
+  if (rng_mode != PM_RNG_UNIFORMS && rng_mode != PM_RNG_NUMPY_PHILOX && rng_mode != PM_RNG_PHILOX4X32)
+    return fail(PM_EINVAL, "bad rng mode");
+  if (rng_mode == PM_RNG_UNIFORMS && !uniforms && n_sweeps > 0) return fail(PM_EINVAL, "uniforms required");
+  if (h->model == PM_MODEL_ISING && !h->has_field) return fail(PM_ESTATE, "call pm_lat_set_ising first");
+  if (h->model == PM_MODEL_POTTS4 && !h->has_potts) return fail(PM_ESTATE, "call pm_lat_set_potts first");
+  if (n_sweeps == 0) return PM_OK;
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  const int64_t HW = int64_t(h->H) * h->W;
+  const int64_t n0 = (HW + 1) / 2, n1 = HW / 2;
+  if (rng_mode == PM_RNG_UNIFORMS) {
+    const size_t need = size_t(n_sweeps) * HW;
+    if (need > h->uni_cap) {
+      if (h->uni) cudaFree(h->uni);
+      h->uni = nullptr;
+      h->uni_cap = 0;
+      PM_CUDA(cudaMalloc(&h->uni, sizeof(double) * need));
+      h->uni_cap = need;
+    }
+    PM_CUDA(cudaMemcpyAsync(h->uni, uniforms, sizeof(double) * need, cudaMemcpyHostToDevice, h->stream));
+  }
+  const bool fast = rng_mode == PM_RNG_PHILOX4X32 && fast_path_ok(h);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (total_ms) {
+    PM_CUDA(cudaEventCreate(&e0));
+    PM_CUDA(cudaEventCreate(&e1));
+    PM_CUDA(cudaEventRecord(e0, h->stream));
+  }
+  for (int t = 0; t < n_sweeps; ++t) {
+    for (int c = 0; c < 2; ++c) {
+      const int64_t nc = c == 0 ? n0 : n1;
+      if (nc == 0) continue;
+      if (fast) {
+        PackedArgs pa;
+        pa.other = c == 0 ? h->pk1 : h->pk0;
+        pa.mine = c == 0 ? h->pk0 : h->pk1;
+        pa.H = h->H;
+        pa.W2 = h->W / 2;
+        pa.colour = c;
+        pa.n0 = n0;
+        pa.sweep = stream_pos + uint64_t(t);
+        pa.seed = key0;
+        for (int k = 0; k < 9; ++k) pa.thr[k] = h->thr[k];
+        const int64_t threads = int64_t(h->H) * (h->W / 2 / 16);
+        const int blocks = int((threads + 255) / 256);
+        if (h->model == PM_MODEL_ISING)
+          gibbs_packed_kernel<PM_MODEL_ISING><<<blocks, 256, 0, h->stream>>>(pa, nullptr);
+        else
+          gibbs_packed_kernel<PM_MODEL_POTTS4><<<blocks, 256, 0, h->stream>>>(pa, h->pthr);
+      } else {
+        GenericArgs a;
+        a.lat = view_of(h);
+        a.periodic = h->boundary == PM_BOUNDARY_PERIODIC;
+        a.model = h->model;
+        a.rng = rng_mode;
+        a.colour = c;
+        a.n0 = n0;
+        a.n_c = nc;
+        a.cls = h->cls;
+        a.ptab = h->ptab;
+        a.cdf = h->cdf;
+        a.key0 = key0;
+        a.key1 = key1;
+        a.base = stream_pos + uint64_t(t) * HW + (c == 0 ? 0 : n0);
+        a.sweep = stream_pos + uint64_t(t);
+        a.uni = rng_mode == PM_RNG_UNIFORMS ? h->uni + size_t(t) * HW + (c == 0 ? 0 : n0) : nullptr;
+        gibbs_generic_kernel<<<grid_for(h, nc), 256, 0, h->stream>>>(a);
+      }
+      PM_CUDA(cudaGetLastError());
+    }
+  }
+  if (total_ms) {
+    PM_CUDA(cudaEventRecord(e1, h->stream));
+    PM_CUDA(cudaEventSynchronize(e1));
+    PM_CUDA(cudaEventElapsedTime(total_ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  PM_CUDA(cudaStreamSynchronize(h->stream));
+  return PM_OK;
+}
+
+int pm_lat_stream(pm_lat_t h, void** stream) {
+  if (!h || !stream) return fail(PM_EINVAL, "null argument");
+  *stream = h->stream;
+  return PM_OK;
+}
+
+int pm_lat_packed(pm_lat_t h, int* packed) {
+  if (!h || !packed) return fail(PM_EINVAL, "null argument");
+  *packed = fast_path_ok(h) ? 1 : 0;
+  return PM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,290 @@
+"""Checkerboard Gibbs sampling of Ising and q=4 Potts lattices on B200.
+
+Mirror of the reference `parmcmc.ising` sweep path (ising.py:47-187):
+`IsingLattice`, `ColorPartition`/`color_lattice`, `conditional_prob` and
+`gibbs_sweep(lat, part, rng_buffer, plan)` keep their signatures and semantics:
+
+    P(s_i = +1 | rest) = expit(z_i),  z_i = b_i + w * sum_j s_j        (ising.py:11-16)
+
+colour 0 ((i+j) even) updates against frozen colour 1, then colour 1, with the
+uniform of each site pre-assigned by its packed (scan-order) index
+(ising.py:175-187).  The sweep runs on the device (include/pmb200.h pm_lat_*);
+`ColorPartition` owns the device-resident lattice state, as the reference's
+partition owns the packed spin arrays between sweeps (ising.py:101-150).
+
+Uniform sources (the `rng_buffer` argument is duck-typed as in the reference):
+  * a DeviateBuffer (this package's or the reference's, UNIFORM01): the numpy
+    Philox4x64 stream is generated on the device at the buffer's position and
+    the buffer is advanced -> bit-exact with the reference sweep;
+  * a SitePhilox: Philox4x32-10 keyed by (seed, sweep, site) (BASELINE c4);
+  * anything else with `.take(n)`: the uniforms are drawn on the host in the
+    reference's order and shipped to the device.
+Extensions beyond the reference: periodic boundaries and the Potts q=4 model.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+from scipy.special import expit
+
+from . import _lib
+from .rng import BufferKind, DeviateBuffer, SitePhilox, philox_key_of
+
+__all__ = [
+    "IsingLattice", "PottsLattice", "ColorPartition", "conditional_prob", "color_lattice",
+    "gibbs_sweep", "gibbs_sweeps", "potts_sweeps", "ising_prob_table", "potts_cdf_table",
+]
+
+
+def conditional_prob(z):
+    """P(s_i = +1) = 1/(1+exp(-z)), overflow-safe; scalar or array (ising.py:96-98)."""
+    return expit(z)
+
+
+class IsingLattice:
+    """Spin grid (int8 +-1), bias grid and uniform coupling (ising.py:47-93).
+
+    `boundary` ("free" as the reference, or "periodic") is an extension.
+    """
+
+    def __init__(self, s, b, w: float, boundary: str = "free"):
+        s = np.asarray(s)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        if s.ndim != 2 or s.size == 0:
+            raise ValueError(f"spin grid must be non-empty 2-D, got shape {s.shape}")
+        if b.shape != s.shape:
+            raise ValueError(f"bias shape {b.shape} != spin shape {s.shape}")
+        if not np.isin(s, (-1, 1)).all():
+            raise ValueError("spins must be -1 or +1")
+        if not np.isfinite(b).all() or not np.isfinite(w):
+            raise ValueError("bias and coupling must be finite")
+        if boundary not in ("free", "periodic"):
+            raise ValueError("boundary must be 'free' or 'periodic'")
+        if boundary == "periodic" and (s.shape[0] % 2 or s.shape[1] % 2):
+            raise ValueError("periodic checkerboard needs even height and width")
+        self.s = s.astype(np.int8)
+        self.b = b
+        self.w = float(w)
+        self.boundary = boundary
+
+    @property
+    def height(self) -> int:
+        return self.s.shape[0]
+
+    @property
+    def width(self) -> int:
+        return self.s.shape[1]
+
+    @classmethod
+    def from_image(cls, image01, w: float, bias_scale: float) -> "IsingLattice":
+        """{0,1} pixels -> {-1,+1} spins; bias = bias_scale * observed spin (ising.py:73-82)."""
+        image01 = np.asarray(image01)
+        if image01.size == 0:
+            raise ValueError("empty image")
+        if not np.isin(image01, (0, 1)).all():
+            raise ValueError("image entries must be 0 or 1")
+        spins = 2 * image01.astype(np.int8) - 1
+        return cls(spins, bias_scale * spins.astype(np.float64), w)
+
+
+class PottsLattice:
+    """q=4 Potts lattice: states 0..3, P(a | rest) proportional to exp(coupling * n_a)."""
+
+    def __init__(self, s, coupling: float, boundary: str = "periodic"):
+        s = np.asarray(s)
+        if s.ndim != 2 or s.size == 0:
+            raise ValueError(f"state grid must be non-empty 2-D, got shape {s.shape}")
+        if not np.isin(s, (0, 1, 2, 3)).all():
+            raise ValueError("Potts states must be 0..3")
+        if not np.isfinite(coupling):
+            raise ValueError("coupling must be finite")
+        if boundary not in ("free", "periodic"):
+            raise ValueError("boundary must be 'free' or 'periodic'")
+        if boundary == "periodic" and (s.shape[0] % 2 or s.shape[1] % 2):
+            raise ValueError("periodic checkerboard needs even height and width")
+        self.s = s.astype(np.int8)
+        self.coupling = float(coupling)
+        self.boundary = boundary
+
+    @property
+    def height(self) -> int:
+        return self.s.shape[0]
+
+    @property
+    def width(self) -> int:
+        return self.s.shape[1]
+
+
+class LatticeDevice:
+    """A pm_lat_t handle: the device-resident lattice state."""
+
+    def __init__(self, height: int, width: int, boundary: str, model: int, device: int = 0):
+        lib = _lib.load()
+        _lib.require_device(device)
+        h = ctypes.c_void_p()
+        bnd = _lib.PM_BOUNDARY_PERIODIC if boundary == "periodic" else _lib.PM_BOUNDARY_FREE
+        _lib.check(lib.pm_lat_create(device, int(height), int(width), bnd, model, ctypes.byref(h)),
+                   "pm_lat_create")
+        self._h = h
+        self.height, self.width, self.model = height, width, model
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_spins(self, s: np.ndarray) -> None:
+        s = np.ascontiguousarray(s, dtype=np.int8)
+        _lib.call("pm_lat_set_spins", self._h, _lib.i8ptr(s))
+
+    def get_spins(self) -> np.ndarray:
+        out = np.empty((self.height, self.width), dtype=np.int8)
+        _lib.call("pm_lat_get_spins", self._h, _lib.i8ptr(out))
+        return out
+
+    def stream(self) -> int:
+        p = ctypes.c_void_p()
+        _lib.call("pm_lat_stream", self._h, ctypes.byref(p))
+        return p.value or 0
+
+    def fast_path(self) -> bool:
+        v = ctypes.c_int()
+        _lib.call("pm_lat_packed", self._h, ctypes.byref(v))
+        return bool(v.value)
+
+    def sweeps(self, n: int, mode: int, key0: int = 0, key1: int = 0, pos: int = 0, uniforms=None) -> None:
+        u = None if uniforms is None else np.ascontiguousarray(uniforms, dtype=np.float64)
+        _lib.call("pm_lat_sweeps", self._h, int(n), int(mode), ctypes.c_uint64(key0),
+                  ctypes.c_uint64(key1), ctypes.c_uint64(pos), _lib.dptr(u))
+
+    def time_sweeps(self, n: int, mode: int, key0: int = 0, key1: int = 0, pos: int = 0) -> float:
+        """Device milliseconds of n sweeps with an in-kernel RNG (CUDA events, handle stream)."""
+        ms = ctypes.c_float()
+        _lib.call("pm_lat_time_sweeps", self._h, int(n), int(mode), ctypes.c_uint64(key0),
+                  ctypes.c_uint64(key1), ctypes.c_uint64(pos), ctypes.byref(ms))
+        return float(ms.value)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.load().pm_lat_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class ColorPartition:
+    """Checkerboard split (ising.py:101-150) owning the device-resident state.
+
+    colors[c] are the flat indices of colour c in scan order (the packed order);
+    the spins live on the device between sweeps and are unpacked into the
+    lattice after every sweep call, as the reference's unpack_into does.
+    """
+
+    def __init__(self, lat, device: int = 0):
+        h, w = lat.height, lat.width
+        flat_color = (np.add.outer(np.arange(h), np.arange(w)) % 2).ravel()
+        self.colors = [np.flatnonzero(flat_color == c) for c in (0, 1)]
+        model = _lib.PM_MODEL_POTTS4 if isinstance(lat, PottsLattice) else _lib.PM_MODEL_ISING
+        self.device = LatticeDevice(h, w, lat.boundary, model, device)
+        if model == _lib.PM_MODEL_ISING:
+            b = np.ascontiguousarray(lat.b, dtype=np.float64)
+            uniform_b = bool(np.all(b == b.flat[0]))
+            if uniform_b and b.flat[0] == 0.0:
+                _lib.call("pm_lat_set_ising", self.device.handle, float(lat.w), None)
+            else:
+                _lib.call("pm_lat_set_ising", self.device.handle, float(lat.w), _lib.dptr(b.ravel()))
+        else:
+            _lib.call("pm_lat_set_potts", self.device.handle, float(lat.coupling))
+        self.pack_from(lat)
+
+    @property
+    def n_sites(self) -> int:
+        return self.colors[0].size + self.colors[1].size
+
+    def pack_from(self, lat) -> None:
+        self.device.set_spins(lat.s)
+
+    def unpack_into(self, lat) -> None:
+        lat.s[...] = self.device.get_spins()
+
+
+def color_lattice(lat, device: int = 0) -> ColorPartition:
+    """Build the checkerboard partition and upload the lattice (ising.py:153-155)."""
+    return ColorPartition(lat, device)
+
+
+def _run(lat, part: ColorPartition, rng_buffer, n_sweeps: int) -> None:
+    if n_sweeps < 1:
+        return
+    n0, n1 = part.colors[0].size, part.colors[1].size
+    consumed = n_sweeps * (n0 + n1)
+    dev = part.device
+    if isinstance(rng_buffer, SitePhilox):
+        dev.sweeps(n_sweeps, _lib.PM_RNG_PHILOX4X32, rng_buffer.seed, 0, rng_buffer.sweep)
+        rng_buffer.advance(n_sweeps)
+    elif isinstance(rng_buffer, DeviateBuffer) and rng_buffer.kind is BufferKind.UNIFORM01:
+        k0, k1 = rng_buffer.stream_key()
+        dev.sweeps(n_sweeps, _lib.PM_RNG_NUMPY_PHILOX, k0, k1, rng_buffer.position)
+        rng_buffer.skip(consumed)
+    elif _is_reference_uniform_buffer(rng_buffer):
+        # the reference's own DeviateBuffer: same stream; generate on the device, then advance
+        k0, k1 = philox_key_of(rng_buffer._gen)
+        pos = _reference_position(rng_buffer)
+        dev.sweeps(n_sweeps, _lib.PM_RNG_NUMPY_PHILOX, k0, k1, pos)
+        rng_buffer.take(consumed)
+    else:
+        u = np.concatenate([np.asarray(rng_buffer.take(n), dtype=np.float64)
+                            for _ in range(n_sweeps) for n in (n0, n1)])
+        dev.sweeps(n_sweeps, _lib.PM_RNG_UNIFORMS, uniforms=u)
+    part.unpack_into(lat)
+
+
+def _is_reference_uniform_buffer(obj) -> bool:
+    kind = getattr(obj, "kind", None)
+    return (hasattr(obj, "_gen") and hasattr(obj, "refills") and hasattr(obj, "cursor")
+            and getattr(kind, "value", None) == "uniform01")
+
+
+def _reference_position(buf) -> int:
+    """Stream index of the reference DeviateBuffer's next deviate (rng.py:86-127)."""
+    if buf.refills == 0:
+        return 0
+    return (buf.refills - 1) * buf.capacity + buf.cursor
+
+
+def gibbs_sweep(lat: IsingLattice, part: ColorPartition, rng_buffer, plan=None) -> None:
+    """One full sweep: colour 0 against frozen colour 1, then colour 1 (ising.py:175-187).
+
+    `plan` is accepted for signature compatibility (the device grid replaces the
+    worker split, which the reference guarantees is exact, test_ising.py:140-149).
+    """
+    _run(lat, part, rng_buffer, 1)
+
+
+def gibbs_sweeps(lat, part: ColorPartition, rng_buffer, n_sweeps: int, plan=None) -> None:
+    """n_sweeps sweeps in one device call; identical to n_sweeps gibbs_sweep calls."""
+    _run(lat, part, rng_buffer, n_sweeps)
+
+
+def potts_sweeps(lat: PottsLattice, part: ColorPartition, rng_buffer, n_sweeps: int = 1) -> None:
+    """Checkerboard heat-bath sweeps of the q=4 Potts model."""
+    _run(lat, part, rng_buffer, n_sweeps)
+
+
+def ising_prob_table(w: float, b: float = 0.0) -> np.ndarray:
+    """P(+1 | nsum) for nsum = -4..4 as the device uses it (host-built, exact expit)."""
+    out = np.empty(9)
+    _lib.call("pm_ising_prob_table", float(w), float(b), _lib.dptr(out))
+    return out
+
+
+def potts_cdf_table(coupling: float) -> np.ndarray:
+    """cdf[idx, a] for idx = n0 + 5 n1 + 25 n2 + 125 n3, a = 0..2."""
+    out = np.empty(625 * 3)
+    _lib.call("pm_potts_cdf_table", float(coupling), _lib.dptr(out))
+    return out.reshape(625, 3)

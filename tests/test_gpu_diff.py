@@ -1,0 +1,134 @@
+"""Device parity of the differential-update path and the slice sampler (config 2)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import glm_oracle as gl
+from paper_1310_1537_b200 import glm
+from paper_1310_1537_b200.glm import DesignMatrix, GlmWorkspace
+from paper_1310_1537_b200.rng import BufferKind, DeviateBuffer
+from paper_1310_1537_b200.sampler import (ChainConfig, GaussianPrior, SliceWidenError, log_posterior_coord,
+                                          run_chain, slice_sample_coord)
+from paper_1310_1537_b200.synthetic import baseline_design
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return abs(a - b) / max(abs(a), abs(b), 1.0)
+
+
+def test_replay_reference_ops(gpu):
+    z = golden("diff.npz")
+    d = DesignMatrix(z["x"], z["y"])
+    ws = GlmWorkspace(d, z["beta"])
+    for (op, k, dl), v in zip(z["ops"], z["vals"]):
+        if op == 0:
+            assert rel(glm.diff_loglike(ws, d, int(k), dl), v) < 1e-10
+        else:
+            glm.commit_update(ws, int(k), dl)
+    np.testing.assert_allclose(ws.xbeta, z["xbeta"], rtol=0, atol=1e-10)
+    np.testing.assert_array_equal(ws.beta_current, z["beta_final"])
+    assert ws.validate(d, tol=1e-10) <= 1e-10
+
+
+def test_commit_rounding_is_numpy_exact(gpu):
+    x, y, _, beta = baseline_design(5000, 7, seed=2)
+    d = DesignMatrix(x, y)
+    ws = GlmWorkspace(d, beta)
+    xb = ws.xbeta
+    xt = np.ascontiguousarray(x.T)
+    for k, dl in ((3, 0.25), (0, -1.5), (6, 1e-3)):
+        glm.commit_update(ws, k, dl)
+        gl.commit(xb, xt[k], dl)  # glm.py:537 xbeta += delta * xt[k]
+    np.testing.assert_array_equal(ws.xbeta, xb)
+
+
+def test_multi_delta_bitwise_equals_single(gpu):
+    x, y, _, beta = baseline_design(100_000, 50, seed=3)
+    d = DesignMatrix(x, y)
+    ws = GlmWorkspace(d, beta)
+    deltas = np.linspace(-0.3, 0.3, 16)
+    for m in (1, 2, 3, 5, 8, 11, 16):
+        multi = glm.diff_loglike_multi(ws, d, 4, deltas[:m])
+        for j in range(m):
+            assert multi[j] == glm.diff_loglike(ws, d, 4, float(deltas[j]))
+    xb = x @ beta
+    for j in (0, 7, 15):
+        assert rel(multi[j], gl.diff_loglike(xb, x[:, 4].copy(), y, deltas[j])) < 1e-10
+
+
+def test_zero_delta_equals_loglike_and_no_mutation(gpu):
+    z = golden("glm.npz")
+    d = DesignMatrix(z["x4"], z["y4"])
+    ws = GlmWorkspace(d, z["beta4"])
+    before = ws.xbeta.copy()
+    assert rel(glm.diff_loglike(ws, d, 2, 0.0), glm.loglike(d, z["beta4"])) < 1e-12
+    glm.diff_loglike(ws, d, 1, 2.5)
+    np.testing.assert_array_equal(ws.xbeta, before)
+    np.testing.assert_array_equal(ws.beta_current, z["beta4"])
+
+
+def test_workspace_errors(gpu):
+    d = DesignMatrix(np.random.default_rng(0).standard_normal((10, 3)), np.ones(10))
+    ws = GlmWorkspace(d, np.zeros(3), build_transpose=False)
+    with pytest.raises(ValueError):
+        glm.diff_loglike(ws, d, 0, 0.1)
+    ws = GlmWorkspace(d, np.zeros(3))
+    with pytest.raises(IndexError):
+        glm.diff_loglike(ws, d, 3, 0.1)
+    with pytest.raises(IndexError):
+        glm.commit_update(ws, -1, 0.1)
+    with pytest.raises(ValueError):
+        glm.diff_loglike(ws, d, 0, float("nan"))
+
+
+def test_log_posterior_diff_equals_full(gpu):
+    x, y, _, beta = baseline_design(400, 5, seed=8)
+    d = DesignMatrix(x, y)
+    prior = GaussianPrior.isotropic(5, sigma=5.0)
+    ws = GlmWorkspace(d, beta)
+    for k in range(5):
+        a = log_posterior_coord(ws, d, prior, k, 0.3, use_diff=True)
+        b = log_posterior_coord(ws, d, prior, k, 0.3, use_diff=False)
+        assert abs(a - b) / max(abs(a), 1.0) < 1e-12
+
+
+def test_chain_matches_reference_fixture(gpu):
+    z = golden("sampler.npz")
+    d = DesignMatrix(z["x"], z["y"])
+    out = run_chain(d, GaussianPrior.isotropic(4, sigma=5.0), ChainConfig(n_iter=30, n_burnin=5, seed=77))
+    assert np.max(np.abs(out.draws - z["draws"])) <= 1e-6
+    assert out.accept_evals == int(z["evals"])
+    d2 = DesignMatrix(z["x2"], z["y2"])
+    out2 = run_chain(d2, GaussianPrior.isotropic(5, sigma=5.0), ChainConfig(n_iter=40, n_burnin=0, seed=31))
+    assert np.max(np.abs(out2.draws - z["draws2"])) <= 1e-6
+    assert out2.accept_evals == int(z["evals2"])
+    assert out2.device_passes < out2.accept_evals
+
+
+def test_chain_diff_vs_full_identical(gpu):
+    x, y, _, _ = baseline_design(400, 5, seed=8)
+    d = DesignMatrix(x, y)
+    prior = GaussianPrior.isotropic(5, sigma=5.0)
+    cfg = ChainConfig(n_iter=60, n_burnin=10, seed=31)
+    a = run_chain(d, prior, cfg, use_diff_update=True)
+    b = run_chain(d, prior, cfg, use_diff_update=False)
+    assert np.max(np.abs(a.draws - b.draws)) <= 1e-6
+
+
+def test_stepping_out_abort(gpu):
+    d = DesignMatrix([[0.0]], [1.0])
+    wide = GaussianPrior.isotropic(1, sigma=1e9)
+    ws = GlmWorkspace(d, wide.mu)
+    buf = DeviateBuffer(BufferKind.UNIFORM01, seed=1)
+    with pytest.raises(SliceWidenError):
+        slice_sample_coord(ws, d, wide, 0, buf, ChainConfig(n_iter=1, n_burnin=0, slice_max_steps=5))
+
+
+def test_unit_gaussian_target_statistics(gpu):
+    d = DesignMatrix([[0.0]], [1.0])
+    out = run_chain(d, GaussianPrior.isotropic(1), ChainConfig(n_iter=20000, n_burnin=0, seed=123))
+    draws = out.draws[:, 0]
+    assert abs(draws.mean()) < 0.05 and 0.9 < draws.var() < 1.1

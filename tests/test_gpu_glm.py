@@ -1,0 +1,196 @@
+"""Device parity of the GLM hot path (fused log-posterior + gradient kernel).
+
+Bar (BASELINE north_star): fp64 within relative 1e-10 of the reference CPU path,
+|df|/max(|f|,1) and max_k |dg_k|/max(|g_k|,1); fp32-X within 1e-5 of the fp64
+oracle (and 1e-10 of the oracle run on the fp32-rounded X).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import glm_oracle as gl
+from paper_1310_1537_b200 import glm
+from paper_1310_1537_b200.glm import DesignMatrix, ExecPlan, Strategy
+from paper_1310_1537_b200.instrumentation import counters
+from paper_1310_1537_b200.sampler import GaussianPrior
+from paper_1310_1537_b200.synthetic import baseline_design
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def rel(a, b):
+    return abs(a - b) / max(abs(a), abs(b), 1.0)
+
+
+def grel(g, ref):
+    return float(np.max(np.abs(g - ref) / np.maximum(np.abs(ref), 1.0)))
+
+
+def test_golden_reference_cases(gpu):
+    z = golden("glm.npz")
+    for i in range(int(z["n_cases"])):
+        d = DesignMatrix(z[f"x{i}"], z[f"y{i}"])
+        beta = z[f"beta{i}"]
+        r = glm.loglike_grad(d, beta)
+        assert rel(r.f, float(z[f"f{i}"])) < TOL, (i, r.f, float(z[f"f{i}"]))
+        assert grel(r.g, z[f"g{i}"]) < TOL, i
+        assert rel(glm.loglike(d, beta), float(z[f"fl{i}"])) < TOL, i
+        prior = GaussianPrior(z[f"mu{i}"], z[f"sigma{i}"])
+        lp = glm.log_posterior_grad(d, beta, prior)
+        assert rel(lp.f, float(z[f"lp{i}"])) < TOL, i
+        _, pg = gl.prior_terms(beta, prior.mu, prior.sigma)
+        assert grel(lp.g, z[f"g{i}"] + pg) < TOL, i
+
+
+def test_config0_shape_fixture(gpu):
+    z = golden("glm.npz")
+    d = DesignMatrix(z["c0_x"], z["c0_y"])
+    r = glm.log_posterior_grad(d, z["c0_beta"], GaussianPrior.isotropic(32, 0.0, 10.0))
+    assert rel(r.f, float(z["c0_lp"])) < TOL
+    _, pg = gl.prior_terms(z["c0_beta"], np.zeros(32), np.full(32, 10.0))
+    assert grel(r.g, z["c0_g"] + pg) < TOL
+
+
+def test_known_answers(gpu):
+    x = np.random.default_rng(0).standard_normal((37, 4))
+    y = (np.arange(37) % 2).astype(float)
+    d = DesignMatrix(x, y)
+    r = glm.loglike_grad(d, np.zeros(4))
+    assert r.f == pytest.approx(-37 * math.log(2), rel=1e-12)
+    np.testing.assert_allclose(r.g, x.T @ (y - 0.5), rtol=1e-12)
+    d1 = DesignMatrix([[1.0, 2.0]], [1.0])
+    r1 = glm.loglike_grad(d1, np.zeros(2))
+    assert r1.f == pytest.approx(-math.log(2), rel=1e-14)
+    np.testing.assert_allclose(r1.g, [0.5, 1.0], rtol=1e-14)
+    assert glm.loglike(DesignMatrix([[1.0]], [1.0]), np.zeros(1)) == pytest.approx(-math.log(2), rel=1e-14)
+
+
+@pytest.mark.parametrize("n,k", [(1, 1), (31, 1), (32, 32), (33, 33), (95, 31), (1000, 63), (4097, 64),
+                                 (777, 100), (513, 128), (64, 160), (300, 255), (300, 256), (200, 257),
+                                 (100, 512), (9, 2000)])
+def test_ragged_shapes_against_oracle(gpu, n, k):
+    gen = np.random.default_rng(n * 1000 + k)
+    x = gen.standard_normal((n, k)) * gen.uniform(0.5, 2.0)
+    y = (gen.random(n) < 0.5).astype(float)
+    beta = gen.normal(0, 1.0 / math.sqrt(k), k)
+    d = DesignMatrix(x, y)
+    r = glm.loglike_grad(d, beta)
+    f, g = gl.loglike_grad(x, y, beta)
+    assert rel(r.f, f) < TOL and grel(r.g, g) < TOL
+    assert rel(glm.loglike(d, beta), f) < TOL
+
+
+def test_extreme_linear_predictors(gpu):
+    # saturated sigmoids on both sides: the stable split must hold (glm.py:182-192)
+    x = np.array([[800.0], [-800.0], [40.0], [-40.0], [1e-300], [0.0]])
+    y = np.array([1.0, 0.0, 0.0, 1.0, 1.0, 0.0])
+    for b in (1.0, -1.0, 0.5):
+        r = glm.loglike_grad(DesignMatrix(x, y), np.array([b]))
+        f, g = gl.loglike_grad(x, y, np.array([b]))
+        assert np.isfinite(r.f) and rel(r.f, f) < TOL and grel(r.g, g) < TOL
+
+
+def test_fixed_plan_is_bit_deterministic_and_plan_invariant(gpu):
+    z = golden("glm.npz")
+    d = DesignMatrix(z["x4"], z["y4"])
+    beta = z["beta4"]
+    first = glm.loglike_grad(d, beta)
+    for strategy in Strategy:
+        for workers in (1, 4):
+            r = glm.loglike_grad(d, beta, ExecPlan(strategy, workers=workers, n_chunks=3))
+            assert r.f == first.f and np.array_equal(r.g, first.g)
+
+
+def test_sharded_view_matches_flat(gpu):
+    z = golden("glm.npz")
+    d = DesignMatrix(z["x5"], z["y5"])
+    beta = z["beta5"]
+    v = glm.make_sharded(d, 4)
+    a, b = glm.loglike_grad(v, beta), glm.loglike_grad(d, beta)
+    assert rel(a.f, b.f) < 1e-12 and grel(a.g, b.g) < 1e-12
+    assert rel(glm.loglike(v, beta), b.f) < 1e-12
+    prior = GaussianPrior.isotropic(d.n_cols, 0.1, 2.0)
+    assert rel(glm.log_posterior_grad(v, beta, prior).f, glm.log_posterior_grad(d, beta, prior).f) < 1e-12
+
+
+def test_fp32_storage_variant(gpu):
+    x, y, _, beta = baseline_design(20000, 100, seed=5)
+    d = DesignMatrix(x, y)
+    r32 = glm.loglike_grad(d, beta, ExecPlan(x_storage="f32"))
+    x32 = x.astype(np.float32).astype(np.float64)
+    f32, g32 = gl.loglike_grad(x32, y, beta)
+    assert rel(r32.f, f32) < TOL and grel(r32.g, g32) < TOL  # accumulation is fp64
+    f64, g64 = gl.loglike_grad(x, y, beta)
+    assert rel(r32.f, f64) < 1e-5 and grel(r32.g, g64) < 1e-5
+
+
+def test_counters_follow_reference_contract(gpu):
+    z = golden("glm.npz")
+    d = DesignMatrix(z["x4"], z["y4"])
+    counters.reset()
+    glm.loglike_grad(d, z["beta4"])
+    snap = counters.snapshot()
+    assert snap.flops == d.n_rows * (4 * d.n_cols + 8)  # glm.py:354
+    assert snap.parallel_regions == 1 and snap.kernel_launches == 1
+    counters.reset()
+    glm.loglike(d, z["beta4"])
+    assert counters.snapshot().flops == d.n_rows * (2 * d.n_cols + 6)  # glm.py:264
+
+
+def test_beta_validation(gpu):
+    d = DesignMatrix(np.ones((5, 3)), np.ones(5))
+    with pytest.raises(ValueError):
+        glm.loglike(d, np.zeros(4))
+    with pytest.raises(ValueError):
+        glm.loglike_grad(d, np.array([0.0, np.inf, 0.0]))
+
+
+def test_config0_full_size_against_oracle(gpu):
+    x, y, _, beta = baseline_design(100_000, 32, seed=0)
+    d = DesignMatrix(x, y)
+    prior = GaussianPrior.isotropic(32, 0.0, 10.0)
+    r = glm.log_posterior_grad(d, beta, prior)
+    f, g = gl.log_posterior_grad(x, y, beta, prior.mu, prior.sigma, workers=4)
+    assert rel(r.f, f) < TOL and grel(r.g, g) < TOL
+
+
+def test_config1_shape_against_oracle(gpu):
+    # config 1's K=100 at 2e6 rows (the oracle finishes in seconds); full-size checks below
+    x, y, _, betas = baseline_design(2_000_000, 100, seed=1, n_eval=3)
+    d = DesignMatrix(x, y)
+    prior = GaussianPrior.isotropic(100, 0.0, 10.0)
+    for beta in betas:
+        r = glm.log_posterior_grad(d, beta, prior)
+        f, g = gl.log_posterior_grad(x, y, beta, prior.mu, prior.sigma, workers=8)
+        assert rel(r.f, f) < TOL and grel(r.g, g) < TOL
+    r32 = glm.loglike_grad(d, betas[0], ExecPlan(x_storage="f32"))
+    f, g = gl.loglike_grad(x, y, betas[0], workers=8)
+    assert rel(r32.f, f) < 1e-5 and grel(r32.g, g) < 1e-5
+
+
+def test_config1_full_size_properties(gpu):
+    """N=1e7, K=100 fp64 (8 GB): size-independent properties -- L(0) = -N ln 2 and
+    g(0) = X'(y - 1/2) checked against cuBLAS fp64 (torch) -- and linearity of the
+    row-sharded sum (two half-designs add up to the whole)."""
+    import torch
+    n, k = 10_000_000, 100
+    x, y, _, beta = baseline_design(n, k, seed=11)
+    d = DesignMatrix(x, y)
+    r0 = glm.loglike_grad(d, np.zeros(k))
+    assert rel(r0.f, -n * math.log(2)) < 1e-12
+    xt = torch.from_numpy(x).cuda()
+    g_ref = (xt.T @ (torch.from_numpy(y).cuda() - 0.5)).cpu().numpy()
+    del xt
+    torch.cuda.empty_cache()
+    assert grel(r0.g, g_ref) < TOL
+    r = glm.loglike_grad(d, beta)
+    half = n // 2
+    d.release_device()
+    a = glm.loglike_grad(DesignMatrix(x[:half], y[:half]), beta)
+    b = glm.loglike_grad(DesignMatrix(x[half:], y[half:]), beta)
+    assert rel(r.f, a.f + b.f) < TOL and grel(r.g, a.g + b.g) < TOL
+    assert abs(r.f) > 0 and np.all(np.isfinite(r.g))
