@@ -161,6 +161,7 @@ int choose_geometry(pm_glm_s* h) {
     const size_t per_stage = stream_smem_bytes(h->K, xs, 1, 0) - stream_smem_bytes(h->K, xs, 0, 0);
     int S = int((budget - (long)fixed) / (long)per_stage);
     S = std::min(S, kMaxStages);
+    if (S >= 1) S -= S % std::min(S, kNCW);  // each stage owned by one consumer warp
     if (S >= 2) {
       h->kind = KIND_STREAM;
       h->stages = S;

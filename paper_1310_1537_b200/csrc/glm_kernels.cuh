@@ -160,13 +160,18 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
   const size_t tile_pitch = align_up(tile_bytes, 128);
   if (tile_begin >= tile_end) return;
   const int64_t n_mine = (tile_end - tile_begin + stride - 1) / stride;
+  // Every stage must belong to exactly one consumer warp, which uses it in order: an
+  // mbarrier parity wait cannot tell phase n from phase n+2, so a stage shared by two
+  // warps could let one of them run a phase ahead.  nact consumers, Se = multiple of nact.
+  const int nact = S < NCW ? S : NCW;
+  const int Se = S - S % nact;
 
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
       for (int64_t i = 0; i < n_mine; ++i) {
-        const int s = int(i % S);
-        const uint32_t n = uint32_t(i / S);
+        const int s = int(i % Se);
+        const uint32_t n = uint32_t(i / Se);
         if (n > 0) mbar_wait(&sm.empty[s], (n - 1) & 1);
         const int64_t tile = tile_begin + i * stride;
         mbar_arrive_expect_tx(&sm.full[s], tile_bytes + 32 * sizeof(double));
@@ -182,9 +187,10 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
     return;
   }
   const int cw = warp - 1;
-  for (int64_t i = cw; i < n_mine; i += NCW) {
-    const int s = int(i % S);
-    const uint32_t n = uint32_t(i / S);
+  if (cw >= nact) return;
+  for (int64_t i = cw; i < n_mine; i += nact) {
+    const int s = int(i % Se);
+    const uint32_t n = uint32_t(i / Se);
     mbar_wait(&sm.full[s], n & 1);
     const int64_t tile = tile_begin + i * stride;
     const bool valid = tile * kTileRows + lane < row_limit;
@@ -253,7 +259,7 @@ __device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& s
     for (; b < G; ++b) s0 += __ldcg(a.partials + size_t(b) * (K + 1) + c);
     const double tot = (s0 + s1) + (s2 + s3);
     if (c == 0) {
-      double f = -tot;
+      double f = tot;  // partials already hold -sum(nll) = L
       if (a.with_prior) {
         for (int k = 0; k < K; ++k) {
           const double z = (sm.sbeta[k] - a.prior_mu[k]) / a.prior_sigma[k];
