@@ -14,7 +14,9 @@ using namespace pm;
 
 namespace {
 
-constexpr int kNCW = 8;                      // consumer warps of the streaming kernel
+// consumer warps of the streaming kernel: 7 + 1 producer = 8 warps = 2 per SMSP, which lets
+// ptxas give each thread up to 255 registers (9 warps put 3 on one SMSP -> 168 max)
+constexpr int kNCW = 7;
 constexpr int kStreamThreads = (kNCW + 1) * 32;
 constexpr int kMaxStages = 16;
 constexpr int kHbNCW = 4;

@@ -36,11 +36,14 @@ __device__ __forceinline__ void row_terms(double t, double y, double& nll, doubl
   w = y - sig;
 }
 
-// v[r] holds this lane's partial dot product for tile row r.  Returns, in lane l, the full
-// (all-lane) dot product of row l: a 5-level transpose-reduce, 31 shuffles per 32 rows.
-__device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) {
+// v[r] holds this lane's partial dot product for sub-tile row r (R rows).  Returns, in lane l,
+// the full (all-lane) dot product of row l & (R-1): log2(R) transpose-halving steps, then a
+// plain butterfly over the remaining lane bits (so every lane of a row group holds the same
+// bits).  R = 32 costs 31 shuffles per 32 rows.
+template <int R>
+__device__ __forceinline__ double transpose_reduce(double (&v)[R], int lane) {
 #pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
+  for (int s = R / 2; s >= 1; s >>= 1) {
     const bool upper = (lane & s) != 0;
 #pragma unroll
     for (int i = 0; i < s; ++i) {
@@ -49,7 +52,10 @@ __device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) 
       v[i] = keep + shfl_xor_d(send, s);
     }
   }
-  return v[0];
+  double t = v[0];
+#pragma unroll
+  for (int m = R; m < 32; m <<= 1) t += shfl_xor_d(t, m);
+  return t;
 }
 
 template <typename XT>
@@ -57,41 +63,57 @@ __device__ __forceinline__ double ld_x(const XT* p) {
   return static_cast<double>(*p);
 }
 
-// One warp consumes one 32-row tile resident in shared memory.
+// Rows per register-resident sub-tile: x[R][KC] stays in registers from the dot product to
+// the gradient update, so shared memory is read once; R*KC <= 64 doubles per lane.
+template <int KC, bool GRAD>
+struct SubRows {
+  static constexpr int value = !GRAD ? 32 : (KC <= 2 ? 32 : (KC <= 4 ? 16 : 8));
+};
+
+// One warp consumes one 32-row tile resident in shared memory, R rows at a time.
 // Lane l owns columns l + 32 j (j < KC): beta and the gradient accumulators live in
-// registers, so the tile is read from shared memory twice (dot pass, gradient pass)
-// and from HBM once.
+// registers.  The tile is read from HBM once (TMA) and from shared memory once.
+// Each row's transcendental terms are computed by 32/R lanes; only lane < R counts f.
+// `empty` (the stage's release barrier) is arrived on as soon as the last sub-tile's values
+// are in registers, so the producer can refill the stage while this warp still computes.
 template <typename XT, int KC, bool GRAD>
-__device__ __forceinline__ void consume_tile(const XT* xs, const double* ys,
-                                             int K, int lane, bool valid, const double (&breg)[KC],
-                                             double (&g)[KC], double& nll_acc) {
-  double v[32];
+__device__ __forceinline__ void consume_tile(const XT* xs, const double* ys, int K, int lane, int64_t row0,
+                                             int64_t row_limit, const double (&breg)[KC], double (&g)[KC],
+                                             double& nll_acc, uint64_t* empty) {
+  constexpr int R = SubRows<KC, GRAD>::value;
+#pragma unroll 1
+  for (int sub = 0; sub < 32 / R; ++sub) {
+    const XT* xb = xs + (sub * R) * K + lane;
+    double x[R][KC];
+    double v[R];
 #pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    const XT* xr = xs + r * K + lane;
-    double acc = 0.0;
-#pragma unroll
-    for (int j = 0; j < KC; ++j) {
-      if (j < KC - 1 || lane + 32 * j < K) acc = fma(ld_x(xr + 32 * j), breg[j], acc);
-    }
-    v[r] = acc;
-  }
-  const double t = transpose_reduce32(v, lane);
-  // Force the gradient pass to re-read the tile from shared memory: without this the
-  // compiler keeps all 32*KC tile values of the dot pass live in registers and spills.
-  asm volatile("" ::: "memory");
-  double nll, w;
-  row_terms(t, ys[lane], nll, w);
-  nll_acc += valid ? nll : 0.0;
-  if (GRAD) {
-    w = valid ? w : 0.0;
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const double wr = shfl_d(w, r);
-      const XT* xr = xs + r * K + lane;
+    for (int r = 0; r < R; ++r) {
+      double acc = 0.0;
 #pragma unroll
       for (int j = 0; j < KC; ++j) {
-        if (j < KC - 1 || lane + 32 * j < K) g[j] = fma(wr, ld_x(xr + 32 * j), g[j]);
+        x[r][j] = (j < KC - 1 || lane + 32 * j < K) ? ld_x(xb + r * K + 32 * j) : 0.0;
+        acc = fma(x[r][j], breg[j], acc);
+      }
+      v[r] = acc;
+    }
+    const int rr = sub * R + (lane & (R - 1));
+    const double yv = ys[rr];
+    if (sub == 32 / R - 1) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty);  // release semantics order this warp's smem reads
+    }
+    const double t = transpose_reduce<R>(v, lane);
+    double nll, w;
+    row_terms(t, yv, nll, w);
+    const bool valid = row0 + rr < row_limit;
+    nll_acc += (valid && lane < R) ? nll : 0.0;
+    if (GRAD) {
+      w = valid ? w : 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double wr = shfl_d(w, r);
+#pragma unroll
+        for (int j = 0; j < KC; ++j) g[j] = fma(wr, x[r][j], g[j]);
       }
     }
   }
@@ -193,11 +215,9 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
     const uint32_t n = uint32_t(i / Se);
     mbar_wait(&sm.full[s], n & 1);
     const int64_t tile = tile_begin + i * stride;
-    const bool valid = tile * kTileRows + lane < row_limit;
     consume_tile<XT, KC, GRAD>(reinterpret_cast<const XT*>(sm.xs + size_t(s) * tile_pitch),
-                               sm.ys + size_t(s) * 32, K, lane, valid, breg, g, nll_acc);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[s]);
+                               sm.ys + size_t(s) * 32, K, lane, tile * kTileRows, row_limit, breg, g, nll_acc,
+                               &sm.empty[s]);
   }
 }
 
