@@ -57,6 +57,7 @@ CONFIGS = {
     "c1": dict(n=10_000_000, k=100, x_storage="f64", desc="config 1: N=1e7 K=100 fp64 log-posterior+gradient"),
     "c1f32": dict(n=10_000_000, k=100, x_storage="f32",
                   desc="config 1 fp32-X/fp64-accumulate: N=1e7 K=100 log-posterior+gradient"),
+    "c2": dict(chain_n=1_000_000, k=50, desc="config 2: slice-within-Gibbs chain, N=1e6 K=50 fp64 (iterations)"),
     "c3": dict(groups=1000, k=20, mean_rows=2000, desc="config 3: G=1000 n_g~Poisson(2000) K=20 HB batched"),
     "c4": dict(h=8192, w=8192, model="ising", desc="config 4: 8192^2 periodic Ising, Philox4x32 (seed,sweep,site)"),
     "c4potts": dict(h=8192, w=8192, model="potts", desc="config 4 Potts q=4 variant, 8192^2 periodic"),
@@ -369,6 +370,48 @@ def run_glm(args, cfg):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------------------- B200 arm: chain
+def run_chain_bench(args, cfg):
+    """Config 2: `steps` sampler iterations (each = K coordinate updates) of run_chain."""
+    import torch
+    from paper_1310_1537_b200 import glm as pglm
+    from paper_1310_1537_b200.rng import BufferKind, DeviateBuffer
+    from paper_1310_1537_b200.sampler import ChainConfig, GaussianPrior, run_chain
+    from paper_1310_1537_b200.synthetic import baseline_design
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    n, k = cfg["chain_n"], cfg["k"]
+    x, y, _, _ = baseline_design(n, k, seed=2)
+    data = pglm.DesignMatrix(x, y)
+    prior = GaussianPrior.isotropic(k, 0.0, 10.0)
+    if args.warmup:
+        run_chain(data, prior, ChainConfig(n_iter=args.warmup, n_burnin=0, seed=5))
+    clocks = ClockSampler(local)
+    clocks.start()
+    t0 = time.perf_counter()
+    out = run_chain(data, prior, ChainConfig(n_iter=args.steps, n_burnin=0, seed=5),
+                    rng=DeviateBuffer(BufferKind.UNIFORM01, seed=5))
+    wall = time.perf_counter() - t0
+    clk = clocks.stop()
+    peak, src = load_peaks()
+    evals = out.accept_evals
+    if rank == 0:
+        print(json.dumps({
+            "metric": "slice-within-Gibbs iterations/s (config 2)", "value": args.steps / wall,
+            "unit": "iterations/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True, "scaling": "replicas only",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY §8d config 2 generator)",
+            "config": {"workload": cfg["desc"], "N": n, "K": k, "seed": 5},
+            "log_posterior_evals_per_s": evals / wall, "evals_per_coordinate": evals / (args.steps * k),
+            "device_passes_per_coordinate": out.device_passes / (args.steps * k),
+            "roofline": {"bound": "launch/sync latency (dependent evaluations)",
+                         "achieved": out.device_passes * 24 * n / wall / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": out.device_passes * 24 * n / wall / 1e9 / peak, "traffic": None, "peak_source": src},
+            "e2e": {"value": args.steps / wall, "unit": "iterations/s", "h2d_bytes_per_step": 8 * 16 * k,
+                    "d2h_bytes_per_step": 8 * 16 * k},
+            "gpu_launches": out.device_passes + args.steps * k, "clocks": clk}), flush=True)
+
+
 # ---------------------------------------------------------------------------- B200 arm: HB
 def run_hb(args, cfg):
     import torch
@@ -492,6 +535,10 @@ def main():
         args.steps = args.steps or 1000
         args.warmup = args.warmup if args.warmup is not None else 10
         run_glm(args, cfg)
+    elif "chain_n" in cfg:
+        args.steps = args.steps or 20
+        args.warmup = args.warmup if args.warmup is not None else 3
+        run_chain_bench(args, cfg)
     elif "groups" in cfg:
         args.steps = args.steps or 200
         args.warmup = args.warmup if args.warmup is not None else 5

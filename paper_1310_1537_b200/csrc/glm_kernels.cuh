@@ -191,9 +191,9 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
+      int s = 0;        // stage = i % Se
+      uint32_t n = 0;   // use count of the stage = i / Se
       for (int64_t i = 0; i < n_mine; ++i) {
-        const int s = int(i % Se);
-        const uint32_t n = uint32_t(i / Se);
         if (n > 0) mbar_wait(&sm.empty[s], (n - 1) & 1);
         const int64_t tile = tile_begin + i * stride;
         mbar_arrive_expect_tx(&sm.full[s], tile_bytes + 32 * sizeof(double));
@@ -204,20 +204,29 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
           bulk_g2s(sm.xs + size_t(s) * tile_pitch, src, tile_bytes, &sm.full[s]);
         }
         bulk_g2s(sm.ys + size_t(s) * 32, y + tile * kTileRows, 32 * sizeof(double), &sm.full[s]);
+        if (++s == Se) {
+          s = 0;
+          ++n;
+        }
       }
     }
     return;
   }
   const int cw = warp - 1;
   if (cw >= nact) return;
+  int s = cw;       // i % Se for i = cw + m*nact (Se is a multiple of nact)
+  uint32_t n = 0;   // i / Se
   for (int64_t i = cw; i < n_mine; i += nact) {
-    const int s = int(i % Se);
-    const uint32_t n = uint32_t(i / Se);
     mbar_wait(&sm.full[s], n & 1);
     const int64_t tile = tile_begin + i * stride;
     consume_tile<XT, KC, GRAD>(reinterpret_cast<const XT*>(sm.xs + size_t(s) * tile_pitch),
                                sm.ys + size_t(s) * 32, K, lane, tile * kTileRows, row_limit, breg, g, nll_acc,
                                &sm.empty[s]);
+    s += nact;
+    if (s >= Se) {
+      s = cw;
+      ++n;
+    }
   }
 }
 

@@ -138,16 +138,32 @@ struct PackedArgs {
   unsigned long long thr[9];  // Ising: ceil(P(+1 | nsum) * 2^32), nsum = -4..4
 };
 
-__device__ __forceinline__ void load16(const int8_t* p, int8_t (&b)[16]) {
-  const int4 v = __ldg(reinterpret_cast<const int4*>(p));
-  memcpy(b, &v, 16);
+__device__ __forceinline__ uint4 ld16(const int8_t* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
+
+__device__ __forceinline__ uint32_t w_of(const uint4& v, int m) {
+  return m == 0 ? v.x : m == 1 ? v.y : m == 2 ? v.z : v.w;
+}
+
+// Ising: per byte, 1 if the spin is -1 (0xFF) and 0 if +1 (0x01): bit 1 of each byte.
+__device__ __forceinline__ uint32_t down_bits(uint32_t x) { return (x >> 1) & 0x01010101u; }
+
+// Potts: per byte, 5^state for states 0..3 (PRMT table lookup, selector nibbles = states).
+__device__ __forceinline__ uint32_t pow5_bytes(uint32_t x) {
+  const uint32_t t = x | (x >> 4);                       // byte0 = s0 | s1<<4, byte2 = s2 | s3<<4
+  const uint32_t sel = (t & 0xFFu) | ((t >> 8) & 0xFF00u);
+  return __byte_perm(0x7D190501u, 0u, sel);              // bytes {1, 5, 25, 125}[s]
 }
 
 template <int MODEL>
 __global__ void __launch_bounds__(256) gibbs_packed_kernel(PackedArgs a, const unsigned long long* __restrict__ pthr) {
-  __shared__ unsigned long long s_thr[MODEL == PM_MODEL_ISING ? 9 : kPottsIdx * 3];
+  __shared__ unsigned long long s_thr[MODEL == PM_MODEL_ISING ? 5 : kPottsIdx * 3];
   if (MODEL == PM_MODEL_ISING) {
-    if (threadIdx.x < 9) s_thr[threadIdx.x] = a.thr[threadIdx.x];
+    // indexed by the number of -1 neighbours nd = 0..4 (nsum = 4 - 2 nd); static indices
+    // into the parameter array (a dynamic index would copy the params to local memory)
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < 5; ++k) s_thr[k] = a.thr[8 - 2 * k];
+    }
   } else {
     for (int t = threadIdx.x; t < kPottsIdx * 3; t += blockDim.x) s_thr[t] = pthr[t];
   }
@@ -159,45 +175,51 @@ __global__ void __launch_bounds__(256) gibbs_packed_kernel(PackedArgs a, const u
   const int q0 = int(gt % per_row) << 4;
   const int iu = (i == 0) ? a.H - 1 : i - 1;
   const int id = (i == a.H - 1) ? 0 : i + 1;
-  int8_t up[16], dn[16], mid[16];
-  load16(a.other + int64_t(iu) * a.W2 + q0, up);
-  load16(a.other + int64_t(id) * a.W2 + q0, dn);
-  load16(a.other + int64_t(i) * a.W2 + q0, mid);
+  const int8_t* orow = a.other + int64_t(i) * a.W2;
+  const uint4 up = ld16(a.other + int64_t(iu) * a.W2 + q0);
+  const uint4 dn = ld16(a.other + int64_t(id) * a.W2 + q0);
+  const uint4 mid = ld16(orow + q0);
+  // o = 0: horizontal neighbours of packed site q are q-1 and q; o = 1: q and q+1
   const int o = (i + a.colour) & 1;
-  // o = 0: horizontal neighbours are packed q-1 and q; o = 1: q and q+1
-  const int8_t edge = o ? __ldg(a.other + int64_t(i) * a.W2 + ((q0 + 16 == a.W2) ? 0 : q0 + 16))
-                        : __ldg(a.other + int64_t(i) * a.W2 + ((q0 == 0) ? a.W2 - 1 : q0 - 1));
+  const uint32_t edge = o ? uint32_t(uint8_t(__ldg(orow + ((q0 + 16 == a.W2) ? 0 : q0 + 16))))
+                          : uint32_t(uint8_t(__ldg(orow + ((q0 == 0) ? a.W2 - 1 : q0 - 1))));
   const uint64_t s0 = uint64_t(a.colour) * uint64_t(a.n0) + uint64_t(i) * a.W2 + q0;
-  int8_t res[16];
+  uint32_t res[4];
 #pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    const U32x4 blk = site_philox_block((s0 >> 2) + g, a.sweep, a.seed);
+  for (int m = 0; m < 4; ++m) {
+    const uint32_t cur = w_of(mid, m);
+    // byte b of `sh` = the other horizontal neighbour of site 4m+b (funnel shift across words)
+    const uint32_t sh = o == 0 ? __funnelshift_l(m == 0 ? (edge << 24) : w_of(mid, m - 1), cur, 8)
+                               : __funnelshift_r(cur, m == 3 ? edge : w_of(mid, m + 1), 8);
+    const U32x4 blk = site_philox_block((s0 >> 2) + m, a.sweep, a.seed);
+    uint32_t out = 0;
+    if (MODEL == PM_MODEL_ISING) {
+      const uint32_t nd = down_bits(w_of(up, m)) + down_bits(w_of(dn, m)) + down_bits(cur) + down_bits(sh);
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int q = 4 * g + t;
-      int8_t l, r;
-      if (o == 0) {
-        l = (q == 0) ? edge : mid[q - 1];
-        r = mid[q];
-      } else {
-        l = mid[q];
-        r = (q == 15) ? edge : mid[q + 1];
+      for (int b = 0; b < 4; ++b) {
+        const uint32_t k = (nd >> (8 * b)) & 0xFFu;
+        const bool plus = uint64_t(blk.v[b]) < s_thr[k];
+        out |= (plus ? 0x01u : 0xFFu) << (8 * b);
       }
-      const uint32_t w = blk.v[t];
-      if (MODEL == PM_MODEL_ISING) {
-        const int nsum = up[q] + dn[q] + l + r;
-        res[q] = (uint64_t(w) < s_thr[nsum + 4]) ? int8_t(1) : int8_t(-1);
-      } else {
-        const int pw[4] = {1, 5, 25, 125};
-        const int idx = pw[up[q]] + pw[dn[q]] + pw[l] + pw[r];
+    } else {
+      const uint32_t p1 = pow5_bytes(w_of(up, m)), p2 = pow5_bytes(w_of(dn, m));
+      const uint32_t p3 = pow5_bytes(cur), p4 = pow5_bytes(sh);
+      // two 16-bit lanes per word so the sums (<= 500) cannot overflow
+      const uint32_t ev = (p1 & 0x00FF00FFu) + (p2 & 0x00FF00FFu) + (p3 & 0x00FF00FFu) + (p4 & 0x00FF00FFu);
+      const uint32_t od = ((p1 >> 8) & 0x00FF00FFu) + ((p2 >> 8) & 0x00FF00FFu) + ((p3 >> 8) & 0x00FF00FFu) +
+                          ((p4 >> 8) & 0x00FF00FFu);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const uint32_t idx = ((b & 1) ? od : ev) >> (16 * (b >> 1)) & 0xFFFFu;
         const unsigned long long* t3 = s_thr + idx * 3;
-        res[q] = int8_t((w >= t3[0]) + (w >= t3[1]) + (w >= t3[2]));
+        const uint64_t w = blk.v[b];
+        const uint32_t st = uint32_t(w >= t3[0]) + uint32_t(w >= t3[1]) + uint32_t(w >= t3[2]);
+        out |= st << (8 * b);
       }
     }
+    res[m] = out;
   }
-  int4 outv;
-  memcpy(&outv, res, 16);
-  *reinterpret_cast<int4*>(a.mine + int64_t(i) * a.W2 + q0) = outv;
+  *reinterpret_cast<uint4*>(a.mine + int64_t(i) * a.W2 + q0) = make_uint4(res[0], res[1], res[2], res[3]);
 }
 
 // ---------------------------------------------------------------- layout conversion

@@ -35,14 +35,9 @@ PM_HD void mulhilo64(uint64_t a, uint64_t b, uint64_t& hi, uint64_t& lo) {
 }
 
 PM_HD void mulhilo32(uint32_t a, uint32_t b, uint32_t& hi, uint32_t& lo) {
-#if defined(__CUDA_ARCH__)
-  lo = a * b;
-  hi = __umulhi(a, b);
-#else
-  const uint64_t p = (uint64_t)a * b;
+  const uint64_t p = (uint64_t)a * b;  // one IMAD.WIDE.U32 on the device
   lo = (uint32_t)p;
   hi = (uint32_t)(p >> 32);
-#endif
 }
 
 PM_HD U64x4 philox4x64_10(U64x4 c, uint64_t k0, uint64_t k1) {
