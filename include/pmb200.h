@@ -197,6 +197,21 @@ PM_API int pm_lat_stream(pm_lat_t h, void** stream);
 /* 1 if sweeps run on the red-black packed fast path (periodic, even H and W). */
 PM_API int pm_lat_packed(pm_lat_t h, int* packed);
 
+/* Strip of a periodic H x W lattice for multi-GPU sweeps: this handle owns
+ * global rows [row0, row0+rows) and keeps one halo row of each colour above and below.
+ * Requires even H, W and W % 32 == 0; spins via pm_lat_set/get_spins (rows x W); the
+ * field via pm_lat_set_ising (uniform) / pm_lat_set_potts.  Site colours and RNG site
+ * indices use global coordinates, so any strip decomposition gives the single-GPU spins. */
+PM_API int pm_lat_create_strip(int device, int32_t height, int32_t width, int32_t row0, int32_t rows,
+                               int model, pm_lat_t* out);
+/* Update colour `colour` of the own rows (Philox4x32 keyed by (seed, sweep, site)) on
+ * `stream` (cudaStream_t, NULL = handle stream) reading the other colour's halo rows.
+ * The caller then exchanges this colour's first/last own rows with the neighbours. */
+PM_API int pm_lat_strip_half_sweep(pm_lat_t h, int colour, uint64_t seed, uint64_t sweep, void* stream);
+/* Device pointer of packed row `array_row` of colour `colour` (W/2 bytes): 0 = top halo,
+ * 1..rows = own rows, rows+1 = bottom halo. */
+PM_API int pm_lat_strip_row(pm_lat_t h, int colour, int32_t array_row, void** dev_ptr);
+
 /* Host-side table builders, exported so tests can check them against the oracle. */
 PM_API int pm_ising_prob_table(double w, double b, double* p_out /*9: nsum=-4..4*/);
 PM_API int pm_potts_cdf_table(double coupling, double* cdf_out /*625*3*/);

@@ -130,12 +130,16 @@ __global__ void __launch_bounds__(256) gibbs_generic_kernel(GenericArgs a) {
 struct PackedArgs {
   const int8_t* other;
   int8_t* mine;
-  int H, W2;
+  int H, W2;                  // global lattice height, packed width
   int colour;
-  int64_t n0;
+  int64_t n0;                 // global sites of colour 0
   uint64_t sweep;
   uint64_t seed;
   unsigned long long thr[9];  // Ising: ceil(P(+1 | nsum) * 2^32), nsum = -4..4
+  // strip decomposition: own rows are global rows row0 .. row0+rows-1, stored at array rows
+  // halo .. halo+rows-1; with halo = 1 the arrays carry one halo row above and below
+  // (filled by the caller's exchange) and there is no vertical wrap inside the strip.
+  int row0, rows, halo;
 };
 
 __device__ __forceinline__ uint4 ld16(const int8_t* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
@@ -155,6 +159,9 @@ __device__ __forceinline__ uint32_t pow5_bytes(uint32_t x) {
 }
 
 template <int MODEL>
+__device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const unsigned long long* s_thr, int i, int q0);
+
+template <int MODEL>
 __global__ void __launch_bounds__(256) gibbs_packed_kernel(PackedArgs a, const unsigned long long* __restrict__ pthr) {
   __shared__ unsigned long long s_thr[MODEL == PM_MODEL_ISING ? 5 : kPottsIdx * 3];
   if (MODEL == PM_MODEL_ISING) {
@@ -168,14 +175,22 @@ __global__ void __launch_bounds__(256) gibbs_packed_kernel(PackedArgs a, const u
     for (int t = threadIdx.x; t < kPottsIdx * 3; t += blockDim.x) s_thr[t] = pthr[t];
   }
   __syncthreads();
+  // 2-D grid: x = 16-site column groups of a row, y = rows (no integer division)
   const int per_row = a.W2 >> 4;
-  const int64_t gt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (gt >= int64_t(a.H) * per_row) return;
-  const int i = int(gt / per_row);
-  const int q0 = int(gt % per_row) << 4;
-  const int iu = (i == 0) ? a.H - 1 : i - 1;
-  const int id = (i == a.H - 1) ? 0 : i + 1;
-  const int8_t* orow = a.other + int64_t(i) * a.W2;
+  const int cgrp = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cgrp >= per_row) return;
+  for (int r = blockIdx.y; r < a.rows; r += gridDim.y) {
+    gibbs_packed_row<MODEL>(a, s_thr, r, cgrp << 4);
+  }
+}
+
+template <int MODEL>
+__device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const unsigned long long* s_thr, int r, int q0) {
+  const int li = r + a.halo;   // array row
+  const int i = a.row0 + r;    // global row: colour parity and RNG site index
+  const int iu = a.halo ? li - 1 : (li == 0 ? a.rows - 1 : li - 1);
+  const int id = a.halo ? li + 1 : (li == a.rows - 1 ? 0 : li + 1);
+  const int8_t* orow = a.other + int64_t(li) * a.W2;
   const uint4 up = ld16(a.other + int64_t(iu) * a.W2 + q0);
   const uint4 dn = ld16(a.other + int64_t(id) * a.W2 + q0);
   const uint4 mid = ld16(orow + q0);
@@ -219,22 +234,26 @@ __global__ void __launch_bounds__(256) gibbs_packed_kernel(PackedArgs a, const u
     }
     res[m] = out;
   }
-  *reinterpret_cast<uint4*>(a.mine + int64_t(i) * a.W2 + q0) = make_uint4(res[0], res[1], res[2], res[3]);
+  *reinterpret_cast<uint4*>(a.mine + int64_t(li) * a.W2 + q0) = make_uint4(res[0], res[1], res[2], res[3]);
 }
 
 // ---------------------------------------------------------------- layout conversion
-__global__ void pack_kernel(const int8_t* __restrict__ grid, int H, int W, int8_t* pk0, int8_t* pk1) {
+// grid [H][W] <-> packed colour arrays.  par0 = global row of grid row 0 (colour parity),
+// aoff = array row of grid row 0 (1 for strips, whose arrays start with a halo row).
+__global__ void pack_kernel(const int8_t* __restrict__ grid, int H, int W, int8_t* pk0, int8_t* pk1, int par0,
+                            int aoff) {
   const int64_t n = int64_t(H) * W;
   for (int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < n; f += int64_t(gridDim.x) * blockDim.x) {
     const int i = int(f / W), j = int(f % W);
-    ((i + j) & 1 ? pk1 : pk0)[int64_t(i) * (W >> 1) + (j >> 1)] = grid[f];
+    ((par0 + i + j) & 1 ? pk1 : pk0)[int64_t(i + aoff) * (W >> 1) + (j >> 1)] = grid[f];
   }
 }
-__global__ void unpack_kernel(int8_t* __restrict__ grid, int H, int W, const int8_t* pk0, const int8_t* pk1) {
+__global__ void unpack_kernel(int8_t* __restrict__ grid, int H, int W, const int8_t* pk0, const int8_t* pk1,
+                              int par0, int aoff) {
   const int64_t n = int64_t(H) * W;
   for (int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < n; f += int64_t(gridDim.x) * blockDim.x) {
     const int i = int(f / W), j = int(f % W);
-    grid[f] = ((i + j) & 1 ? pk1 : pk0)[int64_t(i) * (W >> 1) + (j >> 1)];
+    grid[f] = ((par0 + i + j) & 1 ? pk1 : pk0)[int64_t(i + aoff) * (W >> 1) + (j >> 1)];
   }
 }
 
@@ -282,8 +301,11 @@ struct pm_lat_s {
   int sms = 0;
   cudaStream_t stream = nullptr;
   std::mutex mu;
-  int H = 0, W = 0, boundary = 0, model = 0;
+  int H = 0, W = 0, boundary = 0, model = 0;   // H = own rows for a strip
   int packed = 0;
+  // strip of a periodic global lattice (multi-GPU, §8e): own rows are global rows
+  // row0 .. row0+H-1, arrays hold H+2 rows (halo above and below)
+  int strip = 0, row0 = 0, H_global = 0;
   int8_t* pk0 = nullptr;
   int8_t* pk1 = nullptr;
   int8_t* scratch = nullptr;  // H*W staging for set/get
@@ -417,7 +439,7 @@ int pm_lat_set_spins(pm_lat_t h, const int8_t* s) {
   DeviceGuard g(h->device);
   if (h->packed) {
     PM_CUDA(cudaMemcpyAsync(h->scratch, s, n, cudaMemcpyHostToDevice, h->stream));
-    pack_kernel<<<grid_for(h, n), 256, 0, h->stream>>>(h->scratch, h->H, h->W, h->pk0, h->pk1);
+    pack_kernel<<<grid_for(h, n), 256, 0, h->stream>>>(h->scratch, h->H, h->W, h->pk0, h->pk1, h->row0, h->strip);
     PM_CUDA(cudaGetLastError());
   } else {
     PM_CUDA(cudaMemcpyAsync(h->pk0, s, n, cudaMemcpyHostToDevice, h->stream));
@@ -432,7 +454,8 @@ int pm_lat_get_spins(pm_lat_t h, int8_t* s) {
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard g(h->device);
   if (h->packed) {
-    unpack_kernel<<<grid_for(h, n), 256, 0, h->stream>>>(h->scratch, h->H, h->W, h->pk0, h->pk1);
+    unpack_kernel<<<grid_for(h, n), 256, 0, h->stream>>>(h->scratch, h->H, h->W, h->pk0, h->pk1, h->row0,
+                                                         h->strip);
     PM_CUDA(cudaGetLastError());
     PM_CUDA(cudaMemcpyAsync(s, h->scratch, n, cudaMemcpyDeviceToHost, h->stream));
   } else {
@@ -508,6 +531,95 @@ int pm_lat_set_potts(pm_lat_t h, double coupling) {
 static int lat_sweeps_impl(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t key0, uint64_t key1,
                            uint64_t stream_pos, const double* uniforms, float* total_ms);
 
+// One half-sweep (colour c) of the packed fast path; for a strip, the own rows of the strip.
+static void launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t seed, cudaStream_t st) {
+  const int Hg = h->strip ? h->H_global : h->H;
+  PackedArgs pa;
+  pa.other = c == 0 ? h->pk1 : h->pk0;
+  pa.mine = c == 0 ? h->pk0 : h->pk1;
+  pa.H = Hg;
+  pa.W2 = h->W / 2;
+  pa.colour = c;
+  pa.n0 = int64_t(Hg) * (h->W / 2);
+  pa.sweep = sweep;
+  pa.seed = seed;
+  for (int k = 0; k < 9; ++k) pa.thr[k] = h->thr[k];
+  pa.row0 = h->row0;
+  pa.rows = h->H;
+  pa.halo = h->strip;
+  const int per_row = h->W / 2 / 16;
+  const int bx = std::min(256, (per_row + 31) / 32 * 32);
+  const dim3 grid((per_row + bx - 1) / bx, std::min(h->H, 65535));
+  if (h->model == PM_MODEL_ISING)
+    gibbs_packed_kernel<PM_MODEL_ISING><<<grid, bx, 0, st>>>(pa, nullptr);
+  else
+    gibbs_packed_kernel<PM_MODEL_POTTS4><<<grid, bx, 0, st>>>(pa, h->pthr);
+}
+
+int pm_lat_create_strip(int device, int32_t height, int32_t width, int32_t row0, int32_t rows, int model,
+                        pm_lat_t* out) {
+  if (!out) return fail(PM_EINVAL, "null output");
+  if (height < 2 || width < 2 || (height % 2) || (width % 2))
+    return fail(PM_EINVAL, "periodic checkerboard needs even height and width");
+  if ((width / 2) % 16) return fail(PM_EINVAL, "strips need width % 32 == 0 (16-site packed groups)");
+  if (rows < 1 || row0 < 0 || row0 + rows > height) return fail(PM_ERANGE, "strip rows out of range");
+  if (model != PM_MODEL_ISING && model != PM_MODEL_POTTS4) return fail(PM_EINVAL, "bad model");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (device < 0 || device >= n) return fail(PM_ERANGE, "device index out of range");
+  pm_lat_s* h = new pm_lat_s();
+  h->device = device;
+  h->H = rows;
+  h->W = width;
+  h->boundary = PM_BOUNDARY_PERIODIC;
+  h->model = model;
+  h->packed = 1;
+  h->strip = 1;
+  h->row0 = row0;
+  h->H_global = height;
+  DeviceGuard g(device);
+  h->sms = sm_count(device);
+  const size_t arr = size_t(rows + 2) * (width / 2) + 16;
+  e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&h->pk0, arr);
+  if (e == cudaSuccess) e = cudaMalloc(&h->pk1, arr);
+  if (e == cudaSuccess) e = cudaMemset(h->pk0, 0, arr);
+  if (e == cudaSuccess) e = cudaMemset(h->pk1, 0, arr);
+  if (e == cudaSuccess) e = cudaMalloc(&h->scratch, size_t(rows) * width + 16);
+  if (e != cudaSuccess) {
+    free_lat(h);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return cuda_fail(e, "pm_lat_create_strip");
+  }
+  *out = h;
+  return PM_OK;
+}
+
+int pm_lat_strip_half_sweep(pm_lat_t h, int colour, uint64_t seed, uint64_t sweep, void* stream) {
+  if (!h) return fail(PM_EINVAL, "null handle");
+  if (!h->strip) return fail(PM_ESTATE, "not a strip handle");
+  if (colour != 0 && colour != 1) return fail(PM_EINVAL, "colour must be 0 or 1");
+  if (h->model == PM_MODEL_ISING && !h->has_field) return fail(PM_ESTATE, "call pm_lat_set_ising first");
+  if (h->model == PM_MODEL_POTTS4 && !h->has_potts) return fail(PM_ESTATE, "call pm_lat_set_potts first");
+  if (h->model == PM_MODEL_ISING && h->n_class != 1) return fail(PM_EINVAL, "strips need a uniform field");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  launch_packed(h, colour, sweep, seed, stream ? static_cast<cudaStream_t>(stream) : h->stream);
+  PM_CUDA(cudaGetLastError());
+  return PM_OK;
+}
+
+int pm_lat_strip_row(pm_lat_t h, int colour, int32_t array_row, void** dev_ptr) {
+  if (!h || !dev_ptr) return fail(PM_EINVAL, "null argument");
+  if (!h->strip) return fail(PM_ESTATE, "not a strip handle");
+  if (colour != 0 && colour != 1) return fail(PM_EINVAL, "colour must be 0 or 1");
+  if (array_row < 0 || array_row > h->H + 1) return fail(PM_ERANGE, "array row out of range");
+  *dev_ptr = (colour ? h->pk1 : h->pk0) + size_t(array_row) * (h->W / 2);
+  return PM_OK;
+}
+
 int pm_lat_sweeps(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t key0, uint64_t key1, uint64_t stream_pos,
                   const double* uniforms) {
   return lat_sweeps_impl(h, n_sweeps, rng_mode, key0, key1, stream_pos, uniforms, nullptr);
@@ -529,6 +641,7 @@ static int lat_sweeps_impl(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t 
   if (rng_mode == PM_RNG_UNIFORMS && !uniforms && n_sweeps > 0) return fail(PM_EINVAL, "uniforms required");
   if (h->model == PM_MODEL_ISING && !h->has_field) return fail(PM_ESTATE, "call pm_lat_set_ising first");
   if (h->model == PM_MODEL_POTTS4 && !h->has_potts) return fail(PM_ESTATE, "call pm_lat_set_potts first");
+  if (h->strip) return fail(PM_ESTATE, "strip handles sweep with pm_lat_strip_half_sweep + halo exchange");
   if (n_sweeps == 0) return PM_OK;
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard g(h->device);
@@ -557,22 +670,7 @@ static int lat_sweeps_impl(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t 
       const int64_t nc = c == 0 ? n0 : n1;
       if (nc == 0) continue;
       if (fast) {
-        PackedArgs pa;
-        pa.other = c == 0 ? h->pk1 : h->pk0;
-        pa.mine = c == 0 ? h->pk0 : h->pk1;
-        pa.H = h->H;
-        pa.W2 = h->W / 2;
-        pa.colour = c;
-        pa.n0 = n0;
-        pa.sweep = stream_pos + uint64_t(t);
-        pa.seed = key0;
-        for (int k = 0; k < 9; ++k) pa.thr[k] = h->thr[k];
-        const int64_t threads = int64_t(h->H) * (h->W / 2 / 16);
-        const int blocks = int((threads + 255) / 256);
-        if (h->model == PM_MODEL_ISING)
-          gibbs_packed_kernel<PM_MODEL_ISING><<<blocks, 256, 0, h->stream>>>(pa, nullptr);
-        else
-          gibbs_packed_kernel<PM_MODEL_POTTS4><<<blocks, 256, 0, h->stream>>>(pa, h->pthr);
+        launch_packed(h, c, stream_pos + uint64_t(t), key0, h->stream);
       } else {
         GenericArgs a;
         a.lat = view_of(h);

@@ -35,9 +35,16 @@ PM_HD void mulhilo64(uint64_t a, uint64_t b, uint64_t& hi, uint64_t& lo) {
 }
 
 PM_HD void mulhilo32(uint32_t a, uint32_t b, uint32_t& hi, uint32_t& lo) {
-  const uint64_t p = (uint64_t)a * b;  // one IMAD.WIDE.U32 on the device
+#if defined(__CUDA_ARCH__)
+  // one IMAD.WIDE.U32 (the C++ form leaves an extra add of zero on the high word)
+  asm("{\n\t.reg .u64 t;\n\tmul.wide.u32 t, %2, %3;\n\tmov.b64 {%0, %1}, t;\n\t}"
+      : "=r"(lo), "=r"(hi)
+      : "r"(a), "r"(b));
+#else
+  const uint64_t p = (uint64_t)a * b;
   lo = (uint32_t)p;
   hi = (uint32_t)(p >> 32);
+#endif
 }
 
 PM_HD U64x4 philox4x64_10(U64x4 c, uint64_t k0, uint64_t k1) {

@@ -21,7 +21,8 @@ import numpy as np
 from .glm import DesignMatrix, GradResult, _check_beta
 from .parallel import partition
 
-__all__ = ["shard_bounds", "ordered_sum", "gather_partials", "DistributedDesign"]
+__all__ = ["shard_bounds", "ordered_sum", "gather_partials", "DistributedDesign",
+           "strip_bounds", "exchange_halos", "LatticeStrip", "strip_sweeps"]
 
 
 def shard_bounds(n_rows: int, world: int, rank: int) -> tuple[int, int]:
@@ -96,3 +97,125 @@ class DistributedDesign:
     def log_posterior_grad(self, beta, prior=None) -> GradResult:
         out = self.log_posterior_grad_device(beta, prior).cpu().numpy()
         return GradResult(float(out[0]), out[1:].copy())
+
+
+# ---------------------------------------------------------------------------
+# lattice strips with halo-row exchange
+# ---------------------------------------------------------------------------
+
+def strip_bounds(height: int, world: int, rank: int) -> tuple[int, int]:
+    """Global rows owned by `rank` (same partition rule as the rows of X)."""
+    return partition(height, world)[rank]
+
+
+def exchange_halos(first_row, last_row, top_halo, bottom_halo, rank: int, world: int, group=None) -> None:
+    """Refresh the halo rows of one colour after that colour was updated.
+
+    The row above a strip belongs to rank (rank-1) % world (its last own row), the row
+    below to rank (rank+1) % world (its first own row); the lattice is periodic.  Every
+    rank issues its operations in the same canonical order (send up, send down, receive
+    from below, receive from above) so FIFO-matched transports (NCCL) and tag-matched
+    ones (gloo) pair them identically, including world == 2 where up == down.
+    """
+    if world == 1:
+        top_halo.copy_(last_row)
+        bottom_halo.copy_(first_row)
+        return
+    import torch.distributed as dist
+    up, down = (rank - 1) % world, (rank + 1) % world
+    gu = dist.get_global_rank(group, up) if group is not None else up
+    gd = dist.get_global_rank(group, down) if group is not None else down
+    ops = [dist.P2POp(dist.isend, first_row, gu, group, tag=0),
+           dist.P2POp(dist.isend, last_row, gd, group, tag=1),
+           dist.P2POp(dist.irecv, bottom_halo, gd, group, tag=0),
+           dist.P2POp(dist.irecv, top_halo, gu, group, tag=1)]
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+
+
+class _DevBuf:
+    """__cuda_array_interface__ view of raw device bytes (torch.as_tensor consumes it)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class LatticeStrip:
+    """This rank's strip of a periodic H x W lattice on its GPU (pm_lat_create_strip)."""
+
+    def __init__(self, height: int, width: int, row0: int, rows: int, device: int,
+                 model: str = "ising", w: float = 0.0, coupling: float = 0.0):
+        import ctypes
+
+        from . import _lib
+        self._lib = _lib
+        _lib.require_device(device)
+        h = ctypes.c_void_p()
+        m = _lib.PM_MODEL_ISING if model == "ising" else _lib.PM_MODEL_POTTS4
+        _lib.check(_lib.load().pm_lat_create_strip(device, height, width, row0, rows, m, ctypes.byref(h)),
+                   "pm_lat_create_strip")
+        self._h = h
+        self.height, self.width, self.row0, self.rows, self.device = height, width, row0, rows, device
+        if model == "ising":
+            _lib.call("pm_lat_set_ising", h, float(w), None)
+        else:
+            _lib.call("pm_lat_set_potts", h, float(coupling))
+        self._views = {}
+
+    def set_spins(self, own_rows: np.ndarray) -> None:
+        s = np.ascontiguousarray(own_rows, dtype=np.int8)
+        assert s.shape == (self.rows, self.width)
+        self._lib.call("pm_lat_set_spins", self._h, self._lib.i8ptr(s))
+
+    def get_spins(self) -> np.ndarray:
+        out = np.empty((self.rows, self.width), dtype=np.int8)
+        self._lib.call("pm_lat_get_spins", self._h, self._lib.i8ptr(out))
+        return out
+
+    def row(self, colour: int, array_row: int):
+        """torch uint8 tensor aliasing packed row `array_row` of `colour` (0/rows+1 = halos)."""
+        import ctypes
+
+        import torch
+        key = (colour, array_row)
+        t = self._views.get(key)
+        if t is None:
+            p = ctypes.c_void_p()
+            self._lib.call("pm_lat_strip_row", self._h, int(colour), int(array_row), ctypes.byref(p))
+            t = torch.as_tensor(_DevBuf(p.value, self.width // 2), device=f"cuda:{self.device}")
+            self._views[key] = t
+        return t
+
+    def half_sweep(self, colour: int, seed: int, sweep: int) -> None:
+        import ctypes
+
+        import torch
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self._lib.call("pm_lat_strip_half_sweep", self._h, int(colour), ctypes.c_uint64(seed),
+                       ctypes.c_uint64(sweep), ctypes.c_void_p(stream))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._views.clear()
+            self._lib.load().pm_lat_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def strip_sweeps(strip, n_sweeps: int, seed: int, sweep0: int, rank: int, world: int, group=None) -> None:
+    """n_sweeps full sweeps of a strip-decomposed lattice: per colour, the device half-sweep
+    then one halo exchange of that colour (bit-identical to the single-GPU sweep)."""
+    r = strip.rows
+    for c in (0, 1):  # halos of both colours must be current before the first half-sweep
+        exchange_halos(strip.row(c, 1), strip.row(c, r), strip.row(c, 0), strip.row(c, r + 1), rank, world, group)
+    for t in range(n_sweeps):
+        for c in (0, 1):
+            strip.half_sweep(c, seed, sweep0 + t)
+            exchange_halos(strip.row(c, 1), strip.row(c, r), strip.row(c, 0), strip.row(c, r + 1), rank, world,
+                           group)

@@ -59,3 +59,87 @@ def test_rank_ordered_fold_equals_reference_merge(world):
     for _, _, _, tot in res:
         assert tot[0] == f_ref and np.array_equal(tot[1:], g_ref)  # identical on every rank
     assert abs(res[0][3][0] - float(z["c0_f"])) / abs(float(z["c0_f"])) < 1e-13
+
+
+# ---------------------------------------------------------------------------
+# lattice strips: the halo-exchange schedule of paper_1310_1537_b200.dist, driven by a CPU
+# emulation of the strip half-sweep (same global row / colour / RNG-site indexing as the
+# device kernel), must reproduce the full-lattice oracle bit for bit for any strip count.
+# ---------------------------------------------------------------------------
+
+class _CpuStrip:
+    def __init__(self, full, w, row0, rows):
+        import math
+        self.H, self.W = full.shape
+        self.W2 = self.W // 2
+        self.row0, self.rows, self.w = row0, rows, w
+        self.math = math
+        self.pk = [torch.zeros((rows + 2, self.W2), dtype=torch.uint8) for _ in range(2)]
+        for r in range(rows):
+            i = row0 + r
+            for j in range(self.W):
+                self.pk[(i + j) & 1][r + 1, j // 2] = int(full[i, j]) & 0xFF
+
+    def row(self, colour, array_row):
+        return self.pk[colour][array_row]
+
+    def half_sweep(self, c, seed, sweep):
+        from oracle import gibbs_oracle as go
+        lib = go.load()
+        other = self.pk[1 - c].numpy().view(np.int8)
+        mine = self.pk[c].numpy()
+        n0 = self.H * self.W2
+        for r in range(1, self.rows + 1):
+            i = self.row0 + r - 1
+            o = (i + c) & 1
+            for q in range(self.W2):
+                nsum = int(other[r - 1, q]) + int(other[r + 1, q]) + int(other[r, (q - 1 + o) % self.W2]) + \
+                    int(other[r, (q + o) % self.W2])
+                wn = self.w * float(nsum)
+                p = 1.0 / (1.0 + self.math.exp(-(0.0 + wn)))
+                u = lib.oracle_site_uniform(c * n0 + i * self.W2 + q, sweep, seed)
+                mine[r, q] = 0x01 if u < p else 0xFF
+
+    def own(self):
+        out = np.empty((self.rows, self.W), dtype=np.int8)
+        for r in range(self.rows):
+            i = self.row0 + r
+            for j in range(self.W):
+                out[r, j] = np.int8(np.uint8(self.pk[(i + j) & 1][r + 1, j // 2]))
+        return out
+
+
+def _strip_worker(rank, world, port, q, shape, sweeps, seed):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1310_1537_b200.dist import strip_bounds, strip_sweeps
+        from paper_1310_1537_b200.synthetic import ising_spins
+        full = ising_spins(*shape, seed=4)
+        a, b = strip_bounds(shape[0], world, rank)
+        strip = _CpuStrip(full, 0.8814, a, b - a)
+        strip_sweeps(strip, sweeps, seed, 0, rank, world)
+        q.put((rank, a, strip.own()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_strip_halo_exchange_matches_full_lattice(world):
+    from oracle import gibbs_oracle as go
+    from paper_1310_1537_b200.synthetic import ising_spins
+    shape, sweeps, seed = (12, 8), 3, 77
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_strip_worker, args=(r, world, port, q, shape, sweeps, seed)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=300) for _ in range(world)), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    got = np.concatenate([r[2] for r in res], axis=0)
+    ref = go.ising_sweeps(ising_spins(*shape, seed=4), None, 0.8814, True, sweeps, go.RNG_PHILOX4X32, seed, 0, 0)
+    np.testing.assert_array_equal(got, ref)

@@ -164,3 +164,40 @@ def test_single_node_and_zero_coupling(gpu):
         gibbs_sweeps(lat, part, buf, 10)
         total += float(lat.s.sum())
     assert abs(total / (200 * 256)) < 0.05
+
+
+def _local_exchange(strips, colour):
+    """In-process halo exchange between strips on one GPU (the NCCL schedule's data flow)."""
+    n = len(strips)
+    for k, s in enumerate(strips):
+        up, down = strips[(k - 1) % n], strips[(k + 1) % n]
+        s.row(colour, 0).copy_(up.row(colour, up.rows))
+        s.row(colour, s.rows + 1).copy_(down.row(colour, 1))
+
+
+@pytest.mark.parametrize("n_strips,model", [(1, "ising"), (2, "ising"), (3, "ising"), (4, "potts"), (5, "ising")])
+def test_strips_match_single_lattice(gpu, n_strips, model):
+    import torch
+    from paper_1310_1537_b200.dist import LatticeStrip, strip_bounds
+    H, W, sweeps, seed = 96, 64, 20, 31
+    full = ising_spins(H, W, seed=6) if model == "ising" else potts_states(H, W, seed=6)
+    strips = []
+    for k in range(n_strips):
+        a, b = strip_bounds(H, n_strips, k)
+        s = LatticeStrip(H, W, a, b - a, 0, model=model, w=0.8814, coupling=1.0986)
+        s.set_spins(full[a:b])
+        strips.append(s)
+    for c in (0, 1):
+        _local_exchange(strips, c)
+    for t in range(sweeps):
+        for c in (0, 1):
+            for s in strips:
+                s.half_sweep(c, seed, t)
+            _local_exchange(strips, c)
+    torch.cuda.synchronize()
+    got = np.concatenate([s.get_spins() for s in strips], axis=0)
+    if model == "ising":
+        ref = go.ising_sweeps(full, None, 0.8814, True, sweeps, go.RNG_PHILOX4X32, seed, 0, 0)
+    else:
+        ref = go.potts_sweeps(full, 1.0986, True, sweeps, go.RNG_PHILOX4X32, seed, 0, 0)
+    np.testing.assert_array_equal(got, ref)
