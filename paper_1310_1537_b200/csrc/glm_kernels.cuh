@@ -274,26 +274,26 @@ __device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& s
   if (*sm.flag == 0) return;
   __threadfence();
   const int G = gridDim.x;
-  // column totals in fixed order (4 interleaved accumulators, combined pairwise)
-  for (int c = tid; c <= K; c += blockDim.x) {
-    if (c > 0 && !grad) break;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int b = 0;
-    for (; b + 4 <= G; b += 4) {
-      s0 += __ldcg(a.partials + size_t(b) * (K + 1) + c);
-      s1 += __ldcg(a.partials + size_t(b + 1) * (K + 1) + c);
-      s2 += __ldcg(a.partials + size_t(b + 2) * (K + 1) + c);
-      s3 += __ldcg(a.partials + size_t(b + 3) * (K + 1) + c);
+  const int lane = tid & 31, nwarps = blockDim.x >> 5;
+  if (a.with_prior) {  // -0.5 z_k^2 (sampler.py:55-58) computed in parallel into the free wg scratch
+    for (int k = tid; k < K; k += blockDim.x) {
+      const double z = (sm.sbeta[k] - a.prior_mu[k]) / a.prior_sigma[k];
+      sm.wg[k] = -0.5 * z * z;
     }
-    for (; b < G; ++b) s0 += __ldcg(a.partials + size_t(b) * (K + 1) + c);
-    const double tot = (s0 + s1) + (s2 + s3);
+    __syncthreads();
+  }
+  // column totals in a fixed order: one warp per column, lane l folds CTAs l, l+32, ...
+  // (all loads independent, so one L2 round trip per 32 CTAs), then the fixed butterfly
+  for (int c = tid >> 5; c <= K; c += nwarps) {
+    if (c > 0 && !grad) break;
+    double part = 0.0;
+    for (int b = lane; b < G; b += 32) part += __ldcg(a.partials + size_t(b) * (K + 1) + c);
+    const double tot = warp_sum(part);
+    if (lane != 0) continue;
     if (c == 0) {
       double f = tot;  // partials already hold -sum(nll) = L
       if (a.with_prior) {
-        for (int k = 0; k < K; ++k) {
-          const double z = (sm.sbeta[k] - a.prior_mu[k]) / a.prior_sigma[k];
-          f += -0.5 * z * z;
-        }
+        for (int k = 0; k < K; ++k) f += sm.wg[k];  // prior terms, ascending k
       }
       a.out[0] = f;
     } else {
