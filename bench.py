@@ -157,8 +157,61 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------- CPU baseline
+def cpu_worker_other(args):
+    """CPU oracle timings for configs 2-4 (bounded samples; see the `sample` strings)."""
+    cores = host_cores()
+    cfg = CONFIGS[args.config]
+    if "chain_n" in cfg:
+        from oracle import sampler_oracle as so
+        from paper_1310_1537_b200.synthetic import baseline_design
+        x, y, _, _ = baseline_design(cfg["chain_n"], cfg["k"], seed=2)
+        t0 = time.perf_counter()
+        _, evals = so.run_chain(x, y, np.zeros(cfg["k"]), np.full(cfg["k"], 10.0), 1, 0, seed=5, workers=cores)
+        dt = time.perf_counter() - t0
+        res = {"value": 1.0 / dt, "unit": "iterations/s", "cores": cores, "kind": "port",
+               "sample": f"oracle/sampler_oracle.py run_chain, 1 iteration (K={cfg['k']} coordinate updates, "
+                         f"{evals} evaluations) at N={cfg['chain_n']}, numpy diff_loglike over {cores} workers"}
+    elif "groups" in cfg:
+        from oracle import glm_oracle as gl
+        from paper_1310_1537_b200.synthetic import hb_design
+        x, y, off, betas, mu, tau = hb_design(cfg["groups"], cfg["k"], seed=3, mean_rows=cfg["mean_rows"])
+        gl.hb_log_posterior_grad(x, y, off, betas, mu, np.full(cfg["k"], tau))
+        t0 = time.perf_counter()
+        for _ in range(3):
+            gl.hb_log_posterior_grad(x, y, off, betas, mu, np.full(cfg["k"], tau))
+        dt = (time.perf_counter() - t0) / 3
+        res = {"value": 1.0 / dt, "unit": "launches/s", "cores": 1, "kind": "port",
+               "sample": "oracle/glm_oracle.py hb_log_posterior_grad (per-group numpy loop, the reference's "
+                         "hb.py:127-135 composition), full config-3 data, mean of 3 after 1 warm-up"}
+    else:
+        from oracle import gibbs_oracle as go
+        from paper_1310_1537_b200.synthetic import ising_spins, potts_states
+        h, w = cfg["h"], cfg["w"]
+        t0 = time.perf_counter()
+        if cfg["model"] == "ising":
+            go.ising_sweeps(ising_spins(h, w, seed=0), None, 2 * 0.4407, True, 1, go.RNG_PHILOX4X32, 2024, 0, 0)
+        else:
+            go.potts_sweeps(potts_states(h, w, seed=0), 0.4407, True, 1, go.RNG_PHILOX4X32, 2024, 0, 0)
+        dt = time.perf_counter() - t0
+        res = {"value": 1.0 / dt, "unit": "sweeps/s", "cores": 1, "kind": "port",
+               "sample": f"oracle/gibbs_oracle.c (scalar C restatement of ising.py:175-187 + Philox4x32), "
+                         f"1 sweep at {h}x{w}, 1 core"}
+    print(json.dumps(res))
+
+
+def cpu_baseline_other(config: str) -> dict:
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--cpu-worker", "--config", config]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, check=True).stdout
+        return json.loads(out.strip().splitlines()[-1])
+    except Exception as exc:
+        return {"value": None, "unit": None, "cores": host_cores(), "kind": "port", "sample": f"failed: {exc}"}
+
+
 def cpu_worker_main(args):
     """Subprocess body: time the oracle port on a bounded sample (OPENBLAS set to 1 above)."""
+    if "n" not in CONFIGS[args.config]:
+        return cpu_worker_other(args)
     from oracle import glm_oracle as gl
     from paper_1310_1537_b200.synthetic import baseline_design
     cores = host_cores()
@@ -409,7 +462,8 @@ def run_chain_bench(args, cfg):
                          "frac": out.device_passes * 24 * n / wall / 1e9 / peak, "traffic": None, "peak_source": src},
             "e2e": {"value": args.steps / wall, "unit": "iterations/s", "h2d_bytes_per_step": 8 * 16 * k,
                     "d2h_bytes_per_step": 8 * 16 * k},
-            "gpu_launches": out.device_passes + args.steps * k, "clocks": clk}), flush=True)
+            "gpu_launches": out.device_passes + args.steps * k, "clocks": clk,
+            "cpu_baseline": None if args.no_cpu_baseline else cpu_baseline_other(args.config)}), flush=True)
 
 
 # ---------------------------------------------------------------------------- B200 arm: HB
@@ -450,7 +504,8 @@ def run_hb(args, cfg):
                          "note": "wall time incl. beta H2D and (f,g) D2H", "peak_source": src},
             "e2e": {"value": 1000.0 / ms, "unit": "launches/s", "h2d_bytes_per_step": betas.nbytes,
                     "d2h_bytes_per_step": 8 * cfg["groups"] * (cfg["k"] + 1)},
-            "gpu_launches": args.steps, "clocks": clk}), flush=True)
+            "gpu_launches": args.steps, "clocks": clk,
+            "cpu_baseline": None if args.no_cpu_baseline else cpu_baseline_other(args.config)}), flush=True)
 
 
 # ---------------------------------------------------------------------------- B200 arm: Gibbs
@@ -550,7 +605,8 @@ def run_gibbs(args, cfg):
                          "peak_source": src},
             "e2e": {"value": args.steps / e2e, "unit": "sweeps/s", "h2d_bytes_per_step": h * w / args.steps,
                     "d2h_bytes_per_step": h * w / args.steps},
-            "gpu_launches": 2 * args.steps, "clocks": clk}), flush=True)
+            "gpu_launches": 2 * args.steps, "clocks": clk,
+            "cpu_baseline": None if args.no_cpu_baseline else cpu_baseline_other(args.config)}), flush=True)
 
 
 def main():

@@ -50,7 +50,9 @@ enum pm_status {
   PM_ERANGE = 2,
   PM_EDEVICE = 3,
   PM_ENOMEM = 4,
-  PM_ESTATE = 5
+  PM_ESTATE = 5,
+  PM_ESLICE = 6,   /* -> SliceWidenError (sampler.py:32-33, 141-150) */
+  PM_ESHRINK = 7   /* -> RuntimeError "slice shrinkage failed" (sampler.py:163-164) */
 };
 
 /* storage type of the design matrix on the device */
@@ -129,6 +131,18 @@ PM_API int pm_ws_read_xbeta(pm_ws_t ws, double* out);
 /* max_n |xbeta_n - (X beta_current)_n| recomputed on the device (GlmWorkspace.validate,
  * glm.py:484-489). */
 PM_API int pm_ws_validate(pm_ws_t ws, const double* beta_current, double* max_abs_err);
+
+/* Device-resident run_chain (sampler.py:170-200) from the workspace's current xbeta and
+ * beta_inout[K] (in: start point, out: final point), prior N(mu, sigma^2), on the numpy
+ * Philox4x64 UNIFORM01 stream with key (key0, key1) starting at deviate stream_pos (the
+ * reference's consumption order, sampler.py:131-153).  One cooperative kernel; every
+ * conditional evaluation is one grid-wide pass.  draws_out: (n_iter-n_burnin) x K;
+ * *stream_pos_out = position after the chain; *evals_out = the reference's evaluation
+ * count; on PM_ESLICE / PM_ESHRINK *fail_coord = the coordinate. */
+PM_API int pm_ws_run_chain(pm_ws_t ws, const double* mu, const double* sigma, int32_t n_iter, int32_t n_burnin,
+                           double slice_width, int32_t slice_max_steps, uint64_t key0, uint64_t key1,
+                           uint64_t stream_pos, double* draws_out, double* beta_inout, uint64_t* stream_pos_out,
+                           int64_t* evals_out, int32_t* fail_coord);
 
 /* ------------------------------------------------------------------ hierarchical GLM
  * Replaces the per-group loop of loglike_grad over HbDataset.groups (hb.py:64-86,

@@ -17,7 +17,7 @@ from ctypes import (POINTER, c_char_p, c_double, c_int, c_int8, c_int32, c_int64
 
 import numpy as np
 
-PM_OK, PM_EINVAL, PM_ERANGE, PM_EDEVICE, PM_ENOMEM, PM_ESTATE = range(6)
+PM_OK, PM_EINVAL, PM_ERANGE, PM_EDEVICE, PM_ENOMEM, PM_ESTATE, PM_ESLICE, PM_ESHRINK = range(8)
 PM_X_F64, PM_X_F32 = 0, 1
 PM_BOUNDARY_FREE, PM_BOUNDARY_PERIODIC = 0, 1
 PM_MODEL_ISING, PM_MODEL_POTTS4 = 0, 1
@@ -56,6 +56,8 @@ SIGNATURES = {
     "pm_ws_commit": (c_int, [c_void_p, c_int32, c_double]),
     "pm_ws_read_xbeta": (c_int, [c_void_p, _dp]),
     "pm_ws_validate": (c_int, [c_void_p, _dp, _dp]),
+    "pm_ws_run_chain": (c_int, [c_void_p, _dp, _dp, c_int32, c_int32, c_double, c_int32, c_uint64, c_uint64,
+                                c_uint64, _dp, _dp, POINTER(c_uint64), POINTER(c_int64), POINTER(c_int32)]),
     "pm_hb_create": (c_int, [c_int, POINTER(c_void_p)]),
     "pm_hb_destroy": (c_int, [c_void_p]),
     "pm_hb_upload": (c_int, [c_void_p, _dp, _dp, _i64p, c_int32, c_int32]),

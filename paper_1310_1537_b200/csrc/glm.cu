@@ -627,6 +627,32 @@ int pm_ws_commit(pm_ws_t w, int32_t k, double delta) {
   return PM_OK;
 }
 
+int pm_ws_internal_view(pm_ws_t w, pm_ws_view* v) {
+  if (!w || !v) return fail(PM_EINVAL, "null argument");
+  pm_glm_s* h = w->h;
+  v->xbeta = w->xbeta;
+  v->xt = w->xt;
+  v->y = h->y;
+  v->n = h->n_rows;
+  v->ld = h->n_pad;
+  v->K = h->K;
+  v->device = h->device;
+  v->sms = h->sms;
+  v->stream = h->stream;
+  return PM_OK;
+}
+
+int pm_ws_internal_lock(pm_ws_t w, int lock) {
+  if (lock) {
+    w->mu.lock();
+    w->h->mu.lock();
+  } else {
+    w->h->mu.unlock();
+    w->mu.unlock();
+  }
+  return PM_OK;
+}
+
 int pm_ws_read_xbeta(pm_ws_t w, double* out) {
   if (!w || !out) return fail(PM_EINVAL, "null argument");
   pm_glm_s* h = w->h;

@@ -26,14 +26,6 @@ struct DiffArgs {
 };
 
 // Rounding identical to numpy's `xbeta + delta*xk` (glm.py:517): product rounded, then sum.
-__device__ __forceinline__ double shifted_t(double xb, double d, double xk) {
-  return __dadd_rn(xb, __dmul_rn(d, xk));
-}
-
-__device__ __forceinline__ double row_nll(double t, double y) {
-  const double e = exp(-fabs(t));
-  return (1.0 - y) * t + fmax(-t, 0.0) + log1p(e);
-}
 
 // Grid-stride over elements; per-thread sums for each delta in the same order for every M,
 // so f for a given delta is bit-identical whether it is evaluated alone or in a batch.
@@ -163,8 +155,15 @@ struct HbArgs {
 
 // One CTA per group: the group's tiles stream through the same TMA ring as K1; the CTA
 // reduces its warps in fixed order and adds the shared group prior.  No cross-CTA step.
+// Groups are short (~63 tiles), so several CTAs per SM hide latency: smaller register
+// sub-tiles (HbRows) keep the footprint under the 3-CTAs/SM register budget.
+template <int KC, bool GRAD>
+struct HbRows {
+  static constexpr int value = !GRAD ? 32 : (KC == 1 ? 16 : (KC == 2 ? 8 : 4));
+};
+
 template <int KC, bool GRAD, int NCW>
-__global__ void __launch_bounds__((NCW + 1) * 32) hb_kernel(HbArgs a) {
+__global__ void __launch_bounds__((NCW + 1) * 32, 3) hb_kernel(HbArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int K = a.K;
   const int S = a.stages;
@@ -191,8 +190,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32) hb_kernel(HbArgs a) {
   }
   double nll = 0.0;
   const int64_t p0 = a.poff[grp], p1 = a.poff[grp + 1];
-  stream_tiles<double, KC, GRAD, NCW>(a.X, a.y, K, p0 / kTileRows, p1 / kTileRows, 1, p0 + a.nrows[grp], S, sm,
-                                      breg, g, nll, false);
+  stream_tiles<double, KC, GRAD, NCW, HbRows<KC, GRAD>::value>(a.X, a.y, K, p0 / kTileRows, p1 / kTileRows, 1,
+                                                               p0 + a.nrows[grp], S, sm, breg, g, nll, false);
   if (warp > 0) {
     const int cw = warp - 1;
     const double wsum = warp_sum(nll);

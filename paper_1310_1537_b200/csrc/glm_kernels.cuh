@@ -36,6 +36,17 @@ __device__ __forceinline__ void row_terms(double t, double y, double& nll, doubl
   w = y - sig;
 }
 
+// Rounding identical to numpy's `xbeta + delta*xk` (glm.py:517/537): product rounded, then sum.
+__device__ __forceinline__ double shifted_t(double xb, double d, double xk) {
+  return __dadd_rn(xb, __dmul_rn(d, xk));
+}
+
+// nll term only (diff_loglike, glm.py:499-522)
+__device__ __forceinline__ double row_nll(double t, double y) {
+  const double e = exp(-fabs(t));
+  return (1.0 - y) * t + fmax(-t, 0.0) + log1p(e);
+}
+
 // v[r] holds this lane's partial dot product for sub-tile row r (R rows).  Returns, in lane l,
 // the full (all-lane) dot product of row l & (R-1): log2(R) transpose-halving steps, then a
 // plain butterfly over the remaining lane bits (so every lane of a row group holds the same
@@ -76,11 +87,10 @@ struct SubRows {
 // Each row's transcendental terms are computed by 32/R lanes; only lane < R counts f.
 // `empty` (the stage's release barrier) is arrived on as soon as the last sub-tile's values
 // are in registers, so the producer can refill the stage while this warp still computes.
-template <typename XT, int KC, bool GRAD>
+template <typename XT, int KC, bool GRAD, int R = SubRows<KC, GRAD>::value>
 __device__ __forceinline__ void consume_tile(const XT* xs, const double* ys, int K, int lane, int64_t row0,
                                              int64_t row_limit, const double (&breg)[KC], double (&g)[KC],
                                              double& nll_acc, uint64_t* empty) {
-  constexpr int R = SubRows<KC, GRAD>::value;
 #pragma unroll 1
   for (int sub = 0; sub < 32 / R; ++sub) {
     const XT* xb = xs + (sub * R) * K + lane;
@@ -169,7 +179,7 @@ __device__ inline StreamSmem carve_stream_smem(unsigned char* base, int K, int x
 // Producer/consumer ring over the tiles tile_begin, tile_begin+stride, ... < tile_end.
 // Warp 0 lane 0 issues TMA bulk copies; warps 1..NCW consume tiles round-robin.
 // Rows with global (padded) index >= row_limit are masked (padding).
-template <typename XT, int KC, bool GRAD, int NCW>
+template <typename XT, int KC, bool GRAD, int NCW, int R = SubRows<KC, GRAD>::value>
 __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const double* __restrict__ y, int K,
                                              int64_t tile_begin, int64_t tile_end, int64_t stride,
                                              int64_t row_limit, int S, const StreamSmem& sm,
@@ -219,7 +229,7 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
   for (int64_t i = cw; i < n_mine; i += nact) {
     mbar_wait(&sm.full[s], n & 1);
     const int64_t tile = tile_begin + i * stride;
-    consume_tile<XT, KC, GRAD>(reinterpret_cast<const XT*>(sm.xs + size_t(s) * tile_pitch),
+    consume_tile<XT, KC, GRAD, R>(reinterpret_cast<const XT*>(sm.xs + size_t(s) * tile_pitch),
                                sm.ys + size_t(s) * 32, K, lane, tile * kTileRows, row_limit, breg, g, nll_acc,
                                &sm.empty[s]);
     s += nact;

@@ -43,6 +43,24 @@ struct DeviceGuard {
 
 int sm_count(int device);
 
+}  // namespace pm
+
+// Workspace internals shared between glm.cu (owner) and chain.cu (hidden symbols).
+struct pm_ws_view {
+  double* xbeta;
+  const double* xt;   // [K][ld]
+  const double* y;
+  int64_t n, ld;
+  int K;
+  int device;
+  int sms;
+  void* stream;
+};
+extern "C" int pm_ws_internal_view(pm_ws_t ws, pm_ws_view* v);
+extern "C" int pm_ws_internal_lock(pm_ws_t ws, int lock);
+
+namespace pm {
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device); `mask` is a
 // per-kernel static bitmask of devices already configured.
 cudaError_t ensure_smem_attr(const void* kernel, std::atomic<uint64_t>& mask);

@@ -62,8 +62,11 @@ class ExecPlan:
     n_chunks: int = 1
     device: int = 0
     x_storage: str = "f64"
+    chain: str = "device"
 
     def __post_init__(self):
+        if self.chain not in ("device", "host"):
+            raise ValueError(f"chain must be 'device' or 'host', got {self.chain!r}")
         if self.workers < 1:
             raise ValueError(f"workers must be >= 1, got {self.workers}")
         if self.n_chunks < 1:

@@ -108,6 +108,47 @@ def test_chain_matches_reference_fixture(gpu):
     assert out2.device_passes < out2.accept_evals
 
 
+def test_config2_shape_chain_against_oracle(gpu):
+    """Config 2 (N=1e6, K=50, prior N(0,10^2)): the first iterations' draws within 1e-6 of
+    the CPU oracle chain on the identical uniform stream, identical evaluation counts."""
+    from oracle import sampler_oracle as so
+    x, y, _, _ = baseline_design(1_000_000, 50, seed=2)
+    d = DesignMatrix(x, y)
+    prior = GaussianPrior.isotropic(50, 0.0, 10.0)
+    out = run_chain(d, prior, ChainConfig(n_iter=2, n_burnin=0, seed=5))
+    ref, evals = so.run_chain(x, y, prior.mu, prior.sigma, 2, 0, seed=5, workers=8)
+    assert np.max(np.abs(out.draws - ref)) <= 1e-6
+    assert out.accept_evals == evals
+
+
+def test_resident_chain_equals_host_driven_chain(gpu):
+    from paper_1310_1537_b200.glm import ExecPlan
+    x, y, _, _ = baseline_design(20_000, 6, seed=3)
+    d = DesignMatrix(x, y)
+    prior = GaussianPrior.isotropic(6, 0.0, 10.0)
+    cfg = ChainConfig(n_iter=25, n_burnin=5, seed=9)
+    a = run_chain(d, prior, cfg)                                    # one cooperative kernel
+    b = run_chain(d, prior, cfg, ExecPlan(chain="host"))            # host loop, device evals
+    assert np.max(np.abs(a.draws - b.draws)) <= 1e-6
+    assert a.accept_evals == b.accept_evals
+    buf = DeviateBuffer(BufferKind.UNIFORM01, seed=9)
+    c = run_chain(d, prior, cfg, rng=buf)
+    assert np.array_equal(a.draws, c.draws)
+    host_buf = DeviateBuffer(BufferKind.UNIFORM01, seed=9)
+    run_chain(d, prior, cfg, ExecPlan(chain="host"), rng=host_buf)
+    assert buf.position == host_buf.position  # the device consumed exactly the host's uniforms
+    dbg = run_chain(d, prior, ChainConfig(n_iter=230, n_burnin=30, seed=9), debug=True)
+    full = run_chain(d, prior, ChainConfig(n_iter=230, n_burnin=30, seed=9))
+    assert np.array_equal(dbg.draws, full.draws) and dbg.accept_evals == full.accept_evals
+
+
+def test_resident_chain_stepping_out_abort(gpu):
+    d = DesignMatrix([[0.0]], [1.0])
+    wide = GaussianPrior.isotropic(1, sigma=1e9)
+    with pytest.raises(SliceWidenError):
+        run_chain(d, wide, ChainConfig(n_iter=3, n_burnin=0, seed=1, slice_max_steps=5))
+
+
 def test_chain_diff_vs_full_identical(gpu):
     x, y, _, _ = baseline_design(400, 5, seed=8)
     d = DesignMatrix(x, y)

@@ -78,6 +78,17 @@ def test_diff_oracle_replays_reference_ops():
     np.testing.assert_allclose(xbeta, z["xbeta"], rtol=0, atol=1e-12)
 
 
+def test_sampler_oracle_matches_reference_chain():
+    from oracle import sampler_oracle as so
+    z = golden("sampler.npz")
+    draws, evals = so.run_chain(z["x"], z["y"], np.zeros(4), np.full(4, 5.0), 30, 5, seed=77)
+    np.testing.assert_array_equal(draws, z["draws"])
+    assert evals == int(z["evals"])
+    draws2, evals2 = so.run_chain(z["x2"], z["y2"], np.zeros(5), np.full(5, 5.0), 40, 0, seed=31)
+    np.testing.assert_array_equal(draws2, z["draws2"])
+    assert evals2 == int(z["evals2"])
+
+
 def test_hb_oracle_matches_reference():
     z = golden("hb.npz")
     f, g = gl.hb_log_posterior_grad(z["x"], z["y"], z["offsets"], z["betas"], z["mu"], z["sigma"])
