@@ -482,14 +482,14 @@ def run_hb(args, cfg):
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
+    ms = dev.time_evals(betas, mu, sigma, n=args.steps) / args.steps  # device, CUDA events
+    clk = clocks.stop()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         dev.eval(betas, mu, sigma)
-    wall = time.perf_counter() - t0
-    clk = clocks.stop()
+    e2e_ms = (time.perf_counter() - t0) / args.steps * 1e3
     n = int(off[-1])
     bytes_launch = n * (cfg["k"] * 8 + 8)
-    ms = wall / args.steps * 1e3
     peak, src = load_peaks()
     if rank == 0:
         print(json.dumps({
@@ -501,8 +501,8 @@ def run_hb(args, cfg):
             "group_evals_per_s": cfg["groups"] * 1000.0 / ms,
             "roofline": {"bound": "hbm", "achieved": bytes_launch / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": bytes_launch / (ms * 1e-3) / 1e9 / peak, "traffic": load_traffic(args.config),
-                         "note": "wall time incl. beta H2D and (f,g) D2H", "peak_source": src},
-            "e2e": {"value": 1000.0 / ms, "unit": "launches/s", "h2d_bytes_per_step": betas.nbytes,
+                         "peak_source": src},
+            "e2e": {"value": 1000.0 / e2e_ms, "unit": "launches/s", "h2d_bytes_per_step": betas.nbytes,
                     "d2h_bytes_per_step": 8 * cfg["groups"] * (cfg["k"] + 1)},
             "gpu_launches": args.steps, "clocks": clk,
             "cpu_baseline": None if args.no_cpu_baseline else cpu_baseline_other(args.config)}), flush=True)

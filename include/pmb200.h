@@ -161,6 +161,10 @@ PM_API int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64
 PM_API int pm_hb_eval(pm_hb_t h, const double* betas, const double* mu, const double* sigma,
                int want_grad, double* f_out, double* g_out);
 PM_API int pm_hb_stream(pm_hb_t h, void** stream);
+/* Benchmark helper: n back-to-back kernel launches on device-resident betas (uploaded once),
+ * bracketed by CUDA events on the handle's stream; *total_ms = elapsed device time. */
+PM_API int pm_hb_time_evals(pm_hb_t h, const double* betas, const double* mu, const double* sigma,
+                            int want_grad, int32_t n, float* total_ms);
 
 /* ------------------------------------------------------------------ lattice Gibbs
  * Replaces IsingLattice/ColorPartition/gibbs_sweep (ising.py:47-187) and adds the

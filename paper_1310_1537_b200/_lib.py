@@ -63,6 +63,7 @@ SIGNATURES = {
     "pm_hb_upload": (c_int, [c_void_p, _dp, _dp, _i64p, c_int32, c_int32]),
     "pm_hb_eval": (c_int, [c_void_p, _dp, _dp, _dp, c_int, _dp, _dp]),
     "pm_hb_stream": (c_int, [c_void_p, POINTER(c_void_p)]),
+    "pm_hb_time_evals": (c_int, [c_void_p, _dp, _dp, _dp, c_int, c_int32, POINTER(ctypes.c_float)]),
     "pm_lat_create": (c_int, [c_int, c_int32, c_int32, c_int, c_int, POINTER(c_void_p)]),
     "pm_lat_destroy": (c_int, [c_void_p]),
     "pm_lat_set_spins": (c_int, [c_void_p, _i8p]),

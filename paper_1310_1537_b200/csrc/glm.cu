@@ -845,10 +845,10 @@ int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64_t* off
   return PM_OK;
 }
 
-int pm_hb_eval(pm_hb_t h, const double* betas, const double* mu, const double* sigma, int want_grad, double* f_out,
-               double* g_out) {
-  if (!h || !betas || !f_out) return fail(PM_EINVAL, "null argument");
-  std::lock_guard<std::mutex> lk(h->mu);
+}  // extern "C"
+
+// validate, stage betas/prior on the device and build the kernel arguments (mutex held)
+static int hb_stage(pm_hb_t h, const double* betas, const double* mu, const double* sigma, HbArgs& a) {
   if (h->G == 0) return fail(PM_ESTATE, "no data uploaded");
   const int G = h->G, K = h->K;
   if (!all_finite(betas, int64_t(G) * K)) return fail(PM_EINVAL, "betas contain non-finite entries");
@@ -859,7 +859,6 @@ int pm_hb_eval(pm_hb_t h, const double* betas, const double* mu, const double* s
       if (!(sigma[k] > 0) || !std::isfinite(mu[k]) || !std::isfinite(sigma[k]))
         return fail(PM_EINVAL, "prior must be finite with sigma > 0");
   }
-  DeviceGuard gd(h->device);
   std::memcpy(h->pin_in, betas, sizeof(double) * size_t(G) * K);
   if (prior) {
     std::memcpy(h->pin_in + size_t(G) * K, mu, sizeof(double) * K);
@@ -872,7 +871,6 @@ int pm_hb_eval(pm_hb_t h, const double* betas, const double* mu, const double* s
     PM_CUDA(cudaMemcpyAsync(h->sigma_dev, h->pin_in + size_t(G) * K + K, sizeof(double) * K,
                             cudaMemcpyHostToDevice, h->stream));
   }
-  HbArgs a;
   a.X = h->X;
   a.y = h->y;
   a.poff = h->poff;
@@ -884,6 +882,20 @@ int pm_hb_eval(pm_hb_t h, const double* betas, const double* mu, const double* s
   a.sigma = prior ? h->sigma_dev : nullptr;
   a.out_f = h->out_f;
   a.out_g = h->out_g;
+  return PM_OK;
+}
+
+extern "C" {
+
+int pm_hb_eval(pm_hb_t h, const double* betas, const double* mu, const double* sigma, int want_grad, double* f_out,
+               double* g_out) {
+  if (!h || !betas || !f_out) return fail(PM_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard gd(h->device);
+  HbArgs a;
+  int rc = hb_stage(h, betas, mu, sigma, a);
+  if (rc) return rc;
+  const int G = h->G, K = h->K;
   const bool grad = want_grad != 0 && g_out != nullptr;
   HbLaunch fn = grad ? pick_hb<true>((K + 31) / 32) : pick_hb<false>((K + 31) / 32);
   cudaError_t e = fn(a, G, h->smem, h->stream);
@@ -901,6 +913,32 @@ int pm_hb_eval(pm_hb_t h, const double* betas, const double* mu, const double* s
 int pm_hb_stream(pm_hb_t h, void** stream) {
   if (!h || !stream) return fail(PM_EINVAL, "null argument");
   *stream = h->stream;
+  return PM_OK;
+}
+
+int pm_hb_time_evals(pm_hb_t h, const double* betas, const double* mu, const double* sigma, int want_grad,
+                     int32_t n, float* total_ms) {
+  if (!h || !betas || !total_ms) return fail(PM_EINVAL, "null argument");
+  if (n < 1) return fail(PM_EINVAL, "n must be >= 1");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard gd(h->device);
+  HbArgs a;
+  int rc = hb_stage(h, betas, mu, sigma, a);
+  if (rc) return rc;
+  HbLaunch fn = want_grad ? pick_hb<true>((h->K + 31) / 32) : pick_hb<false>((h->K + 31) / 32);
+  cudaEvent_t e0, e1;
+  PM_CUDA(cudaEventCreate(&e0));
+  PM_CUDA(cudaEventCreate(&e1));
+  PM_CUDA(cudaEventRecord(e0, h->stream));
+  for (int i = 0; i < n; ++i) {
+    cudaError_t e = fn(a, h->G, h->smem, h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "hb kernel launch");
+  }
+  PM_CUDA(cudaEventRecord(e1, h->stream));
+  PM_CUDA(cudaEventSynchronize(e1));
+  PM_CUDA(cudaEventElapsedTime(total_ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
   return PM_OK;
 }
 

@@ -129,6 +129,17 @@ class HbDevice:
                   int(want_grad), _lib.dptr(f), _lib.dptr(g))
         return f, g
 
+    def time_evals(self, betas, mu=None, sigma=None, n: int = 10, want_grad: bool = True) -> float:
+        """Device milliseconds of n back-to-back launches (CUDA events on the handle stream)."""
+        import ctypes as ct
+        betas = np.ascontiguousarray(betas, dtype=np.float64)
+        mu = None if mu is None else np.ascontiguousarray(mu, dtype=np.float64)
+        sigma = None if sigma is None else np.ascontiguousarray(sigma, dtype=np.float64)
+        ms = ct.c_float()
+        _lib.call("pm_hb_time_evals", self._h, _lib.dptr(betas), _lib.dptr(mu), _lib.dptr(sigma), int(want_grad),
+                  int(n), ct.byref(ms))
+        return float(ms.value)
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             _lib.load().pm_hb_destroy(self._h)
