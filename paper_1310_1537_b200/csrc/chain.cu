@@ -19,6 +19,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
 
 #include "glm_kernels.cuh"
 #include "philox.cuh"
@@ -79,14 +80,41 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
   const int64_t i0 = int64_t(blockIdx.x) * blockDim.x + tid;
 
   // One conditional log-likelihood pass for M deltas of coordinate k: out[m] = L(beta + d_m e_k).
-  auto pass = [&](int k, const double* d, int M, double* out) {
+  auto pass = [&](auto mtag, int k, const double* d, double* out) {
+    constexpr int M = decltype(mtag)::value;
     double acc[kChainMaxM] = {0.0, 0.0, 0.0};
     const double* xk = a.xt + int64_t(k) * a.ld;
     const double* xp = pend_k >= 0 ? a.xt + int64_t(pend_k) * a.ld : nullptr;
-    for (int64_t i = i0; i < a.n; i += stride) {
+    // 4 rows per step: all loads first, then 4 independent transcendental chains (ILP);
+    // the per-thread summation order is the same for every M (rows in ascending order)
+    constexpr int U = 4;
+    int64_t i = i0;
+    for (; i + (U - 1) * stride < a.n; i += U * stride) {
+      double xb[U], xv[U], yy[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t r = i + u * stride;
+        xb[u] = a.xbeta[r];
+        xv[u] = xk[r];
+        yy[u] = a.y[r];
+        if (xp) xb[u] = __dadd_rn(xb[u], __dmul_rn(pend_d, xp[r]));  // fused commit_update, glm.py:537
+      }
+      if (xp) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) a.xbeta[i + u * stride] = xb[u];
+      }
+      for (int m = 0; m < M; ++m) {
+        double t[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) t[u] = row_nll(shifted_t(xb[u], d[m], xv[u]), yy[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[m] += t[u];
+      }
+    }
+    for (; i < a.n; i += stride) {
       double xb = a.xbeta[i];
       if (xp) {
-        xb = __dadd_rn(xb, __dmul_rn(pend_d, xp[i]));  // fused commit_update, glm.py:537
+        xb = __dadd_rn(xb, __dmul_rn(pend_d, xp[i]));
         a.xbeta[i] = xb;
       }
       const double xv = xk[i], yy = a.y[i];
@@ -130,7 +158,7 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
       double left = __dsub_rn(x0, __dmul_rn(r, w));
       double right = __dadd_rn(left, w);
       double d3[3] = {0.0, __dsub_rn(left, x0), __dsub_rn(right, x0)}, ll3[3];
-      pass(k, d3, 3, ll3);
+      pass(std::integral_constant<int, 3>{}, k, d3, ll3);
       const double f0 = post(x0, ll3[0]);
       evals += 1;
       const double level = __dadd_rn(f0, log(__dsub_rn(1.0, u_level)));
@@ -146,7 +174,7 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
           break;
         }
         double dd = __dsub_rn(left, x0), ll;
-        pass(k, &dd, 1, &ll);
+        pass(std::integral_constant<int, 1>{}, k, &dd, &ll);
         fl = post(left, ll);
         evals += 1;
       }
@@ -162,7 +190,7 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
           break;
         }
         double dd = __dsub_rn(right, x0), ll;
-        pass(k, &dd, 1, &ll);
+        pass(std::integral_constant<int, 1>{}, k, &dd, &ll);
         fr = post(right, ll);
         evals += 1;
       }
@@ -174,7 +202,7 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
         const double u = uniform_at(a, pos++);
         x1 = __dadd_rn(left, __dmul_rn(u, __dsub_rn(right, left)));
         double dd = __dsub_rn(x1, x0), ll;
-        pass(k, &dd, 1, &ll);
+        pass(std::integral_constant<int, 1>{}, k, &dd, &ll);
         const double f1 = post(x1, ll);
         evals += 1;
         if (f1 > level) {

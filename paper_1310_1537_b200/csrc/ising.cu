@@ -162,7 +162,7 @@ template <int MODEL>
 __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const unsigned long long* s_thr, int i, int q0);
 
 template <int MODEL>
-__global__ void __launch_bounds__(256) gibbs_packed_kernel(PackedArgs a, const unsigned long long* __restrict__ pthr) {
+__global__ void __launch_bounds__(256, 6) gibbs_packed_kernel(PackedArgs a, const unsigned long long* __restrict__ pthr) {
   __shared__ unsigned long long s_thr[MODEL == PM_MODEL_ISING ? 5 : kPottsIdx * 3];
   if (MODEL == PM_MODEL_ISING) {
     // indexed by the number of -1 neighbours nd = 0..4 (nsum = 4 - 2 nd); static indices
