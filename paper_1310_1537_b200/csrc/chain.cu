@@ -15,6 +15,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -61,6 +62,7 @@ __device__ __forceinline__ double logprior(const ChainArgs& a, int k, double v) 
   return __dmul_rn(__dmul_rn(-0.5, z), z);
 }
 
+template <int U>
 __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sbeta[];  // [K]
@@ -85,9 +87,8 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
     double acc[kChainMaxM] = {0.0, 0.0, 0.0};
     const double* xk = a.xt + int64_t(k) * a.ld;
     const double* xp = pend_k >= 0 ? a.xt + int64_t(pend_k) * a.ld : nullptr;
-    // 4 rows per step: all loads first, then 4 independent transcendental chains (ILP);
+    // U rows per step: all loads first, then U independent transcendental chains (ILP);
     // the per-thread summation order is the same for every M (rows in ascending order)
-    constexpr int U = 4;
     int64_t i = i0;
     for (; i + (U - 1) * stride < a.n; i += U * stride) {
       double xb[U], xv[U], yy[U];
@@ -281,10 +282,18 @@ int pm_ws_run_chain(pm_ws_t ws, const double* mu, const double* sigma, int32_t n
   DeviceGuard g(v.device);
   cudaStream_t st = static_cast<cudaStream_t>(v.stream);
   const size_t smem = sizeof(double) * size_t(v.K);
+  // tuning knobs (defaults measured on B200): rows per ILP batch and CTAs per SM
+  const char* eu = std::getenv("PM_CHAIN_UNROLL");
+  const char* eb = std::getenv("PM_CHAIN_BLOCKS_PER_SM");
+  const int unroll = eu ? std::atoi(eu) : 1;
+  const int want_per_sm = eb ? std::max(1, std::atoi(eb)) : 2;
+  void* kfn = unroll >= 4 ? reinterpret_cast<void*>(chain_kernel<4>)
+                          : (unroll == 2 ? reinterpret_cast<void*>(chain_kernel<2>)
+                                         : reinterpret_cast<void*>(chain_kernel<1>));
   int per_sm = 0;
-  PM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chain_kernel, kChainThreads, smem));
+  PM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kChainThreads, smem));
   if (per_sm < 1) return fail(PM_EDEVICE, "chain kernel cannot be resident");
-  const int grid = std::max(1, std::min(v.sms * std::min(per_sm, 2),
+  const int grid = std::max(1, std::min(v.sms * std::min(per_sm, want_per_sm),
                                         int((v.n + kChainThreads - 1) / kChainThreads)));
   const int kept = n_iter - n_burnin;
   double* dbuf = nullptr;
@@ -328,8 +337,7 @@ int pm_ws_run_chain(pm_ws_t ws, const double* mu, const double* sigma, int32_t n
   a.out_evals = d_evals;
   a.status = d_status;
   void* kargs[] = {&a};
-  PM_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(chain_kernel), dim3(grid), dim3(kChainThreads), kargs,
-                                      smem, st));
+  PM_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kChainThreads), kargs, smem, st));
   unsigned long long pos = 0;
   long long evals = 0;
   int status[2] = {0, -1};
