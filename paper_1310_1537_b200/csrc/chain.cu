@@ -285,7 +285,7 @@ int pm_ws_run_chain(pm_ws_t ws, const double* mu, const double* sigma, int32_t n
   // tuning knobs (defaults measured on B200): rows per ILP batch and CTAs per SM
   const char* eu = std::getenv("PM_CHAIN_UNROLL");
   const char* eb = std::getenv("PM_CHAIN_BLOCKS_PER_SM");
-  const int unroll = eu ? std::atoi(eu) : 1;
+  const int unroll = eu ? std::atoi(eu) : 2;
   const int want_per_sm = eb ? std::max(1, std::atoi(eb)) : 2;
   void* kfn = unroll >= 4 ? reinterpret_cast<void*>(chain_kernel<4>)
                           : (unroll == 2 ? reinterpret_cast<void*>(chain_kernel<2>)
