@@ -230,6 +230,10 @@ PM_API int pm_lat_strip_half_sweep(pm_lat_t h, int colour, uint64_t seed, uint64
  * 1..rows = own rows, rows+1 = bottom halo. */
 PM_API int pm_lat_strip_row(pm_lat_t h, int colour, int32_t array_row, void** dev_ptr);
 
+/* Host evaluation of the kernels' per-row logistic terms (the same pm_math.cuh code the
+ * device runs, bit for bit): nll = (1-y)t + softplus(-t), w = y - sigmoid(t).  For tests. */
+PM_API int pm_row_terms_host(const double* t, const double* y, int64_t n, double* nll_out, double* w_out);
+
 /* Host-side table builders, exported so tests can check them against the oracle. */
 PM_API int pm_ising_prob_table(double w, double b, double* p_out /*9: nsum=-4..4*/);
 PM_API int pm_potts_cdf_table(double coupling, double* cdf_out /*625*3*/);

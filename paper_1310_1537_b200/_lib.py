@@ -78,6 +78,7 @@ SIGNATURES = {
     "pm_lat_create_strip": (c_int, [c_int, c_int32, c_int32, c_int32, c_int32, c_int, POINTER(c_void_p)]),
     "pm_lat_strip_half_sweep": (c_int, [c_void_p, c_int, c_uint64, c_uint64, c_void_p]),
     "pm_lat_strip_row": (c_int, [c_void_p, c_int, c_int32, POINTER(c_void_p)]),
+    "pm_row_terms_host": (c_int, [_dp, _dp, c_int64, _dp, _dp]),
     "pm_ising_prob_table": (c_int, [c_double, c_double, _dp]),
     "pm_potts_cdf_table": (c_int, [c_double, _dp]),
 }

@@ -15,6 +15,7 @@
 #pragma once
 
 #include "pm_internal.cuh"
+#include "pm_math.cuh"
 
 namespace pm {
 
@@ -28,12 +29,9 @@ struct BetaPack {
 // Per-row stable terms, identical algebra to _nll_sum (glm.py:186-192) and expit.
 //   nll = (1-y) t + max(-t,0) + log1p(exp(-|t|))       (the reference's f is -sum nll)
 //   w   = y - sigmoid(t)                                (glm.py:371)
+// (lean fp64 exp/log1p/reciprocal of pm_math.cuh: <= 2 ulp, no special-case paths)
 __device__ __forceinline__ void row_terms(double t, double y, double& nll, double& w) {
-  const double e = exp(-fabs(t));
-  nll = (1.0 - y) * t + fmax(-t, 0.0) + log1p(e);
-  const double inv = 1.0 / (1.0 + e);
-  const double sig = (t >= 0.0) ? inv : e * inv;
-  w = y - sig;
+  pm_row_terms(t, y, nll, w);
 }
 
 // Rounding identical to numpy's `xbeta + delta*xk` (glm.py:517/537): product rounded, then sum.
@@ -42,10 +40,7 @@ __device__ __forceinline__ double shifted_t(double xb, double d, double xk) {
 }
 
 // nll term only (diff_loglike, glm.py:499-522)
-__device__ __forceinline__ double row_nll(double t, double y) {
-  const double e = exp(-fabs(t));
-  return (1.0 - y) * t + fmax(-t, 0.0) + log1p(e);
-}
+__device__ __forceinline__ double row_nll(double t, double y) { return pm_row_nll(t, y); }
 
 // v[r] holds this lane's partial dot product for sub-tile row r (R rows).  Returns, in lane l,
 // the full (all-lane) dot product of row l & (R-1): log2(R) transpose-halving steps, then a

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "pm_internal.cuh"
+#include "pm_math.cuh"
 
 namespace pm {
 
@@ -56,6 +57,12 @@ cudaError_t ensure_smem_attr(const void* kernel, std::atomic<uint64_t>& mask) {
 extern "C" {
 
 int pm_abi_version(void) { return PM_ABI_VERSION; }
+
+int pm_row_terms_host(const double* t, const double* y, int64_t n, double* nll_out, double* w_out) {
+  if (!t || !y || !nll_out || !w_out) return pm::fail(PM_EINVAL, "null argument");
+  for (int64_t i = 0; i < n; ++i) pm::pm_row_terms(t[i], y[i], nll_out[i], w_out[i]);
+  return PM_OK;
+}
 
 const char* pm_last_error(void) { return pm::g_last_error.c_str(); }
 
