@@ -18,6 +18,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "philox.cuh"
@@ -158,66 +159,96 @@ __device__ __forceinline__ uint32_t pow5_bytes(uint32_t x) {
   return __byte_perm(0x7D190501u, 0u, sel);              // bytes {1, 5, 25, 125}[s]
 }
 
-template <int MODEL>
-__device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const unsigned long long* s_thr, int i, int q0);
+// Threshold tables in shared memory.  T32: every threshold ceil(p*2^32) is < 2^32 (checked on
+// the host), so the exact test u < p is the 32-bit compare word < T; otherwise 64-bit.
+template <int MODEL, bool T32>
+struct GibbsTables {
+  // Ising: by number of -1 neighbours nd = 0..4 (nsum = 4 - 2 nd)
+  // Potts: by idx = sum of 5^state over the 4 neighbours; T32 packs the 3 thresholds in a uint4
+  using IsingT = typename std::conditional<T32, uint32_t, unsigned long long>::type;
+  typename std::conditional<MODEL == PM_MODEL_ISING, IsingT[8],
+                            typename std::conditional<T32, uint4[kPottsIdx], unsigned long long[kPottsIdx * 3]>::type>::type
+      t;
+};
 
-template <int MODEL>
-__global__ void __launch_bounds__(256, 6) gibbs_packed_kernel(PackedArgs a, const unsigned long long* __restrict__ pthr) {
-  __shared__ unsigned long long s_thr[MODEL == PM_MODEL_ISING ? 5 : kPottsIdx * 3];
-  if (MODEL == PM_MODEL_ISING) {
-    // indexed by the number of -1 neighbours nd = 0..4 (nsum = 4 - 2 nd); static indices
-    // into the parameter array (a dynamic index would copy the params to local memory)
-    if (threadIdx.x == 0) {
+// Thread = NG consecutive 16-site groups of one packed row (setup amortised over 16*NG sites).
+template <int MODEL, bool T32, int NG>
+__device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const GibbsTables<MODEL, T32>& tb, int r,
+                                                 int q0);
+
+template <int MODEL, bool T32, int NG>
+__global__ void __launch_bounds__(256, NG == 1 ? 6 : 4)
+    gibbs_packed_kernel(PackedArgs a, const unsigned long long* __restrict__ pthr, const uint4* __restrict__ pthr32) {
+  __shared__ GibbsTables<MODEL, T32> tb;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  if constexpr (MODEL == PM_MODEL_ISING) {
+    // static indices into the parameter array (a dynamic index would copy the params to local memory)
+    if (tid == 0) {
 #pragma unroll
-      for (int k = 0; k < 5; ++k) s_thr[k] = a.thr[8 - 2 * k];
+      for (int k = 0; k < 5; ++k) tb.t[k] = a.thr[8 - 2 * k];
     }
+  } else if constexpr (T32) {
+    uint4* dst = reinterpret_cast<uint4*>(&tb.t[0]);
+    for (int t = tid; t < kPottsIdx; t += blockDim.x * blockDim.y) dst[t] = pthr32[t];
   } else {
-    for (int t = threadIdx.x; t < kPottsIdx * 3; t += blockDim.x) s_thr[t] = pthr[t];
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&tb.t[0]);
+    for (int t = tid; t < kPottsIdx * 3; t += blockDim.x * blockDim.y) dst[t] = pthr[t];
   }
   __syncthreads();
-  // 2-D grid: x = 16-site column groups of a row, y = rows (no integer division)
-  const int per_row = a.W2 >> 4;
+  // 2-D grid of 2-D blocks: x = (16*NG)-site column groups of a row, y = rows
+  const int per_row = a.W2 / (16 * NG);
   const int cgrp = blockIdx.x * blockDim.x + threadIdx.x;
   if (cgrp >= per_row) return;
-  for (int r = blockIdx.y; r < a.rows; r += gridDim.y) {
-    gibbs_packed_row<MODEL>(a, s_thr, r, cgrp << 4);
+  for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < a.rows; r += gridDim.y * blockDim.y) {
+    gibbs_packed_row<MODEL, T32, NG>(a, tb, r, cgrp * 16 * NG);
   }
 }
 
-template <int MODEL>
-__device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const unsigned long long* s_thr, int r, int q0) {
+template <int MODEL, bool T32, int NG>
+__device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const GibbsTables<MODEL, T32>& tb, int r,
+                                                 int q0) {
+  constexpr int NW = 4 * NG;   // 32-bit words (4 sites each) handled by this thread
   const int li = r + a.halo;   // array row
   const int i = a.row0 + r;    // global row: colour parity and RNG site index
   const int iu = a.halo ? li - 1 : (li == 0 ? a.rows - 1 : li - 1);
   const int id = a.halo ? li + 1 : (li == a.rows - 1 ? 0 : li + 1);
   const int8_t* orow = a.other + int64_t(li) * a.W2;
-  const uint4 up = ld16(a.other + int64_t(iu) * a.W2 + q0);
-  const uint4 dn = ld16(a.other + int64_t(id) * a.W2 + q0);
-  const uint4 mid = ld16(orow + q0);
+  const int8_t* urow = a.other + int64_t(iu) * a.W2;
+  const int8_t* drow = a.other + int64_t(id) * a.W2;
+  uint32_t U[NW], D[NW], M[NW];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    const uint4 u4 = ld16(urow + q0 + 16 * g), d4 = ld16(drow + q0 + 16 * g), m4 = ld16(orow + q0 + 16 * g);
+    U[4 * g] = u4.x, U[4 * g + 1] = u4.y, U[4 * g + 2] = u4.z, U[4 * g + 3] = u4.w;
+    D[4 * g] = d4.x, D[4 * g + 1] = d4.y, D[4 * g + 2] = d4.z, D[4 * g + 3] = d4.w;
+    M[4 * g] = m4.x, M[4 * g + 1] = m4.y, M[4 * g + 2] = m4.z, M[4 * g + 3] = m4.w;
+  }
   // o = 0: horizontal neighbours of packed site q are q-1 and q; o = 1: q and q+1
   const int o = (i + a.colour) & 1;
-  const uint32_t edge = o ? uint32_t(uint8_t(__ldg(orow + ((q0 + 16 == a.W2) ? 0 : q0 + 16))))
-                          : uint32_t(uint8_t(__ldg(orow + ((q0 == 0) ? a.W2 - 1 : q0 - 1))));
-  const uint64_t s0 = uint64_t(a.colour) * uint64_t(a.n0) + uint64_t(i) * a.W2 + q0;
-  uint32_t res[4];
+  const int qe = o ? ((q0 + 16 * NG == a.W2) ? 0 : q0 + 16 * NG) : ((q0 == 0) ? a.W2 - 1 : q0 - 1);
+  const uint32_t edge = uint32_t(uint8_t(__ldg(orow + qe)));
+  const uint64_t g0 = (uint64_t(a.colour) * uint64_t(a.n0) + uint64_t(i) * a.W2 + q0) >> 2;  // Philox block
+  uint32_t res[NW];
 #pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    const uint32_t cur = w_of(mid, m);
+  for (int m = 0; m < NW; ++m) {
+    const uint32_t cur = M[m];
     // byte b of `sh` = the other horizontal neighbour of site 4m+b (funnel shift across words)
-    const uint32_t sh = o == 0 ? __funnelshift_l(m == 0 ? (edge << 24) : w_of(mid, m - 1), cur, 8)
-                               : __funnelshift_r(cur, m == 3 ? edge : w_of(mid, m + 1), 8);
-    const U32x4 blk = site_philox_block((s0 >> 2) + m, a.sweep, a.seed);
+    const uint32_t sh = o == 0 ? __funnelshift_l(m == 0 ? (edge << 24) : M[m - 1], cur, 8)
+                               : __funnelshift_r(cur, m == NW - 1 ? edge : M[m + 1], 8);
+    const U32x4 blk = site_philox_block(g0 + m, a.sweep, a.seed);
     uint32_t out = 0;
-    if (MODEL == PM_MODEL_ISING) {
-      const uint32_t nd = down_bits(w_of(up, m)) + down_bits(w_of(dn, m)) + down_bits(cur) + down_bits(sh);
+    if constexpr (MODEL == PM_MODEL_ISING) {
+      const uint32_t nd = down_bits(U[m]) + down_bits(D[m]) + down_bits(cur) + down_bits(sh);
+      uint32_t plus_bits = 0;  // bit 8b set <=> site b becomes +1
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        const uint32_t k = (nd >> (8 * b)) & 0xFFu;
-        const bool plus = uint64_t(blk.v[b]) < s_thr[k];
-        out |= (plus ? 0x01u : 0xFFu) << (8 * b);
+        const uint32_t k = __byte_perm(nd, 0u, 0x4440u + b);
+        const bool plus = T32 ? (blk.v[b] < uint32_t(tb.t[k])) : (uint64_t(blk.v[b]) < uint64_t(tb.t[k]));
+        plus_bits |= plus ? (1u << (8 * b)) : 0u;
       }
+      out = 0xFFFFFFFFu - 0xFEu * plus_bits;  // per byte: 0x01 (+1) or 0xFF (-1), no borrows
     } else {
-      const uint32_t p1 = pow5_bytes(w_of(up, m)), p2 = pow5_bytes(w_of(dn, m));
+      const uint32_t p1 = pow5_bytes(U[m]), p2 = pow5_bytes(D[m]);
       const uint32_t p3 = pow5_bytes(cur), p4 = pow5_bytes(sh);
       // two 16-bit lanes per word so the sums (<= 500) cannot overflow
       const uint32_t ev = (p1 & 0x00FF00FFu) + (p2 & 0x00FF00FFu) + (p3 & 0x00FF00FFu) + (p4 & 0x00FF00FFu);
@@ -226,15 +257,24 @@ __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const unsi
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const uint32_t idx = ((b & 1) ? od : ev) >> (16 * (b >> 1)) & 0xFFFFu;
-        const unsigned long long* t3 = s_thr + idx * 3;
-        const uint64_t w = blk.v[b];
-        const uint32_t st = uint32_t(w >= t3[0]) + uint32_t(w >= t3[1]) + uint32_t(w >= t3[2]);
+        const uint32_t w = blk.v[b];
+        uint32_t st;
+        if constexpr (T32) {
+          const uint4 th = reinterpret_cast<const uint4*>(&tb.t[0])[idx];
+          st = uint32_t(w >= th.x) + uint32_t(w >= th.y) + uint32_t(w >= th.z);
+        } else {
+          const unsigned long long* t3 = reinterpret_cast<const unsigned long long*>(&tb.t[0]) + idx * 3;
+          st = uint32_t(uint64_t(w) >= t3[0]) + uint32_t(uint64_t(w) >= t3[1]) + uint32_t(uint64_t(w) >= t3[2]);
+        }
         out |= st << (8 * b);
       }
     }
     res[m] = out;
   }
-  *reinterpret_cast<uint4*>(a.mine + int64_t(li) * a.W2 + q0) = make_uint4(res[0], res[1], res[2], res[3]);
+#pragma unroll
+  for (int g = 0; g < NG; ++g)
+    *reinterpret_cast<uint4*>(a.mine + int64_t(li) * a.W2 + q0 + 16 * g) =
+        make_uint4(res[4 * g], res[4 * g + 1], res[4 * g + 2], res[4 * g + 3]);
 }
 
 // ---------------------------------------------------------------- layout conversion
@@ -320,6 +360,8 @@ struct pm_lat_s {
   bool has_potts = false;
   double* cdf = nullptr;
   unsigned long long* pthr = nullptr;
+  uint4* pthr32 = nullptr;    // Potts thresholds as (t0, t1, t2, 0) when all < 2^32
+  bool t32 = false;           // every threshold of the active model fits 32 bits
   // uniforms staging
   double* uni = nullptr;
   size_t uni_cap = 0;
@@ -329,8 +371,9 @@ namespace {
 
 void free_lat(pm_lat_s* h) {
   for (void* p : {(void*)h->pk0, (void*)h->pk1, (void*)h->scratch, (void*)h->cls, (void*)h->ptab, (void*)h->cdf,
-                  (void*)h->pthr, (void*)h->uni})
+                  (void*)h->pthr, (void*)h->pthr32, (void*)h->uni})
     if (p) cudaFree(p);
+  h->pthr32 = nullptr;
   h->pk0 = h->pk1 = h->scratch = nullptr;
   h->cls = nullptr;
   h->ptab = h->cdf = h->uni = nullptr;
@@ -504,7 +547,11 @@ int pm_lat_set_ising(pm_lat_t h, double w, const double* bias) {
   }
   h->n_class = int(cls.empty() ? 1 : uniq.size());
   h->w = w;
-  for (int t = 0; t < 9; ++t) h->thr[t] = thr32(tab[t]);
+  h->t32 = true;
+  for (int t = 0; t < 9; ++t) {
+    h->thr[t] = thr32(tab[t]);
+    if (h->thr[t] > 0xFFFFFFFFull) h->t32 = false;  // p == 1: the 32-bit compare cannot express it
+  }
   h->has_field = true;
   return PM_OK;
 }
@@ -516,14 +563,24 @@ int pm_lat_set_potts(pm_lat_t h, double coupling) {
   std::vector<double> cdf(kPottsIdx * 3);
   potts_cdf(coupling, cdf.data());
   std::vector<unsigned long long> thr(kPottsIdx * 3);
-  for (int t = 0; t < kPottsIdx * 3; ++t) thr[t] = thr32(cdf[t]);
+  bool fits = true;
+  for (int t = 0; t < kPottsIdx * 3; ++t) {
+    thr[t] = thr32(cdf[t]);
+    if (thr[t] > 0xFFFFFFFFull) fits = false;
+  }
+  std::vector<uint4> t4(kPottsIdx);
+  for (int i = 0; i < kPottsIdx; ++i)
+    t4[i] = make_uint4(uint32_t(thr[3 * i]), uint32_t(thr[3 * i + 1]), uint32_t(thr[3 * i + 2]), 0u);
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard g(h->device);
   cudaStreamSynchronize(h->stream);
   if (!h->cdf) PM_CUDA(cudaMalloc(&h->cdf, sizeof(double) * kPottsIdx * 3));
   if (!h->pthr) PM_CUDA(cudaMalloc(&h->pthr, sizeof(unsigned long long) * kPottsIdx * 3));
+  if (!h->pthr32) PM_CUDA(cudaMalloc(&h->pthr32, sizeof(uint4) * kPottsIdx));
   PM_CUDA(cudaMemcpy(h->cdf, cdf.data(), sizeof(double) * kPottsIdx * 3, cudaMemcpyHostToDevice));
   PM_CUDA(cudaMemcpy(h->pthr, thr.data(), sizeof(unsigned long long) * kPottsIdx * 3, cudaMemcpyHostToDevice));
+  PM_CUDA(cudaMemcpy(h->pthr32, t4.data(), sizeof(uint4) * kPottsIdx, cudaMemcpyHostToDevice));
+  h->t32 = fits;
   h->has_potts = true;
   return PM_OK;
 }
@@ -547,13 +604,30 @@ static void launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t seed, cud
   pa.row0 = h->row0;
   pa.rows = h->H;
   pa.halo = h->strip;
-  const int per_row = h->W / 2 / 16;
-  const int bx = std::min(256, (per_row + 31) / 32 * 32);
-  const dim3 grid((per_row + bx - 1) / bx, std::min(h->H, 65535));
-  if (h->model == PM_MODEL_ISING)
-    gibbs_packed_kernel<PM_MODEL_ISING><<<grid, bx, 0, st>>>(pa, nullptr);
-  else
-    gibbs_packed_kernel<PM_MODEL_POTTS4><<<grid, bx, 0, st>>>(pa, h->pthr);
+  const int W2 = h->W / 2;
+  const int ng = (W2 % 64 == 0) ? 4 : (W2 % 32 == 0) ? 2 : 1;   // 16-site groups per thread
+  const int per_row = W2 / (16 * ng);
+  const int bx = std::min(256, per_row);
+  const int by = std::max(1, 256 / bx);
+  const dim3 block(bx, by);
+  const dim3 grid((per_row + bx - 1) / bx, std::min((h->H + by - 1) / by, 65535));
+  const bool ising = h->model == PM_MODEL_ISING;
+#define PM_LAUNCH_PACKED(M, T, N) gibbs_packed_kernel<M, T, N><<<grid, block, 0, st>>>(pa, h->pthr, h->pthr32)
+#define PM_LAUNCH_NG(M, T)            \
+  do {                                \
+    if (ng == 4)                      \
+      PM_LAUNCH_PACKED(M, T, 4);      \
+    else if (ng == 2)                 \
+      PM_LAUNCH_PACKED(M, T, 2);      \
+    else                              \
+      PM_LAUNCH_PACKED(M, T, 1);      \
+  } while (0)
+  if (ising && h->t32) PM_LAUNCH_NG(PM_MODEL_ISING, true);
+  else if (ising) PM_LAUNCH_NG(PM_MODEL_ISING, false);
+  else if (h->t32) PM_LAUNCH_NG(PM_MODEL_POTTS4, true);
+  else PM_LAUNCH_NG(PM_MODEL_POTTS4, false);
+#undef PM_LAUNCH_NG
+#undef PM_LAUNCH_PACKED
 }
 
 int pm_lat_create_strip(int device, int32_t height, int32_t width, int32_t row0, int32_t rows, int model,
