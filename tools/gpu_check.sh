@@ -14,7 +14,7 @@ if [ "${BENCH:-1}" = "1" ]; then
   timeout 900 python bench.py > gpurun_out/bench_c1.log 2>&1; echo "bench rc=$?" >> gpurun_out/rc.txt
 fi
 if [ "${EXTRA:-1}" = "1" ]; then
-  for c in c1f32 c0 c3 c4 c4potts; do
+  for c in c1f32 c0 c2 c3 c4 c4potts; do
     timeout 600 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_$c.log 2>&1; echo "bench $c rc=$?" >> gpurun_out/rc.txt
   done
 fi
