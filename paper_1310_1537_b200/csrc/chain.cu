@@ -15,6 +15,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -31,7 +32,7 @@ using namespace pm;
 namespace {
 
 constexpr int kChainThreads = 256;
-constexpr int kChainMaxM = 3;
+constexpr int kChainMaxM = 9;  // deltas per pass (3 + kSpecFirst)
 
 struct ChainArgs {
   double* xbeta;
@@ -62,15 +63,21 @@ __device__ __forceinline__ double logprior(const ChainArgs& a, int k, double v) 
   return __dmul_rn(__dmul_rn(-0.5, z), z);
 }
 
+constexpr int kSpecFirst = 6;   // shrink candidates evaluated with f0/left/right in the first pass
+constexpr int kSpecNext = 4;    // shrink candidates per later pass
+
 template <int U>
 __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sbeta[];  // [K]
   __shared__ double red[kChainThreads / 32][kChainMaxM];
   __shared__ double tot_s[kChainMaxM];
+  __shared__ double ubuf[32];        // uniforms of stream indices ubase .. ubase+31
+  __shared__ uint64_t ubase_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x;
   for (int k = tid; k < a.K; k += blockDim.x) sbeta[k] = a.beta[k];
+  if (tid == 0) ubase_s = ~0ull;
   __syncthreads();
 
   uint64_t pos = a.pos0;
@@ -81,10 +88,29 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
   const int64_t stride = int64_t(G) * blockDim.x;
   const int64_t i0 = int64_t(blockIdx.x) * blockDim.x + tid;
 
+  // Uniform of stream index idx (numpy Philox DeviateBuffer stream).  Every thread of the CTA
+  // calls this with the same idx at the same point; warp 0 refills 32 consecutive uniforms.
+  auto getu = [&](uint64_t idx) -> double {
+    const uint64_t base = ubase_s;
+    if (base == ~0ull || idx < base || idx >= base + 32) {
+      __syncthreads();
+      if (warp == 0) ubuf[lane] = uniform_at(a, idx + lane);
+      if (tid == 0) ubase_s = idx;
+      __syncthreads();
+      return ubuf[0];
+    }
+    return ubuf[idx - base];
+  };
+
   // One conditional log-likelihood pass for M deltas of coordinate k: out[m] = L(beta + d_m e_k).
   auto pass = [&](auto mtag, int k, const double* d, double* out) {
     constexpr int M = decltype(mtag)::value;
-    double acc[kChainMaxM] = {0.0, 0.0, 0.0};
+    double acc[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) acc[m] = 0.0;
+    double dm[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) dm[m] = d[m];
     const double* xk = a.xt + int64_t(k) * a.ld;
     const double* xp = pend_k >= 0 ? a.xt + int64_t(pend_k) * a.ld : nullptr;
     // U rows per step: all loads first, then U independent transcendental chains (ILP);
@@ -104,10 +130,11 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
 #pragma unroll
         for (int u = 0; u < U; ++u) a.xbeta[i + u * stride] = xb[u];
       }
+#pragma unroll
       for (int m = 0; m < M; ++m) {
         double t[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) t[u] = row_nll(shifted_t(xb[u], d[m], xv[u]), yy[u]);
+        for (int u = 0; u < U; ++u) t[u] = row_nll(shifted_t(xb[u], dm[m], xv[u]), yy[u]);
 #pragma unroll
         for (int u = 0; u < U; ++u) acc[m] += t[u];
       }
@@ -119,9 +146,11 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
         a.xbeta[i] = xb;
       }
       const double xv = xk[i], yy = a.y[i];
-      for (int m = 0; m < M; ++m) acc[m] += row_nll(shifted_t(xb, d[m], xv), yy);
+#pragma unroll
+      for (int m = 0; m < M; ++m) acc[m] += row_nll(shifted_t(xb, dm[m], xv), yy);
     }
     pend_k = -1;
+#pragma unroll
     for (int m = 0; m < M; ++m) {
       const double s = warp_sum(acc[m]);
       if (lane == 0) red[warp][m] = s;
@@ -133,15 +162,15 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
       a.partials[(size_t(parity) * G + blockIdx.x) * kChainMaxM + tid] = s;
     }
     grid.sync();
-    if (warp == 0) {  // every CTA folds all CTA partials in the same fixed order
-      for (int m = 0; m < M; ++m) {
-        double p = 0.0;
-        for (int b = lane; b < G; b += 32) p += __ldcg(a.partials + (size_t(parity) * G + b) * kChainMaxM + m);
-        p = warp_sum(p);
-        if (lane == 0) tot_s[m] = -p;
-      }
+    // every CTA folds all CTA partials in the same fixed order: warp w folds delta m = w, w+8..
+    for (int m = warp; m < M; m += kChainThreads / 32) {
+      double p = 0.0;
+      for (int b = lane; b < G; b += 32) p += __ldcg(a.partials + (size_t(parity) * G + b) * kChainMaxM + m);
+      p = warp_sum(p);
+      if (lane == 0) tot_s[m] = -p;
     }
     __syncthreads();
+#pragma unroll
     for (int m = 0; m < M; ++m) out[m] = tot_s[m];
     __syncthreads();
     parity ^= 1;
@@ -151,23 +180,47 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
   for (int it = 0; it < a.n_iter && !status; ++it) {
     for (int k = 0; k < a.K && !status; ++k) {
       const double x0 = sbeta[k];
+      const double tiny = __dmul_rn(1e-12, __dadd_rn(1.0, fabs(x0)));
       // log_posterior_coord(ws, data, prior, k, x - x0) = ll + logpdf(k, beta_k + (x - x0))
       auto post = [&](double x, double ll) { return __dadd_rn(ll, logprior(a, k, __dadd_rn(x0, __dsub_rn(x, x0)))); };
-      const double u_level = uniform_at(a, pos++);
+      // Shrink candidates from (L, R) starting at stream index p, each assuming the previous
+      // one was rejected: after a rejection the new interval depends only on x1 < x0
+      // (sampler.py:156-162), so the sequence is known before any comparison.
+      auto build = [&](double L, double R, uint64_t p, int nmax, double* cand) -> int {
+        int n = 0;
+        while (n < nmax) {
+          const double x1 = __dadd_rn(L, __dmul_rn(getu(p + n), __dsub_rn(R, L)));
+          cand[n++] = x1;
+          if (x1 < x0) L = x1; else R = x1;
+          if (__dsub_rn(R, L) < tiny) break;  // the scan ends here whatever the outcome
+        }
+        return n;
+      };
+      const double u_level = getu(pos);
       const double w = a.width;
-      const double r = uniform_at(a, pos++);
+      const double r = getu(pos + 1);
+      pos += 2;
       double left = __dsub_rn(x0, __dmul_rn(r, w));
       double right = __dadd_rn(left, w);
-      double d3[3] = {0.0, __dsub_rn(left, x0), __dsub_rn(right, x0)}, ll3[3];
-      pass(std::integral_constant<int, 3>{}, k, d3, ll3);
-      const double f0 = post(x0, ll3[0]);
+      // pass 1: f0, left_0, right_0 and kSpecFirst shrink candidates (assuming no stepping-out)
+      double cand[kSpecFirst > kSpecNext ? kSpecFirst : kSpecNext];
+      const int n1 = build(left, right, pos, kSpecFirst, cand);
+      double d1[3 + kSpecFirst], ll1[3 + kSpecFirst];
+      d1[0] = 0.0;
+      d1[1] = __dsub_rn(left, x0);
+      d1[2] = __dsub_rn(right, x0);
+      for (int j = 0; j < kSpecFirst; ++j) d1[3 + j] = j < n1 ? __dsub_rn(cand[j], x0) : 0.0;
+      pass(std::integral_constant<int, 3 + kSpecFirst>{}, k, d1, ll1);
+      const double f0 = post(x0, ll1[0]);
       evals += 1;
       const double level = __dadd_rn(f0, log(__dsub_rn(1.0, u_level)));
       // stepping out (sampler.py:138-150)
-      double fl = post(left, ll3[1]);
+      bool stepped = false;
+      double fl = post(left, ll1[1]);
       evals += 1;
       int steps = 0;
       while (fl > level) {
+        stepped = true;
         left = __dsub_rn(left, w);
         if (++steps > a.max_steps) {
           status = 1;
@@ -180,10 +233,11 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
         evals += 1;
       }
       if (status) break;
-      double fr = post(right, ll3[2]);
+      double fr = post(right, ll1[2]);
       evals += 1;
       steps = 0;
       while (fr > level) {
+        stepped = true;
         right = __dadd_rn(right, w);
         if (++steps > a.max_steps) {
           status = 1;
@@ -196,15 +250,24 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
         evals += 1;
       }
       if (status) break;
-      // shrinkage (sampler.py:152-164)
+      // shrinkage (sampler.py:152-164), candidates consumed in order from speculative batches
+      int avail = stepped ? 0 : n1, j = 0;
+      double llc[kSpecFirst > kSpecNext ? kSpecFirst : kSpecNext];
+      for (int q = 0; q < n1; ++q) llc[q] = ll1[3 + q];
       double x1 = x0;
       bool accepted = false;
       for (int s = 0; s < 1000; ++s) {
-        const double u = uniform_at(a, pos++);
-        x1 = __dadd_rn(left, __dmul_rn(u, __dsub_rn(right, left)));
-        double dd = __dsub_rn(x1, x0), ll;
-        pass(std::integral_constant<int, 1>{}, k, &dd, &ll);
-        const double f1 = post(x1, ll);
+        if (j == avail) {  // next batch from the current interval
+          avail = build(left, right, pos, kSpecNext, cand);
+          double dn[kSpecNext];
+          for (int q = 0; q < kSpecNext; ++q) dn[q] = q < avail ? __dsub_rn(cand[q], x0) : 0.0;
+          pass(std::integral_constant<int, kSpecNext>{}, k, dn, llc);
+          j = 0;
+        }
+        x1 = cand[j];
+        const double f1 = post(x1, llc[j]);
+        ++j;
+        ++pos;
         evals += 1;
         if (f1 > level) {
           accepted = true;
@@ -214,8 +277,8 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
           left = x1;
         else
           right = x1;
-        if (__dsub_rn(right, left) < __dmul_rn(1e-12, __dadd_rn(1.0, fabs(x0)))) {
-          x1 = x0;
+        if (__dsub_rn(right, left) < tiny) {
+          x1 = x0;  // degenerate slice; keep the current point
           accepted = true;
           break;
         }
@@ -337,7 +400,23 @@ int pm_ws_run_chain(pm_ws_t ws, const double* mu, const double* sigma, int32_t n
   a.out_evals = d_evals;
   a.status = d_status;
   void* kargs[] = {&a};
+  const bool timing = std::getenv("PM_CHAIN_TIMING") != nullptr;
+  cudaEvent_t te0 = nullptr, te1 = nullptr;
+  if (timing) {
+    cudaEventCreate(&te0);
+    cudaEventCreate(&te1);
+    cudaEventRecord(te0, st);
+  }
   PM_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kChainThreads), kargs, smem, st));
+  if (timing) {
+    float ms = 0.f;
+    cudaEventRecord(te1, st);
+    cudaEventSynchronize(te1);
+    cudaEventElapsedTime(&ms, te0, te1);
+    std::fprintf(stderr, "[pm_ws_run_chain] kernel %.3f ms grid %d x %d\n", ms, grid, kChainThreads);
+    cudaEventDestroy(te0);
+    cudaEventDestroy(te1);
+  }
   unsigned long long pos = 0;
   long long evals = 0;
   int status[2] = {0, -1};
