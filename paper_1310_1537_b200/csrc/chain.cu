@@ -63,11 +63,12 @@ __device__ __forceinline__ double logprior(const ChainArgs& a, int k, double v) 
   return __dmul_rn(__dmul_rn(-0.5, z), z);
 }
 
-constexpr int kSpecFirst = 6;   // shrink candidates evaluated with f0/left/right in the first pass
-constexpr int kSpecNext = 4;    // shrink candidates per later pass
-
-template <int U>
+// U: rows per ILP batch; SF: shrink candidates evaluated with f0/left/right in the first pass;
+// SN: shrink candidates per later pass
+template <int U, int SF, int SN>
 __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
+  constexpr int kSpecFirst = SF;
+  constexpr int kSpecNext = SN;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sbeta[];  // [K]
   __shared__ double red[kChainThreads / 32][kChainMaxM];
@@ -350,9 +351,13 @@ int pm_ws_run_chain(pm_ws_t ws, const double* mu, const double* sigma, int32_t n
   const char* eb = std::getenv("PM_CHAIN_BLOCKS_PER_SM");
   const int unroll = eu ? std::atoi(eu) : 2;
   const int want_per_sm = eb ? std::max(1, std::atoi(eb)) : 2;
-  void* kfn = unroll >= 4 ? reinterpret_cast<void*>(chain_kernel<4>)
-                          : (unroll == 2 ? reinterpret_cast<void*>(chain_kernel<2>)
-                                         : reinterpret_cast<void*>(chain_kernel<1>));
+  const char* es = std::getenv("PM_CHAIN_SPEC");
+  const int spec = es ? std::atoi(es) : 4;  // speculative shrink candidates in the first pass
+  void* kfn;
+  if (spec >= 6) kfn = unroll >= 2 ? reinterpret_cast<void*>(chain_kernel<2, 6, 4>) : reinterpret_cast<void*>(chain_kernel<1, 6, 4>);
+  else if (spec >= 4) kfn = unroll >= 2 ? reinterpret_cast<void*>(chain_kernel<2, 4, 3>) : reinterpret_cast<void*>(chain_kernel<1, 4, 3>);
+  else if (spec >= 2) kfn = unroll >= 2 ? reinterpret_cast<void*>(chain_kernel<2, 2, 2>) : reinterpret_cast<void*>(chain_kernel<1, 2, 2>);
+  else kfn = unroll >= 2 ? reinterpret_cast<void*>(chain_kernel<2, 1, 1>) : reinterpret_cast<void*>(chain_kernel<1, 1, 1>);
   int per_sm = 0;
   PM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kChainThreads, smem));
   if (per_sm < 1) return fail(PM_EDEVICE, "chain kernel cannot be resident");
