@@ -144,6 +144,10 @@ PM_API int pm_ws_run_chain(pm_ws_t ws, const double* mu, const double* sigma, in
                            uint64_t stream_pos, double* draws_out, double* beta_inout, uint64_t* stream_pos_out,
                            int64_t* evals_out, int32_t* fail_coord);
 
+/* Device time (CUDA events around the cooperative kernel) of this thread's last
+ * pm_ws_run_chain call, in milliseconds. */
+PM_API int pm_chain_last_kernel_ms(float* ms);
+
 /* ------------------------------------------------------------------ hierarchical GLM
  * Replaces the per-group loop of loglike_grad over HbDataset.groups (hb.py:64-86,
  * 127-135) with one launch over CSR-batched groups sharing K.

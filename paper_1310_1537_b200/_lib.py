@@ -58,6 +58,7 @@ SIGNATURES = {
     "pm_ws_validate": (c_int, [c_void_p, _dp, _dp]),
     "pm_ws_run_chain": (c_int, [c_void_p, _dp, _dp, c_int32, c_int32, c_double, c_int32, c_uint64, c_uint64,
                                 c_uint64, _dp, _dp, POINTER(c_uint64), POINTER(c_int64), POINTER(c_int32)]),
+    "pm_chain_last_kernel_ms": (c_int, [POINTER(ctypes.c_float)]),
     "pm_hb_create": (c_int, [c_int, POINTER(c_void_p)]),
     "pm_hb_destroy": (c_int, [c_void_p]),
     "pm_hb_upload": (c_int, [c_void_p, _dp, _dp, _i64p, c_int32, c_int32]),

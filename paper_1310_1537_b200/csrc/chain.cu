@@ -319,9 +319,17 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
   }
 }
 
+thread_local float g_last_chain_ms = 0.f;
+
 }  // namespace
 
 extern "C" {
+
+int pm_chain_last_kernel_ms(float* ms) {
+  if (!ms) return fail(PM_EINVAL, "null argument");
+  *ms = g_last_chain_ms;
+  return PM_OK;
+}
 
 int pm_ws_run_chain(pm_ws_t ws, const double* mu, const double* sigma, int32_t n_iter, int32_t n_burnin,
                     double slice_width, int32_t slice_max_steps, uint64_t key0, uint64_t key1, uint64_t stream_pos,
@@ -366,11 +374,13 @@ int pm_ws_run_chain(pm_ws_t ws, const double* mu, const double* sigma, int32_t n
   const int kept = n_iter - n_burnin;
   double* dbuf = nullptr;
   const size_t nd = size_t(3) * v.K + size_t(kept) * v.K + size_t(2) * grid * kChainMaxM;
-  PM_CUDA(cudaMalloc(&dbuf, sizeof(double) * nd + 64));
+  // stream-ordered allocation: no device-wide synchronisation of cudaMalloc/cudaFree
+  PM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dbuf), sizeof(double) * nd + 64, st));
   struct Free {
     void* p;
-    ~Free() { cudaFree(p); }
-  } fr{dbuf};
+    cudaStream_t s;
+    ~Free() { cudaFreeAsync(p, s); }
+  } fr{dbuf, st};
   double* d_mu = dbuf;
   double* d_sigma = d_mu + v.K;
   double* d_beta = d_sigma + v.K;
@@ -405,23 +415,19 @@ int pm_ws_run_chain(pm_ws_t ws, const double* mu, const double* sigma, int32_t n
   a.out_evals = d_evals;
   a.status = d_status;
   void* kargs[] = {&a};
-  const bool timing = std::getenv("PM_CHAIN_TIMING") != nullptr;
+  // the kernel is always bracketed by CUDA events (pm_chain_last_kernel_ms)
   cudaEvent_t te0 = nullptr, te1 = nullptr;
-  if (timing) {
-    cudaEventCreate(&te0);
-    cudaEventCreate(&te1);
-    cudaEventRecord(te0, st);
-  }
+  PM_CUDA(cudaEventCreate(&te0));
+  PM_CUDA(cudaEventCreate(&te1));
+  PM_CUDA(cudaEventRecord(te0, st));
   PM_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kChainThreads), kargs, smem, st));
-  if (timing) {
-    float ms = 0.f;
-    cudaEventRecord(te1, st);
-    cudaEventSynchronize(te1);
-    cudaEventElapsedTime(&ms, te0, te1);
-    std::fprintf(stderr, "[pm_ws_run_chain] kernel %.3f ms grid %d x %d\n", ms, grid, kChainThreads);
-    cudaEventDestroy(te0);
-    cudaEventDestroy(te1);
-  }
+  PM_CUDA(cudaEventRecord(te1, st));
+  PM_CUDA(cudaEventSynchronize(te1));
+  PM_CUDA(cudaEventElapsedTime(&g_last_chain_ms, te0, te1));
+  cudaEventDestroy(te0);
+  cudaEventDestroy(te1);
+  if (std::getenv("PM_CHAIN_TIMING"))
+    std::fprintf(stderr, "[pm_ws_run_chain] kernel %.3f ms grid %d x %d\n", g_last_chain_ms, grid, kChainThreads);
   unsigned long long pos = 0;
   long long evals = 0;
   int status[2] = {0, -1};
