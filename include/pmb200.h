@@ -211,6 +211,18 @@ PM_API int pm_lat_set_potts(pm_lat_t h, double coupling);
  * uniforms: host double[n_sweeps*H*W] for PM_RNG_UNIFORMS, else NULL. */
 PM_API int pm_lat_sweeps(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t key0, uint64_t key1,
                   uint64_t stream_pos, const double* uniforms);
+/* pm_lat_sweeps plus the diagnostics of the differential path and the denoiser
+ * (replaces ZCache.flips_last_sweep, ising.py:204/253, and the post-burn-in
+ * spin accumulator of denoise, ising.py:275-287):
+ *   flips_out: host int64[n_sweeps] or NULL; flips_out[t] = sites whose value
+ *              changed in sweep t (each site is updated once per sweep, so this
+ *              is also count_nonzero(s_after != s_before), ising.py:284).
+ *   acc_inout: host int32[H*W] or NULL; for every sweep t >= acc_from the new
+ *              spins (Ising) / states (Potts) are added in, row-major.
+ * Same trajectory as pm_lat_sweeps; runs on the generic kernel. */
+PM_API int pm_lat_sweeps_acc(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t key0, uint64_t key1,
+                      uint64_t stream_pos, const double* uniforms, int32_t acc_from, int32_t* acc_inout,
+                      int64_t* flips_out);
 /* Benchmark helper: pm_lat_sweeps for an in-kernel RNG mode, bracketed by CUDA events on the
  * handle's stream; *total_ms = elapsed device time of the n_sweeps sweeps. */
 PM_API int pm_lat_time_sweeps(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t key0, uint64_t key1,

@@ -101,3 +101,27 @@ def potts_cdf(coupling: float, counts) -> np.ndarray:
     out = (c_double * 3)()
     load().oracle_potts_cdf(float(coupling), n, out)
     return np.array(list(out))
+
+
+def denoise(noisy01, w: float, bias_scale: float, sweeps: int, burnin: int, key0: int, key1: int):
+    """CPU restatement of the reference denoiser (ising.py:257-290) on top of the
+    oracle sweep: from_image spins/bias (ising.py:73-82), one free-boundary sweep
+    at a time on the DeviateBuffer stream (H*W deviates per sweep), per-sweep
+    flip counts (ising.py:283-284), sum of post-burn-in spins (ising.py:285-287)
+    and the sign rule (acc >= 0, ties -> 1; kept == 0 -> input unchanged).
+    Returns (restored uint8 image, flips int64[sweeps])."""
+    img = np.asarray(noisy01)
+    s = (2 * img.astype(np.int8) - 1).astype(np.int8)
+    b = bias_scale * s.astype(np.float64)
+    hw = s.size
+    acc = np.zeros(s.shape, dtype=np.int64)
+    flips = np.zeros(sweeps, dtype=np.int64)
+    for t in range(sweeps):
+        nxt = ising_sweeps(s, b, w, False, 1, RNG_NUMPY_PHILOX, key0, key1, t * hw)
+        flips[t] = int(np.count_nonzero(nxt != s))
+        s = nxt
+        if t >= burnin:
+            acc += s
+    if sweeps - burnin <= 0:
+        return img.astype(np.uint8).copy(), flips
+    return (acc >= 0).astype(np.uint8), flips

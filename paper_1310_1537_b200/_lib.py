@@ -74,6 +74,8 @@ SIGNATURES = {
     "pm_lat_sweeps": (c_int, [c_void_p, c_int32, c_int, c_uint64, c_uint64, c_uint64, _dp]),
     "pm_lat_time_sweeps": (c_int, [c_void_p, c_int32, c_int, c_uint64, c_uint64, c_uint64,
                                    POINTER(ctypes.c_float)]),
+    "pm_lat_sweeps_acc": (c_int, [c_void_p, c_int32, c_int, c_uint64, c_uint64, c_uint64, _dp, c_int32,
+                                  POINTER(c_int32), _i64p]),
     "pm_lat_stream": (c_int, [c_void_p, POINTER(c_void_p)]),
     "pm_lat_packed": (c_int, [c_void_p, _ip]),
     "pm_lat_create_strip": (c_int, [c_int, c_int32, c_int32, c_int32, c_int32, c_int, POINTER(c_void_p)]),

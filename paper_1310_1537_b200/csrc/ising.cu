@@ -63,6 +63,9 @@ struct GenericArgs {
   uint64_t base;        // numpy: stream index of this half-sweep's first deviate
   uint64_t sweep;       // philox4x32: sweep number
   const double* uni;    // uniforms of this half-sweep (n_c), PM_RNG_UNIFORMS
+  // optional diagnostics (gibbs_sweep_diff / denoise, ising.py:232-290)
+  unsigned long long* flips;  // += number of sites whose value changed (integer atomics: exact)
+  int32_t* acc;               // [H*W] row-major running sum of the new values, or null
 };
 
 __device__ __forceinline__ double uniform_for(const GenericArgs& a, int64_t p) {
@@ -80,6 +83,7 @@ __device__ __forceinline__ double uniform_for(const GenericArgs& a, int64_t p) {
 __global__ void __launch_bounds__(256) gibbs_generic_kernel(GenericArgs a) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   const int H = a.lat.H, W = a.lat.W;
+  unsigned int nflip = 0;
   for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < a.n_c; p += stride) {
     int i, j;
     if ((W & 1) == 0) {
@@ -120,7 +124,13 @@ __global__ void __launch_bounds__(256) gibbs_generic_kernel(GenericArgs a) {
       const double* c3 = a.cdf + pidx * 3;
       ns = int8_t((u >= c3[0]) + (u >= c3[1]) + (u >= c3[2]));
     }
+    if (a.flips) nflip += (a.lat.get(i, j) != ns) ? 1u : 0u;
+    if (a.acc) a.acc[int64_t(i) * W + j] += ns;
     a.lat.set(i, j, ns);
+  }
+  if (a.flips) {
+    for (int s = 16; s >= 1; s >>= 1) nflip += __shfl_xor_sync(0xffffffffu, nflip, s);
+    if ((threadIdx.x & 31) == 0 && nflip) atomicAdd(a.flips, (unsigned long long)nflip);
   }
 }
 
@@ -586,7 +596,8 @@ int pm_lat_set_potts(pm_lat_t h, double coupling) {
 }
 
 static int lat_sweeps_impl(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t key0, uint64_t key1,
-                           uint64_t stream_pos, const double* uniforms, float* total_ms);
+                           uint64_t stream_pos, const double* uniforms, float* total_ms, int32_t acc_from = 0,
+                           int32_t* acc_out = nullptr, int64_t* flips_out = nullptr);
 
 // One half-sweep (colour c) of the packed fast path; for a strip, the own rows of the strip.
 static void launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t seed, cudaStream_t st) {
@@ -706,8 +717,17 @@ int pm_lat_time_sweeps(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t key0
   return lat_sweeps_impl(h, n_sweeps, rng_mode, key0, key1, stream_pos, nullptr, total_ms);
 }
 
+int pm_lat_sweeps_acc(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t key0, uint64_t key1,
+                      uint64_t stream_pos, const double* uniforms, int32_t acc_from, int32_t* acc_inout,
+                      int64_t* flips_out) {
+  if (acc_from < 0) return fail(PM_EINVAL, "acc_from must be >= 0");
+  return lat_sweeps_impl(h, n_sweeps, rng_mode, key0, key1, stream_pos, uniforms, nullptr, acc_from, acc_inout,
+                         flips_out);
+}
+
 static int lat_sweeps_impl(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t key0, uint64_t key1,
-                           uint64_t stream_pos, const double* uniforms, float* total_ms) {
+                           uint64_t stream_pos, const double* uniforms, float* total_ms, int32_t acc_from,
+                           int32_t* acc_out, int64_t* flips_out) {
   if (!h) return fail(PM_EINVAL, "null handle");
   if (n_sweeps < 0) return fail(PM_EINVAL, "n_sweeps must be >= 0");
   if (rng_mode != PM_RNG_UNIFORMS && rng_mode != PM_RNG_NUMPY_PHILOX && rng_mode != PM_RNG_PHILOX4X32)
@@ -732,7 +752,29 @@ static int lat_sweeps_impl(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t 
     }
     PM_CUDA(cudaMemcpyAsync(h->uni, uniforms, sizeof(double) * need, cudaMemcpyHostToDevice, h->stream));
   }
-  const bool fast = rng_mode == PM_RNG_PHILOX4X32 && fast_path_ok(h);
+  const bool diag = acc_out || flips_out;   // diagnostics run on the generic kernel
+  const bool fast = rng_mode == PM_RNG_PHILOX4X32 && fast_path_ok(h) && !diag;
+  int32_t* d_acc = nullptr;
+  unsigned long long* d_flips = nullptr;
+  struct FreeDiag {
+    void* a;
+    void* b;
+    cudaStream_t s;
+    ~FreeDiag() {
+      if (a) cudaFreeAsync(a, s);
+      if (b) cudaFreeAsync(b, s);
+    }
+  } free_diag{nullptr, nullptr, h->stream};
+  if (acc_out) {
+    PM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_acc), sizeof(int32_t) * HW, h->stream));
+    free_diag.a = d_acc;
+    PM_CUDA(cudaMemcpyAsync(d_acc, acc_out, sizeof(int32_t) * HW, cudaMemcpyHostToDevice, h->stream));
+  }
+  if (flips_out) {
+    PM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_flips), sizeof(unsigned long long) * n_sweeps, h->stream));
+    free_diag.b = d_flips;
+    PM_CUDA(cudaMemsetAsync(d_flips, 0, sizeof(unsigned long long) * n_sweeps, h->stream));
+  }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (total_ms) {
     PM_CUDA(cudaEventCreate(&e0));
@@ -762,6 +804,8 @@ static int lat_sweeps_impl(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t 
         a.base = stream_pos + uint64_t(t) * HW + (c == 0 ? 0 : n0);
         a.sweep = stream_pos + uint64_t(t);
         a.uni = rng_mode == PM_RNG_UNIFORMS ? h->uni + size_t(t) * HW + (c == 0 ? 0 : n0) : nullptr;
+        a.flips = d_flips ? d_flips + t : nullptr;
+        a.acc = (d_acc && t >= acc_from) ? d_acc : nullptr;
         gibbs_generic_kernel<<<grid_for(h, nc), 256, 0, h->stream>>>(a);
       }
       PM_CUDA(cudaGetLastError());
@@ -774,6 +818,9 @@ static int lat_sweeps_impl(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t 
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
+  if (d_acc) PM_CUDA(cudaMemcpyAsync(acc_out, d_acc, sizeof(int32_t) * HW, cudaMemcpyDeviceToHost, h->stream));
+  if (d_flips)
+    PM_CUDA(cudaMemcpyAsync(flips_out, d_flips, sizeof(int64_t) * n_sweeps, cudaMemcpyDeviceToHost, h->stream));
   PM_CUDA(cudaStreamSynchronize(h->stream));
   return PM_OK;
 }

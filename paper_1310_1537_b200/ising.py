@@ -30,11 +30,14 @@ import numpy as np
 from scipy.special import expit
 
 from . import _lib
+from .images import flip_noise, read_pbm, synthetic_binary_image, write_pbm
 from .rng import BufferKind, DeviateBuffer, SitePhilox, philox_key_of
 
 __all__ = [
     "IsingLattice", "PottsLattice", "ColorPartition", "conditional_prob", "color_lattice",
     "gibbs_sweep", "gibbs_sweeps", "potts_sweeps", "ising_prob_table", "potts_cdf_table",
+    "ZCache", "gibbs_sweep_diff", "gibbs_sweeps_diff", "denoise",
+    "read_pbm", "write_pbm", "synthetic_binary_image", "flip_noise",
 ]
 
 
@@ -158,6 +161,20 @@ class LatticeDevice:
         _lib.call("pm_lat_sweeps", self._h, int(n), int(mode), ctypes.c_uint64(key0),
                   ctypes.c_uint64(key1), ctypes.c_uint64(pos), _lib.dptr(u))
 
+    def sweeps_acc(self, n: int, mode: int, key0: int = 0, key1: int = 0, pos: int = 0, uniforms=None,
+                   acc_from: int = 0, acc: np.ndarray | None = None, want_flips: bool = True):
+        """`sweeps` plus per-sweep flip counts and an in-place int32 post-`acc_from` accumulator."""
+        u = None if uniforms is None else np.ascontiguousarray(uniforms, dtype=np.float64)
+        flips = np.zeros(max(int(n), 0), dtype=np.int64) if want_flips else None
+        accp = None
+        if acc is not None:
+            assert acc.dtype == np.int32 and acc.flags.c_contiguous and acc.size == self.height * self.width
+            accp = acc.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        _lib.call("pm_lat_sweeps_acc", self._h, int(n), int(mode), ctypes.c_uint64(key0),
+                  ctypes.c_uint64(key1), ctypes.c_uint64(pos), _lib.dptr(u), int(acc_from), accp,
+                  None if flips is None else _lib.i64ptr(flips))
+        return flips
+
     def time_sweeps(self, n: int, mode: int, key0: int = 0, key1: int = 0, pos: int = 0) -> float:
         """Device milliseconds of n sweeps with an in-kernel RNG (CUDA events, handle stream)."""
         ms = ctypes.c_float()
@@ -218,30 +235,38 @@ def color_lattice(lat, device: int = 0) -> ColorPartition:
     return ColorPartition(lat, device)
 
 
-def _run(lat, part: ColorPartition, rng_buffer, n_sweeps: int) -> None:
+def _run(lat, part: ColorPartition, rng_buffer, n_sweeps: int, diag: dict | None = None):
+    """Run n_sweeps device sweeps drawing from rng_buffer; returns per-sweep flips if diag."""
     if n_sweeps < 1:
-        return
+        return np.zeros(0, dtype=np.int64) if diag is not None else None
     n0, n1 = part.colors[0].size, part.colors[1].size
     consumed = n_sweeps * (n0 + n1)
     dev = part.device
     if isinstance(rng_buffer, SitePhilox):
-        dev.sweeps(n_sweeps, _lib.PM_RNG_PHILOX4X32, rng_buffer.seed, 0, rng_buffer.sweep)
-        rng_buffer.advance(n_sweeps)
+        mode, k0, k1, pos, u = _lib.PM_RNG_PHILOX4X32, rng_buffer.seed, 0, rng_buffer.sweep, None
+        advance = lambda: rng_buffer.advance(n_sweeps)  # noqa: E731
     elif isinstance(rng_buffer, DeviateBuffer) and rng_buffer.kind is BufferKind.UNIFORM01:
-        k0, k1 = rng_buffer.stream_key()
-        dev.sweeps(n_sweeps, _lib.PM_RNG_NUMPY_PHILOX, k0, k1, rng_buffer.position)
-        rng_buffer.skip(consumed)
+        (k0, k1), pos, u = rng_buffer.stream_key(), rng_buffer.position, None
+        mode = _lib.PM_RNG_NUMPY_PHILOX
+        advance = lambda: rng_buffer.skip(consumed)  # noqa: E731
     elif _is_reference_uniform_buffer(rng_buffer):
         # the reference's own DeviateBuffer: same stream; generate on the device, then advance
-        k0, k1 = philox_key_of(rng_buffer._gen)
-        pos = _reference_position(rng_buffer)
-        dev.sweeps(n_sweeps, _lib.PM_RNG_NUMPY_PHILOX, k0, k1, pos)
-        rng_buffer.take(consumed)
+        (k0, k1), pos, u = philox_key_of(rng_buffer._gen), _reference_position(rng_buffer), None
+        mode = _lib.PM_RNG_NUMPY_PHILOX
+        advance = lambda: rng_buffer.take(consumed)  # noqa: E731
     else:
         u = np.concatenate([np.asarray(rng_buffer.take(n), dtype=np.float64)
                             for _ in range(n_sweeps) for n in (n0, n1)])
-        dev.sweeps(n_sweeps, _lib.PM_RNG_UNIFORMS, uniforms=u)
+        mode, k0, k1, pos = _lib.PM_RNG_UNIFORMS, 0, 0, 0
+        advance = lambda: None  # noqa: E731
+    flips = None
+    if diag is None:
+        dev.sweeps(n_sweeps, mode, k0, k1, pos, u)
+    else:
+        flips = dev.sweeps_acc(n_sweeps, mode, k0, k1, pos, u, diag.get("acc_from", 0), diag.get("acc"))
+    advance()
     part.unpack_into(lat)
+    return flips
 
 
 def _is_reference_uniform_buffer(obj) -> bool:
@@ -274,6 +299,128 @@ def gibbs_sweeps(lat, part: ColorPartition, rng_buffer, n_sweeps: int, plan=None
 def potts_sweeps(lat: PottsLattice, part: ColorPartition, rng_buffer, n_sweeps: int = 1) -> None:
     """Checkerboard heat-bath sweeps of the q=4 Potts model."""
     _run(lat, part, rng_buffer, n_sweeps)
+
+
+def _neighbour_sum_grid(s: np.ndarray, periodic: bool) -> np.ndarray:
+    """Sum of the 4 neighbours' values (0 outside a free boundary), as float64."""
+    sf = s.astype(np.float64)
+    if periodic:
+        return (np.roll(sf, 1, 0) + np.roll(sf, -1, 0) + np.roll(sf, 1, 1) + np.roll(sf, -1, 1))
+    out = np.zeros_like(sf)
+    out[1:, :] += sf[:-1, :]
+    out[:-1, :] += sf[1:, :]
+    out[:, 1:] += sf[:, :-1]
+    out[:, :-1] += sf[:, 1:]
+    return out
+
+
+class ZCache:
+    """Neighbour-sum cache of the differential path (ising.py:190-229).
+
+    The reference keeps per-colour neighbour sums and patches them by +-2 per
+    flip so that a low flip rate saves the gather.  On B200 the gather is three
+    coalesced row loads per 16 sites, cheaper than scattering cache updates, so
+    the device sweep always recomputes the sums from the resident lattice and
+    the "cache" is the lattice state the last differential sweep left behind:
+    `nsum(c)` is derived from that snapshot (exact small integers in float64,
+    as the reference's), `validate` compares it with a fresh gather of the
+    current lattice and so still catches a lattice modified behind the
+    cache's back (e.g. by a plain gibbs_sweep).
+    """
+
+    def __init__(self, lat: IsingLattice, part: ColorPartition):
+        self._part = part
+        self._periodic = getattr(lat, "boundary", "free") == "periodic"
+        self._snap = lat.s.copy()
+        self._nsum_cache = None
+        self.flips_last_sweep = 0
+        self.n_nodes = part.colors[0].size + part.colors[1].size
+
+    def _resync(self, s: np.ndarray) -> None:
+        self._snap = s.copy()
+        self._nsum_cache = None
+
+    def _grid(self) -> np.ndarray:
+        if self._nsum_cache is None:
+            self._nsum_cache = _neighbour_sum_grid(self._snap, self._periodic).ravel()
+        return self._nsum_cache
+
+    def nsum(self, c: int) -> np.ndarray:
+        """Neighbour spin sums of colour c in packed (scan) order."""
+        return self._grid()[self._part.colors[c]]
+
+    def z_grid(self, lat: IsingLattice, part: ColorPartition) -> np.ndarray:
+        """z_i = b_i + w * (neighbour spin sum), assembled on the grid (ising.py:210-215)."""
+        out = np.empty(lat.height * lat.width)
+        b = lat.b.ravel()
+        for c in (0, 1):
+            idx = part.colors[c]
+            out[idx] = b[idx] + lat.w * self.nsum(c)
+        return out.reshape(lat.height, lat.width)
+
+    @property
+    def flip_rate(self) -> float:
+        return self.flips_last_sweep / self.n_nodes
+
+    def validate(self, lat: IsingLattice, part: ColorPartition, tol: float = 1e-10) -> float:
+        """Max |cached z - freshly gathered z|; raises AssertionError above tol (ising.py:221-229)."""
+        fresh = _neighbour_sum_grid(lat.s, self._periodic).ravel()
+        diff = np.abs(lat.w * (self._grid() - fresh))
+        err = float(np.max(diff, initial=0.0))
+        if err > tol:
+            raise AssertionError(f"z cache desynchronized: max error {err:g} > {tol:g}")
+        return err
+
+
+def gibbs_sweep_diff(lat: IsingLattice, part: ColorPartition, zcache: ZCache, rng_buffer,
+                     plan=None) -> None:
+    """Differential sweep (ising.py:232-254): same trajectory as gibbs_sweep, plus
+    zcache.flips_last_sweep counted on the device (integer atomics, exact)."""
+    gibbs_sweeps_diff(lat, part, zcache, rng_buffer, 1)
+
+
+def gibbs_sweeps_diff(lat: IsingLattice, part: ColorPartition, zcache: ZCache, rng_buffer,
+                      n_sweeps: int) -> np.ndarray:
+    """n_sweeps differential sweeps in one device call; returns the per-sweep flip counts."""
+    flips = _run(lat, part, rng_buffer, n_sweeps, diag={})
+    if n_sweeps >= 1:
+        zcache.flips_last_sweep = int(flips[-1])
+        zcache._resync(lat.s)
+    return flips
+
+
+def denoise(noisy_image, w: float = 1.0, bias_scale: float = 2.0, sweeps: int = 30, burnin: int = 10,
+            seed: int = 0, use_diff: bool = False, plan=None, trace_out: list | None = None,
+            device: int = 0) -> np.ndarray:
+    """Posterior-mean-sign restoration of a {0,1} image (ising.py:257-290).
+
+    All `sweeps` sweeps run in ONE device call (pm_lat_sweeps_acc): the
+    post-burn-in spin sum is accumulated in an int32 grid on the device (exact,
+    as the reference's float64 sum of +-1 values) and the per-sweep flip counts
+    come back for `trace_out`.  The uniforms are the reference's
+    DeviateBuffer(UNIFORM01, seed) stream, so the restored image is bit-identical.
+    `use_diff` selects the same trajectory in the reference and is accepted for
+    signature compatibility; `plan` likewise.
+    """
+    noisy_image = np.asarray(noisy_image)
+    lat = IsingLattice.from_image(noisy_image, w=w, bias_scale=bias_scale)
+    if sweeps < 0 or burnin < 0:
+        raise ValueError("sweeps and burnin must be >= 0")
+    kept = max(0, sweeps - burnin)
+    if kept == 0 and trace_out is None:
+        return noisy_image.astype(np.uint8).copy()
+    part = color_lattice(lat, device)
+    try:
+        buf = DeviateBuffer(BufferKind.UNIFORM01, seed=seed)
+        acc = np.zeros(lat.height * lat.width, dtype=np.int32)
+        flips = _run(lat, part, buf, sweeps, diag={"acc_from": burnin, "acc": acc})
+    finally:
+        part.device.close()
+    if trace_out is not None:
+        trace_out.extend(float(f) / lat.s.size for f in flips)
+    if kept == 0:
+        return noisy_image.astype(np.uint8).copy()
+    return (acc.reshape(lat.s.shape) >= 0).astype(np.uint8)
 
 
 def ising_prob_table(w: float, b: float = 0.0) -> np.ndarray:

@@ -246,6 +246,55 @@ def hb_fixture():
                         sigma=prior.sigma, f=f, g=g)
 
 
+def denoise_fixture():
+    """Reference denoiser (ising.py:257-290), its per-sweep trace, the differential
+    sweep's flip counter and cached sums (ising.py:190-254), and PBM bytes."""
+    import tempfile
+    out = {}
+    cases = [((64, 64), "two_region", 0.1, 3, 1.0, 2.0, 30, 10, 4), ((32, 32), "two_region", 0.1, 5, 1.0, 2.0, 20, 5, 6),
+             ((48, 48), "all_ones", 0.1, 7, 1.0, 2.0, 25, 8, 8), ((24, 24), "two_region", 0.0, 0, 1.0, 8.0, 12, 4, 1),
+             ((16, 16), "two_region", 0.2, 9, 1.0, 2.0, 0, 0, 1), ((16, 16), "two_region", 0.2, 9, 1.0, 2.0, 5, 5, 2),
+             ((37, 23), "two_region", 0.25, 11, 0.7, 1.5, 9, 3, 12345), ((1, 9), "two_region", 0.3, 1, 1.0, 1.0, 7, 2, 3)]
+    for i, (shape, kind, rate, nseed, w, bscale, sweeps, burnin, seed) in enumerate(cases):
+        noisy = ris.flip_noise(ris.synthetic_binary_image(*shape, kind=kind), rate, seed=nseed)
+        trace = []
+        restored = ris.denoise(noisy, w=w, bias_scale=bscale, sweeps=sweeps, burnin=burnin, seed=seed,
+                               trace_out=trace)
+        restored_diff = ris.denoise(noisy, w=w, bias_scale=bscale, sweeps=sweeps, burnin=burnin, seed=seed,
+                                    use_diff=True)
+        assert (restored == restored_diff).all()
+        buf = rrng.DeviateBuffer(rrng.BufferKind.UNIFORM01, seed=seed)
+        out[f"noisy_{i}"], out[f"out_{i}"] = noisy, restored
+        out[f"trace_{i}"] = np.array(trace, dtype=np.float64)
+        out[f"par_{i}"] = np.array([w, bscale, sweeps, burnin, seed], dtype=np.float64)
+        out[f"key_{i}"] = np.array(buf._gen.bit_generator.state["state"]["key"], dtype=np.uint64)
+    # differential sweeps: flips_last_sweep and the cached sums after each sweep
+    img = ris.flip_noise(ris.synthetic_binary_image(20, 24), 0.15, seed=2)
+    lat = ris.IsingLattice.from_image(img, 1.0, 1.5)
+    part = ris.color_lattice(lat)
+    zc = ris.ZCache(lat, part)
+    buf = rrng.DeviateBuffer(rrng.BufferKind.UNIFORM01, seed=9)
+    flips, nsums = [], []
+    for _ in range(12):
+        ris.gibbs_sweep_diff(lat, part, zc, buf)
+        flips.append(zc.flips_last_sweep)
+        nsums.append(np.concatenate([zc.nsum(0), zc.nsum(1)]))
+    out["diff_img"], out["diff_s1"] = img, lat.s.copy()
+    out["diff_flips"], out["diff_nsum"] = np.array(flips, dtype=np.int64), np.stack(nsums)
+    out["diff_z"] = zc.z_grid(lat, part)
+    # PBM bytes written by the reference (P1 and P4, with a ragged P4 row)
+    with tempfile.TemporaryDirectory() as d:
+        for fmt in ("P1", "P4"):
+            pimg = ris.flip_noise(ris.synthetic_binary_image(7, 13), 0.4, seed=11)
+            path = os.path.join(d, f"x.{fmt}")
+            ris.write_pbm(path, pimg, fmt=fmt)
+            with open(path, "rb") as fh:
+                out[f"pbm_{fmt}"] = np.frombuffer(fh.read(), dtype=np.uint8)
+            out["pbm_img"] = pimg
+    out["n_cases"] = len(cases)
+    np.savez_compressed(os.path.join(HERE, "denoise.npz"), **out)
+
+
 if __name__ == "__main__":
     glm_fixture()
     diff_fixture()
@@ -254,6 +303,7 @@ if __name__ == "__main__":
     periodic_fixture()
     sampler_fixture()
     hb_fixture()
+    denoise_fixture()
     for fn in sorted(os.listdir(HERE)):
         if fn.endswith(".npz"):
             print(fn, os.path.getsize(os.path.join(HERE, fn)))

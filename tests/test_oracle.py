@@ -241,3 +241,15 @@ def test_potts_cdf_is_normalised_and_monotone():
         assert 0.0 <= c[0] <= c[1] <= c[2] <= 1.0
         e = np.exp(1.0986 * np.array(counts, dtype=float))
         np.testing.assert_allclose(c, np.cumsum(e)[:3] / e.sum(), rtol=1e-15)
+
+
+# ------------------------------------------------------------------ denoise (ising.py:257-290)
+def test_denoise_oracle_matches_reference_fixture():
+    z = golden("denoise.npz")
+    for i in range(int(z["n_cases"])):
+        w, bscale, sweeps, burnin, _ = z[f"par_{i}"]
+        key = z[f"key_{i}"]
+        noisy = z[f"noisy_{i}"]
+        out, flips = go.denoise(noisy, float(w), float(bscale), int(sweeps), int(burnin), int(key[0]), int(key[1]))
+        np.testing.assert_array_equal(out, z[f"out_{i}"], err_msg=f"case {i}")
+        np.testing.assert_array_equal(flips / noisy.size, z[f"trace_{i}"], err_msg=f"case {i}")
