@@ -52,7 +52,8 @@ enum pm_status {
   PM_ENOMEM = 4,
   PM_ESTATE = 5,
   PM_ESLICE = 6,   /* -> SliceWidenError (sampler.py:32-33, 141-150) */
-  PM_ESHRINK = 7   /* -> RuntimeError "slice shrinkage failed" (sampler.py:163-164) */
+  PM_ESHRINK = 7,  /* -> RuntimeError "slice shrinkage failed" (sampler.py:163-164) */
+  PM_EDRAIN = 8    /* -> RngDrainError (rng.py:36-37, 178, 214) */
 };
 
 /* storage type of the design matrix on the device */
@@ -245,6 +246,37 @@ PM_API int pm_lat_strip_half_sweep(pm_lat_t h, int colour, uint64_t seed, uint64
 /* Device pointer of packed row `array_row` of colour `colour` (W/2 bytes): 0 = top halo,
  * 1..rows = own rows, rows+1 = bottom halo. */
 PM_API int pm_lat_strip_row(pm_lat_t h, int colour, int32_t array_row, void** dev_ptr);
+
+/* ---------------------------------------------------------------- batch RNG
+ * Device generation of the reference's deviate streams (rng.py:42-138) and its Gamma /
+ * Dirichlet samplers (rng.py:152-215).  A stream is numpy Philox4x64-10 with key
+ * (key[0], key[1]) (SeedSequence(seed, spawn_key=owner), rng.py:42-44); positions are
+ * stream indices: uniform index for UNIFORM01 streams, normal index for STD_NORMAL
+ * streams (normal j = Box-Muller of uniform pair j/2, cos for even j, sin for odd j,
+ * rng.py:47-56 -- the capacity-invariant order of DeviateBuffer's carry logic 91-102).
+ * All outputs are host arrays; ms (nullable) receives the device time (CUDA events). */
+enum pm_rng_kind { PM_RNG_KIND_UNIFORM01 = 0, PM_RNG_KIND_STD_NORMAL = 1 };
+/* out[i] = deviate pos+i of the stream, i < n (DeviateBuffer.take, rng.py:115-127).
+ * out_is_device: out is a device pointer on `device`. */
+PM_API int pm_rng_fill(int device, int kind, uint64_t key0, uint64_t key1, uint64_t pos, int64_t n, double* out,
+                int out_is_device, float* ms);
+/* n draws of gamma_sample(GammaParams(alpha, rate), u_src, n_src) (rng.py:191-198) from
+ * the uniform stream ukey at *upos and the normal stream nkey at *npos; both positions
+ * advance past exactly the deviates n sequential calls consume.  PM_EDRAIN after 10000
+ * rejections in one draw (rng.py:178). */
+PM_API int pm_rng_gamma(int device, double alpha, double rate, int64_t n, const uint64_t* ukey, uint64_t* upos,
+                 const uint64_t* nkey, uint64_t* npos, double* out, float* ms);
+/* n draws of dirichlet_sample(alphas[kd], u_src, n_src) (rng.py:201-215), out[n][kd]. */
+PM_API int pm_rng_dirichlet(int device, const double* alphas, int32_t kd, int64_t n, const uint64_t* ukey,
+                     uint64_t* upos, const uint64_t* nkey, uint64_t* npos, double* out, float* ms);
+/* S independent stream pairs (owner spawn keys, rng.py:7-9), n_per draws each:
+ * ukeys/nkeys [S][2], upos/npos [S] in/out, out [S][n_per] (gamma) / [S][n_per][kd]. */
+PM_API int pm_rng_gamma_streams(int device, double alpha, double rate, int32_t S, int64_t n_per,
+                         const uint64_t* ukeys, uint64_t* upos, const uint64_t* nkeys, uint64_t* npos,
+                         double* out, float* ms);
+PM_API int pm_rng_dirichlet_streams(int device, const double* alphas, int32_t kd, int32_t S, int64_t n_per,
+                             const uint64_t* ukeys, uint64_t* upos, const uint64_t* nkeys, uint64_t* npos,
+                             double* out, float* ms);
 
 /* Host evaluation of the kernels' per-row logistic terms (the same pm_math.cuh code the
  * device runs, bit for bit): nll = (1-y)t + softplus(-t), w = y - sigmoid(t).  For tests. */

@@ -17,7 +17,8 @@ from ctypes import (POINTER, c_char_p, c_double, c_int, c_int8, c_int32, c_int64
 
 import numpy as np
 
-PM_OK, PM_EINVAL, PM_ERANGE, PM_EDEVICE, PM_ENOMEM, PM_ESTATE, PM_ESLICE, PM_ESHRINK = range(8)
+PM_OK, PM_EINVAL, PM_ERANGE, PM_EDEVICE, PM_ENOMEM, PM_ESTATE, PM_ESLICE, PM_ESHRINK, PM_EDRAIN = range(9)
+PM_RNG_KIND_UNIFORM01, PM_RNG_KIND_STD_NORMAL = 0, 1
 PM_X_F64, PM_X_F32 = 0, 1
 PM_BOUNDARY_FREE, PM_BOUNDARY_PERIODIC = 0, 1
 PM_MODEL_ISING, PM_MODEL_POTTS4 = 0, 1
@@ -32,6 +33,8 @@ _dp = POINTER(c_double)
 _i64p = POINTER(c_int64)
 _i8p = POINTER(c_int8)
 _ip = POINTER(c_int)
+_u64p = POINTER(c_uint64)
+_fp = POINTER(ctypes.c_float)
 
 # name -> (restype, argtypes); every symbol include/pmb200.h declares
 SIGNATURES = {
@@ -81,6 +84,13 @@ SIGNATURES = {
     "pm_lat_create_strip": (c_int, [c_int, c_int32, c_int32, c_int32, c_int32, c_int, POINTER(c_void_p)]),
     "pm_lat_strip_half_sweep": (c_int, [c_void_p, c_int, c_uint64, c_uint64, c_void_p]),
     "pm_lat_strip_row": (c_int, [c_void_p, c_int, c_int32, POINTER(c_void_p)]),
+    "pm_rng_fill": (c_int, [c_int, c_int, c_uint64, c_uint64, c_uint64, c_int64, c_void_p, c_int, _fp]),
+    "pm_rng_gamma": (c_int, [c_int, c_double, c_double, c_int64, _u64p, _u64p, _u64p, _u64p, _dp, _fp]),
+    "pm_rng_dirichlet": (c_int, [c_int, _dp, c_int32, c_int64, _u64p, _u64p, _u64p, _u64p, _dp, _fp]),
+    "pm_rng_gamma_streams": (c_int, [c_int, c_double, c_double, c_int32, c_int64, _u64p, _u64p, _u64p, _u64p,
+                                     _dp, _fp]),
+    "pm_rng_dirichlet_streams": (c_int, [c_int, _dp, c_int32, c_int32, c_int64, _u64p, _u64p, _u64p, _u64p,
+                                         _dp, _fp]),
     "pm_row_terms_host": (c_int, [_dp, _dp, c_int64, _dp, _dp]),
     "pm_ising_prob_table": (c_int, [c_double, c_double, _dp]),
     "pm_potts_cdf_table": (c_int, [c_double, _dp]),
@@ -92,6 +102,10 @@ _lib = None
 
 class NativeLibraryMissing(RuntimeError):
     """libpmb200.so is not built or cannot be loaded; there is no CPU fallback."""
+
+
+class RngDrainError(RuntimeError):
+    """A bounded rejection loop exhausted its iteration cap (rng.py:36-37); PM_EDRAIN."""
 
 
 def load() -> ctypes.CDLL:
@@ -132,6 +146,8 @@ def check(rc: int, what: str = "") -> None:
         raise IndexError(msg)
     if rc == PM_ENOMEM:
         raise MemoryError(msg)
+    if rc == PM_EDRAIN:
+        raise RngDrainError(msg)
     raise RuntimeError(f"libpmb200: {msg}")
 
 
@@ -167,6 +183,11 @@ def dptr(a: np.ndarray):
 def i64ptr(a: np.ndarray):
     assert a.dtype == np.int64 and a.flags.c_contiguous
     return a.ctypes.data_as(_i64p)
+
+
+def u64ptr(a: np.ndarray):
+    assert a.dtype == np.uint64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_u64p)
 
 
 def i8ptr(a: np.ndarray):

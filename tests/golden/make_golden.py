@@ -295,6 +295,46 @@ def denoise_fixture():
     np.savez_compressed(os.path.join(HERE, "denoise.npz"), **out)
 
 
+GAMMA_CASES = [(2.0, 3.0, 9, 3000), (1.0, 1.0, 4, 2000), (0.3, 2.0, 5, 1500), (5.5, 0.7, 6, 1000),
+               (1.0000001, 1.0, 7, 500), (50.0, 2.0, 1, 500), (0.999, 1.0, 2, 400)]
+DIRICHLET_CASES = [([2.0, 3.0, 5.0], 11, 500), ([1.0] * 100, 12, 40), ([0.1, 0.5, 1.0, 2.0], 13, 300), ([1.0], 14, 20),
+                   ([0.05] * 5, 15, 200), ([3.0] * 7, 16, 150), ([1.5] * 130, 17, 10)]
+
+
+def rng_batch_fixture():
+    """Reference normal streams, Gamma and Dirichlet draws with their stream consumption
+    (rng.py:59-215), on owner streams (0,) uniform / (1,) normal as _bench_sources."""
+    out = {}
+    for tag, cap, seed, owner, n in (("n8", 4096, 8, (), 4099), ("n10", 3, 10, (1,), 1001)):
+        out[f"normal_{tag}"] = rrng.DeviateBuffer(rrng.BufferKind.STD_NORMAL, cap, seed, owner=owner).take(n)
+    for i, (alpha, rate, seed, n) in enumerate(GAMMA_CASES):
+        u = rrng.DeviateBuffer(rrng.BufferKind.UNIFORM01, 8192, seed, owner=(0,))
+        z = rrng.DeviateBuffer(rrng.BufferKind.STD_NORMAL, 8192, seed, owner=(1,))
+        out[f"gamma_{i}"] = np.array([rrng.gamma_sample(rrng.GammaParams(alpha, rate), u, z) for _ in range(n)])
+        out[f"gamma_used_{i}"] = np.array([u.consumed, z.consumed], dtype=np.int64)
+    for i, (alphas, seed, n) in enumerate(DIRICHLET_CASES):
+        u = rrng.DeviateBuffer(rrng.BufferKind.UNIFORM01, 8192, seed, owner=(0,))
+        z = rrng.DeviateBuffer(rrng.BufferKind.STD_NORMAL, 8192, seed, owner=(1,))
+        out[f"dir_{i}"] = np.array([rrng.dirichlet_sample(alphas, u, z) for _ in range(n)])
+        out[f"dir_used_{i}"] = np.array([u.consumed, z.consumed], dtype=np.int64)
+    # independent owner streams (2s,) uniform / (2s+1,) normal
+    draws, used = [], []
+    for s in range(8):
+        u = rrng.DeviateBuffer(rrng.BufferKind.UNIFORM01, 8192, 21, owner=(2 * s,))
+        z = rrng.DeviateBuffer(rrng.BufferKind.STD_NORMAL, 8192, 21, owner=(2 * s + 1,))
+        draws.append([rrng.gamma_sample(rrng.GammaParams(0.7, 1.5), u, z) for _ in range(50)])
+        used.append([u.consumed, z.consumed])
+    out["gstreams"], out["gstreams_used"] = np.array(draws), np.array(used, dtype=np.int64)
+    draws, used = [], []
+    for s in range(5):
+        u = rrng.DeviateBuffer(rrng.BufferKind.UNIFORM01, 8192, 22, owner=(2 * s,))
+        z = rrng.DeviateBuffer(rrng.BufferKind.STD_NORMAL, 8192, 22, owner=(2 * s + 1,))
+        draws.append([rrng.dirichlet_sample([0.5, 1.0, 2.0], u, z) for _ in range(20)])
+        used.append([u.consumed, z.consumed])
+    out["dstreams"], out["dstreams_used"] = np.array(draws), np.array(used, dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, "rng_batch.npz"), **out)
+
+
 if __name__ == "__main__":
     glm_fixture()
     diff_fixture()
@@ -304,6 +344,7 @@ if __name__ == "__main__":
     sampler_fixture()
     hb_fixture()
     denoise_fixture()
+    rng_batch_fixture()
     for fn in sorted(os.listdir(HERE)):
         if fn.endswith(".npz"):
             print(fn, os.path.getsize(os.path.join(HERE, fn)))
