@@ -61,6 +61,7 @@ CONFIGS = {
     "c3": dict(groups=1000, k=20, mean_rows=2000, desc="config 3: G=1000 n_g~Poisson(2000) K=20 HB batched"),
     "c4": dict(h=8192, w=8192, model="ising", desc="config 4: 8192^2 periodic Ising, Philox4x32 (seed,sweep,site)"),
     "c4potts": dict(h=8192, w=8192, model="potts", desc="config 4 Potts q=4 variant, 8192^2 periodic"),
+    "rng": dict(draws=10_000_000, desc="batch RNG: 10M Gamma(2,3) draws per step on one stream pair (rng.py:246-300)"),
 }
 
 METRIC = "log-posterior+gradient evals/s and achieved HBM GB/s (logistic GLM, fp64)"
@@ -689,6 +690,76 @@ def run_gibbs(args, cfg):
             "cpu_baseline": None if args.no_cpu_baseline else cpu_baseline_other(args.config)}), flush=True)
 
 
+# ---------------------------------------------------------------------------- B200 arm: batch RNG
+def run_rng(args, cfg):
+    """Device batch RNG: Gamma(2, 3) draws/s on one (uniform, normal) stream
+    pair -- the reference's rng_bench GAMMA cell (rng.py:246-300) -- plus stream fill rates."""
+    import ctypes
+
+    import torch
+    from paper_1310_1537_b200 import _lib
+    from paper_1310_1537_b200 import rng as prng
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    n = cfg["draws"]
+    params = prng.GammaParams(2.0, 3.0)
+    u = prng.DeviateBuffer(prng.BufferKind.UNIFORM01, seed=9, owner=(0,))
+    z = prng.DeviateBuffer(prng.BufferKind.STD_NORMAL, seed=9, owner=(1,))
+    for _ in range(args.warmup):
+        prng.gamma_batch(params, n, u, z, local)
+    clocks = ClockSampler(local)
+    clocks.start()
+    dev_ms, walls = [], []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        prng.gamma_batch(params, n, u, z, local, timing=dev_ms)
+        walls.append(time.perf_counter() - t0)
+    clk = clocks.stop()
+    ms = statistics.mean(dev_ms)
+    # stream fill rates into device memory (8 B written per deviate)
+    n_fill = 1 << 28
+    buf = torch.empty(n_fill, dtype=torch.float64, device=f"cuda:{local}")
+    fill = {}
+    k0, k1 = u.stream_key()
+    for name, kind in (("uniform01", _lib.PM_RNG_KIND_UNIFORM01), ("std_normal", _lib.PM_RNG_KIND_STD_NORMAL)):
+        t = ctypes.c_float()
+        for _ in range(2):
+            _lib.call("pm_rng_fill", local, kind, ctypes.c_uint64(k0), ctypes.c_uint64(k1), ctypes.c_uint64(0), n_fill,
+                      buf.data_ptr(), 1, ctypes.byref(t))
+        fill[name] = {"deviates_per_s": n_fill / (t.value * 1e-3), "write_gb_per_s": 8 * n_fill / (t.value * 1e-3) / 1e9}
+    del buf
+    dms = []
+    prng.dirichlet_batch(np.ones(100), 100_000, u, z, local)
+    prng.dirichlet_batch(np.ones(100), 100_000, u, z, local, timing=dms)
+    peak, src = load_peaks()
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import rng_oracle as ro
+        m = 30_000
+        t0 = time.perf_counter()
+        ro.gamma_draws(2.0, 3.0, m, u.stream_key(), 0, z.stream_key(), 0)
+        dt = time.perf_counter() - t0
+        cpu = {"value": m / dt, "unit": "draws/s", "cores": 1, "kind": "port",
+               "sample": f"oracle/rng_oracle.py gamma_draws (restatement of rng.py:163-198, scalar Python, "
+                         f"numpy streams), {m} Gamma(2,3) draws, 1 core -- the reference's per-call cost model"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": "Gamma(2,3) draws/s on one buffered stream pair (device two-scan sampler)",
+            "value": n / (ms * 1e-3), "unit": "draws/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "numpy Philox4x64 streams, seed 9, owners (0,) uniform / (1,) normal",
+            "config": {"workload": cfg["desc"], "draws_per_step": n},
+            "cycles_per_sample_at_2.6GHz": ms * 1e-3 * 2.6e9 / n,
+            "stream_fill": fill,
+            "dirichlet_k100_vectors_per_s": 100_000 / (dms[0] * 1e-3),
+            "roofline": {"bound": "issue (Philox4x64 + fp64 log/sincos) -- HBM fraction of the fill kernel for context",
+                         "achieved": fill["uniform01"]["write_gb_per_s"], "peak": peak, "unit": "GB/s",
+                         "frac": fill["uniform01"]["write_gb_per_s"] / peak, "traffic": None, "peak_source": src},
+            "e2e": {"value": n / statistics.mean(walls), "unit": "draws/s", "h2d_bytes_per_step": 32,
+                    "d2h_bytes_per_step": 8 * n},
+            "gpu_launches": None, "clocks": clk, "cpu_baseline": cpu}), flush=True)
+
+
 def main():
     p = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     p.add_argument("--gpus", type=int, default=1)
@@ -730,6 +801,10 @@ def main():
         args.steps = args.steps or 200
         args.warmup = args.warmup if args.warmup is not None else 5
         run_hb(args, cfg)
+    elif "draws" in cfg:
+        args.steps = args.steps or 10
+        args.warmup = args.warmup if args.warmup is not None else 3
+        run_rng(args, cfg)
     else:
         args.steps = args.steps or 1000
         args.warmup = args.warmup if args.warmup is not None else 10

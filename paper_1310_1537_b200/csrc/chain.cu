@@ -375,6 +375,7 @@ int pm_ws_run_chain(pm_ws_t ws, const double* mu, const double* sigma, int32_t n
   double* dbuf = nullptr;
   const size_t nd = size_t(3) * v.K + size_t(kept) * v.K + size_t(2) * grid * kChainMaxM;
   // stream-ordered allocation: no device-wide synchronisation of cudaMalloc/cudaFree
+  pm::retain_pool(v.device);
   PM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dbuf), sizeof(double) * nd + 64, st));
   struct Free {
     void* p;

@@ -39,6 +39,23 @@ int sm_count(int device) {
   return cache[device];
 }
 
+// Stream-ordered allocations (cudaMallocAsync) come from the device's default pool; with
+// the default release threshold of 0 the pool unmaps its memory at every synchronisation,
+// so each call would pay a fresh physical mapping.  Keep up to 4 GiB cached per device.
+void retain_pool(int device) {
+  static std::mutex mu;
+  static std::vector<char> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (device >= (int)done.size()) done.resize(device + 1, 0);
+  if (done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = uint64_t(4) << 30;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = 1;
+}
+
 cudaError_t ensure_smem_attr(const void* kernel, std::atomic<uint64_t>& mask) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);

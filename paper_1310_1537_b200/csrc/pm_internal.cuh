@@ -42,6 +42,7 @@ struct DeviceGuard {
 };
 
 int sm_count(int device);
+void retain_pool(int device);
 
 }  // namespace pm
 

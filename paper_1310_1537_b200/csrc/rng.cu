@@ -388,6 +388,7 @@ int check_device(int device) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return pm::fail(PM_EDEVICE, "no CUDA device visible");
   if (device < 0 || device >= n) return pm::fail(PM_ERANGE, "device index out of range");
+  pm::retain_pool(device);
   return PM_OK;
 }
 
