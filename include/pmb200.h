@@ -171,6 +171,30 @@ PM_API int pm_hb_stream(pm_hb_t h, void** stream);
 PM_API int pm_hb_time_evals(pm_hb_t h, const double* betas, const double* mu, const double* sigma,
                             int want_grad, int32_t n, float* total_ms);
 
+/* Hierarchical Gibbs sweep state (replaces HbState + hb_sweep, hb.py:110-168): per-group
+ * workspaces (xbeta, transposed X) and per-group numpy Philox uniform streams
+ * (DeviateBuffer(UNIFORM01, seed, owner=(g,)), hb.py:118-119).  Groups are CSR rows
+ * offsets[g]..offsets[g+1] of X (row-major N x K) and y; beta0 [G][K] is the start point
+ * (the reference starts every group at prior.mu); keys [G][2], pos [G] the streams. */
+typedef struct pm_hbs_s* pm_hbs_t;
+PM_API int pm_hbs_create(int device, const double* X, const double* y, const int64_t* offsets, int32_t G,
+                         int32_t K, const double* mu, const double* sigma, const double* beta0,
+                         const uint64_t* keys, const uint64_t* pos, pm_hbs_t* out);
+PM_API int pm_hbs_destroy(pm_hbs_t h);
+/* n_sweeps Gibbs sweeps of every group in ONE launch (one CTA per group; slice-within-Gibbs
+ * per coordinate, sampler.py:112-167; neval-1 extra full evaluations per group and sweep,
+ * hb.py:130-131).  Out: betas [G][K], stream positions [G], evaluation counts of this call
+ * [G].  PM_ESLICE / PM_ESHRINK name the first failing group and coordinate. */
+PM_API int pm_hbs_sweeps(pm_hbs_t h, int32_t n_sweeps, int32_t neval, double slice_width, int32_t max_steps,
+                         double* betas_out, uint64_t* pos_out, int64_t* evals_out, int32_t* fail_group,
+                         int32_t* fail_coord, float* ms);
+/* Replace the shared hyperprior N(mu, sigma^2) used by later sweeps. */
+PM_API int pm_hbs_set_prior(pm_hbs_t h, const double* mu, const double* sigma);
+/* Per-group log-likelihood at the current state (from the maintained xbeta). */
+PM_API int pm_hbs_loglike(pm_hbs_t h, double* ll_out);
+/* Maintained xbeta, concatenated in CSR row order (N doubles). */
+PM_API int pm_hbs_read_xbeta(pm_hbs_t h, double* out);
+
 /* ------------------------------------------------------------------ lattice Gibbs
  * Replaces IsingLattice/ColorPartition/gibbs_sweep (ising.py:47-187) and adds the
  * periodic boundary and the q=4 Potts model.  Colour c = (i+j)%2; colour 0 updates

@@ -47,13 +47,13 @@ class UniformStream:
 
 
 def run_chain(x, y, mu, sigma, n_iter, n_burnin=0, seed=0, slice_width=1.0, slice_max_steps=50,
-              workers: int = 1, rng=None):
-    """Returns (draws[n_iter-n_burnin, K], evals)."""
+              workers: int = 1, rng=None, beta0=None):
+    """Returns (draws[n_iter-n_burnin, K], evals); the chain starts at beta0 (default mu)."""
     n, k = x.shape
     mu = np.asarray(mu, dtype=np.float64)
     sigma = np.asarray(sigma, dtype=np.float64)
     rng = rng if rng is not None else UniformStream(seed)
-    beta = mu.copy()
+    beta = mu.copy() if beta0 is None else np.array(beta0, dtype=np.float64)
     xbeta = x @ beta                 # GlmWorkspace, glm.py:472
     xt = np.ascontiguousarray(x.T)   # glm.py:473
     evals = 0

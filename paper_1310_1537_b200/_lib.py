@@ -68,6 +68,14 @@ SIGNATURES = {
     "pm_hb_eval": (c_int, [c_void_p, _dp, _dp, _dp, c_int, _dp, _dp]),
     "pm_hb_stream": (c_int, [c_void_p, POINTER(c_void_p)]),
     "pm_hb_time_evals": (c_int, [c_void_p, _dp, _dp, _dp, c_int, c_int32, POINTER(ctypes.c_float)]),
+    "pm_hbs_create": (c_int, [c_int, _dp, _dp, _i64p, c_int32, c_int32, _dp, _dp, _dp, _u64p, _u64p,
+                              POINTER(c_void_p)]),
+    "pm_hbs_destroy": (c_int, [c_void_p]),
+    "pm_hbs_sweeps": (c_int, [c_void_p, c_int32, c_int32, c_double, c_int32, _dp, _u64p, _i64p,
+                              POINTER(c_int32), POINTER(c_int32), _fp]),
+    "pm_hbs_set_prior": (c_int, [c_void_p, _dp, _dp]),
+    "pm_hbs_loglike": (c_int, [c_void_p, _dp]),
+    "pm_hbs_read_xbeta": (c_int, [c_void_p, _dp]),
     "pm_lat_create": (c_int, [c_int, c_int32, c_int32, c_int, c_int, POINTER(c_void_p)]),
     "pm_lat_destroy": (c_int, [c_void_p]),
     "pm_lat_set_spins": (c_int, [c_void_p, _i8p]),

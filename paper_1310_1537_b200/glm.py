@@ -35,6 +35,7 @@ __all__ = [
     "Strategy", "ExecPlan", "DesignMatrix", "Shard", "ShardedMatrix",
     "GradResult", "GlmWorkspace", "make_sharded", "loglike", "loglike_grad",
     "log_posterior_grad", "diff_loglike", "diff_loglike_multi", "commit_update",
+    "load_design_csv", "synthetic_logistic",
 ]
 
 
@@ -489,3 +490,55 @@ def commit_update(ws: GlmWorkspace, k: int, delta_beta_k: float,
         counters.add_launches(1)
     ws.beta_current[k] += delta_beta_k
     counters.add_flops(2 * ws.n_rows)
+
+
+# ---------------------------------------------------------------------------------------
+# data I/O and synthesis (host side, glm.py:546-591 of the reference)
+# ---------------------------------------------------------------------------------------
+def load_design_csv(path) -> DesignMatrix:
+    """Plain CSV of K covariate columns followed by one 0/1 response column (glm.py:546-575).
+
+    Blank lines are skipped; ValueError names the row/column of the first bad cell, a
+    ragged row, a missing covariate column or a response outside {0, 1}.
+    """
+    import csv
+    rows: list[list[float]] = []
+    with open(path, newline="") as fh:
+        for ln, row in enumerate(csv.reader(fh), start=1):
+            if not any(c.strip() for c in row):
+                continue
+            parsed = []
+            for col, cell in enumerate(row, start=1):
+                try:
+                    parsed.append(float(cell))
+                except ValueError:
+                    raise ValueError(f"{path}: row {ln}, column {col}: not a number: {cell!r}") from None
+            rows.append(parsed)
+    if not rows:
+        raise ValueError(f"{path}: no data rows")
+    width = len(rows[0])
+    for ln, r in enumerate(rows, start=1):
+        if len(r) != width:
+            raise ValueError(f"{path}: row {ln}: expected {width} columns, got {len(r)}")
+    if width < 2:
+        raise ValueError(f"{path}: need at least one covariate column plus a response column")
+    table = np.asarray(rows)
+    resp = table[:, -1]
+    bad = np.flatnonzero((resp != 0.0) & (resp != 1.0))
+    if bad.size:
+        raise ValueError(f"{path}: row {bad[0] + 1}, column {width}: response must be 0 or 1, got {resp[bad[0]]!r}")
+    return DesignMatrix(table[:, :-1], resp)
+
+
+def synthetic_logistic(n_rows: int, n_cols: int, seed: int = 0, beta=None, beta_scale: float = 1.0):
+    """Seeded instance X ~ N(0,1), y ~ Bernoulli(sigmoid(X beta)) (glm.py:578-591).
+
+    Same generator draws in the same order as the reference (X, then beta unless
+    given, then the uniforms), so the instance is identical.  Returns (DesignMatrix, beta).
+    """
+    from scipy.special import expit
+    gen = np.random.default_rng(seed)
+    x = gen.standard_normal((n_rows, n_cols))
+    beta = gen.normal(0.0, beta_scale, n_cols) if beta is None else _check_beta(beta, n_cols)
+    y = (gen.random(n_rows) < expit(x @ beta)).astype(np.float64)
+    return DesignMatrix(x, y), np.asarray(beta, dtype=np.float64)

@@ -11,13 +11,16 @@ per group streams its rows through the same TMA ring as the flat kernel.
 from __future__ import annotations
 
 import ctypes
+from dataclasses import dataclass
+from enum import Enum
 
 import numpy as np
 
 from . import _lib
 from .glm import DesignMatrix, GradResult
 
-__all__ = ["HbDataset", "CsrGroups", "HbDevice", "hb_log_posterior_grad"]
+__all__ = ["HbDataset", "CsrGroups", "HbDevice", "hb_log_posterior_grad", "MappingMode", "MappingPolicy",
+           "HbState", "synthetic_hb_dataset", "hb_sweep", "hb_sweeps", "hb_benchmark"]
 
 
 class HbDataset:
@@ -165,3 +168,188 @@ def hb_log_posterior_grad(data, betas, prior=None, device: int = 0, want_grad: b
     sigma = None if prior is None else prior.sigma
     f, g = dev.eval(betas, mu, sigma, want_grad)
     return [GradResult(float(f[i]), None if g is None else g[i]) for i in range(dev.G)]
+
+
+# ---------------------------------------------------------------------------------------
+# hierarchical Gibbs sweep (hb.py:46-204 of the reference), device-resident
+# ---------------------------------------------------------------------------------------
+class MappingMode(Enum):
+    """COARSE (workers across groups) / FINE (row-parallel per group), hb.py:46-49.
+
+    On the device both mappings are the same launch -- one CTA per group, its rows
+    split across the CTA's threads -- and, as in the reference, the draws never
+    depend on the mapping.
+    """
+
+    COARSE = "coarse"
+    FINE = "fine"
+
+
+@dataclass(frozen=True)
+class MappingPolicy:
+    mode: MappingMode
+    workers: int = 1
+    neval: int = 1
+
+    def __post_init__(self):
+        if self.workers < 1:
+            raise ValueError("workers must be >= 1")
+        if self.neval < 1:
+            raise ValueError("neval must be >= 1")
+
+
+def synthetic_hb_dataset(m_groups: int, n_cols: int, navg: int, seed: int = 0, prior=None):
+    """Uniform-size groups with beta_m drawn from the hyperprior (hb.py:89-107).
+
+    Same SeedSequence(seed, spawn_key=(m,)) draws as the reference, so the data are
+    identical.  Returns (HbDataset, betas_true (M, K)).
+    """
+    from .glm import synthetic_logistic
+    from .sampler import GaussianPrior
+    if prior is None:
+        prior = GaussianPrior.isotropic(n_cols)
+    groups, betas = [], np.empty((m_groups, n_cols))
+    for m in range(m_groups):
+        gen = np.random.default_rng(np.random.SeedSequence(seed, spawn_key=(m,)))
+        beta_m = prior.mu + prior.sigma * gen.standard_normal(n_cols)
+        child = int(gen.integers(2 ** 63))
+        data, _ = synthetic_logistic(navg, n_cols, seed=child, beta=beta_m)
+        groups.append(data)
+        betas[m] = beta_m
+    return HbDataset(groups), betas
+
+
+class HbState:
+    """Per-group workspaces and uniform streams persisting across sweeps (hb.py:110-124).
+
+    The workspaces (xbeta, transposed X per group) live on the device in one pm_hbs_t
+    handle; each group keeps the reference's stream DeviateBuffer(UNIFORM01,
+    buffer_capacity, seed, owner=(m,)), advanced on the host after every device sweep
+    past exactly the uniforms the group consumed.  Every group starts at prior.mu.
+    """
+
+    def __init__(self, ds: HbDataset, prior, seed: int = 0, buffer_capacity: int = 8192, device: int = 0):
+        from .rng import BufferKind, DeviateBuffer
+        if prior.mu.shape != (ds.n_cols,):
+            raise ValueError("prior dimension does not match dataset")
+        _lib.require_device(device)
+        self.buffers = [DeviateBuffer(BufferKind.UNIFORM01, buffer_capacity, seed, owner=(m,))
+                        for m in range(ds.m_groups)]
+        self.total_evals = 0
+        self.G, self.K = ds.m_groups, ds.n_cols
+        self.device = device
+        csr = ds.to_csr()
+        self._rows = csr.n_rows_total
+        keys = np.ascontiguousarray([b.stream_key() for b in self.buffers], dtype=np.uint64)
+        pos = np.zeros(self.G, dtype=np.uint64)
+        self._betas = np.ascontiguousarray(np.tile(prior.mu, (self.G, 1)))
+        self._prior = (prior.mu.copy(), prior.sigma.copy())
+        h = ctypes.c_void_p()
+        _lib.call("pm_hbs_create", device, _lib.dptr(csr.x), _lib.dptr(csr.y), _lib.i64ptr(csr.offsets), self.G,
+                  self.K, _lib.dptr(self._prior[0]), _lib.dptr(self._prior[1]), _lib.dptr(self._betas),
+                  _lib.u64ptr(keys), _lib.u64ptr(pos), ctypes.byref(h))
+        self._h = h
+        self.last_kernel_ms = 0.0
+
+    @property
+    def betas(self) -> list[np.ndarray]:
+        return [b.copy() for b in self._betas]
+
+    def _use_prior(self, prior) -> None:
+        if prior.mu.shape != (self.K,):
+            raise ValueError("prior dimension does not match dataset")
+        if not (np.array_equal(prior.mu, self._prior[0]) and np.array_equal(prior.sigma, self._prior[1])):
+            _lib.call("pm_hbs_set_prior", self._h, _lib.dptr(prior.mu), _lib.dptr(prior.sigma))
+            self._prior = (prior.mu.copy(), prior.sigma.copy())
+
+    def sweeps(self, prior, n_sweeps: int, neval: int = 1, slice_width: float = 1.0,
+               slice_max_steps: int = 50) -> None:
+        """n_sweeps sweeps of every group in one device launch."""
+        from .sampler import SliceWidenError
+        self._use_prior(prior)
+        pos = np.empty(self.G, dtype=np.uint64)
+        evals = np.zeros(self.G, dtype=np.int64)
+        fg, fk = ctypes.c_int32(-1), ctypes.c_int32(-1)
+        ms = ctypes.c_float()
+        start = np.array([b.position for b in self.buffers], dtype=np.int64)
+        rc = _lib.load().pm_hbs_sweeps(self._h, int(n_sweeps), int(neval), float(slice_width), int(slice_max_steps),
+                                       _lib.dptr(self._betas), _lib.u64ptr(pos), _lib.i64ptr(evals),
+                                       ctypes.byref(fg), ctypes.byref(fk), ctypes.byref(ms))
+        self.last_kernel_ms = float(ms.value)
+        if rc == _lib.PM_OK or rc in (_lib.PM_ESLICE, _lib.PM_ESHRINK):
+            for m, b in enumerate(self.buffers):
+                b.skip(int(pos[m]) - int(start[m]))
+            self.total_evals += int(evals.sum())
+        if rc == _lib.PM_ESLICE:
+            raise SliceWidenError(_lib.last_error())
+        if rc == _lib.PM_ESHRINK:
+            raise RuntimeError(_lib.last_error())
+        _lib.check(rc, "pm_hbs_sweeps")
+
+    def loglike(self) -> np.ndarray:
+        """Per-group log-likelihood at the current coefficients (maintained xbeta)."""
+        out = np.empty(self.G)
+        _lib.call("pm_hbs_loglike", self._h, _lib.dptr(out))
+        return out
+
+    def xbeta(self) -> np.ndarray:
+        """Maintained X_g beta_g for all groups, concatenated in row order."""
+        out = np.empty(self._rows)
+        _lib.call("pm_hbs_read_xbeta", self._h, _lib.dptr(out))
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.load().pm_hbs_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def hb_sweep(ds: HbDataset, state: HbState, prior, policy: MappingPolicy, slice_width: float = 1.0,
+             slice_max_steps: int = 50) -> list[np.ndarray]:
+    """One Gibbs sweep: every group's coefficient vector updated once (hb.py:138-168).
+
+    Returns the post-sweep coefficient vectors (copies).
+    """
+    state.sweeps(prior, 1, policy.neval, slice_width, slice_max_steps)
+    return state.betas
+
+
+def hb_sweeps(ds: HbDataset, state: HbState, prior, policy: MappingPolicy, n_sweeps: int,
+              slice_width: float = 1.0, slice_max_steps: int = 50) -> list[np.ndarray]:
+    """n_sweeps hb_sweep calls fused into one launch (identical draws)."""
+    state.sweeps(prior, n_sweeps, policy.neval, slice_width, slice_max_steps)
+    return state.betas
+
+
+def hb_benchmark(ds: HbDataset, prior, policies: list[MappingPolicy], n_sweeps: int = 3, reps: int = 3,
+                 seed: int = 0, clock_ghz: float = 2.6, slice_width: float = 1.0):
+    """Time n_sweeps sweeps under each policy; one BenchRecord per policy (hb.py:171-204).
+
+    Each repetition restarts from a fresh state with the same seed; the wall time covers
+    the n_sweeps sweeps (one device launch) and `evals` = n_sweeps * neval, so cpr is a
+    cycles-per-group-row figure as in the reference.
+    """
+    import statistics
+    import time
+
+    from .perf import BenchRecord
+    records = []
+    for policy in policies:
+        walls = []
+        for _ in range(reps):
+            state = HbState(ds, prior, seed=seed)
+            t0 = time.perf_counter()
+            state.sweeps(prior, n_sweeps, policy.neval, slice_width)
+            walls.append(time.perf_counter() - t0)
+            state.close()
+        records.append(BenchRecord.from_wall(
+            label=f"hb/{policy.mode.value}/neval{policy.neval}", n_rows=ds.n_rows_total, n_cols=ds.n_cols,
+            workers=policy.workers, n_chunks=1, wall_seconds=statistics.median(walls),
+            evals=n_sweeps * policy.neval, clock_ghz=clock_ghz))
+    return records

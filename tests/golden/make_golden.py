@@ -335,6 +335,34 @@ def rng_batch_fixture():
     np.savez_compressed(os.path.join(HERE, "rng_batch.npz"), **out)
 
 
+def hb_sweep_fixture():
+    """Reference hierarchical Gibbs sweeps (HbState + hb_sweep, hb.py:110-168)."""
+    out = {}
+    # case 0: the reference generator, isotropic prior, 3 sweeps
+    ds, _ = rhb.synthetic_hb_dataset(6, 3, 80, seed=4)
+    prior = rsmp.GaussianPrior.isotropic(3)
+    # case 1: ragged groups (1..150 rows), non-zero prior mean, neval 3, small buffers
+    groups = [rglm.synthetic_logistic(n, 3, seed=40 + i, beta=np.array([0.5, -1.0, 0.25]))[0]
+              for i, n in enumerate([1, 7, 33, 64, 150])]
+    ds1 = rhb.HbDataset(groups)
+    prior1 = rsmp.GaussianPrior(np.array([0.2, -0.1, 0.3]), np.array([0.5, 0.5, 0.5]))
+    for c, (d, pr, seed, cap, neval, sweeps) in enumerate([(ds, prior, 5, 8192, 1, 3), (ds1, prior1, 6, 7, 3, 4)]):
+        st = rhb.HbState(d, pr, seed=seed, buffer_capacity=cap)
+        pol = rhb.MappingPolicy(rhb.MappingMode.COARSE, workers=1, neval=neval)
+        traj = []
+        for _ in range(sweeps):
+            traj.append(np.array(rhb.hb_sweep(d, st, pr, pol)))
+        out[f"betas_{c}"] = np.stack(traj)
+        out[f"evals_{c}"] = np.int64(st.total_evals)
+        out[f"used_{c}"] = np.array([b.consumed for b in st.buffers], dtype=np.int64)
+        out[f"x_{c}"] = np.concatenate([g.x for g in d.groups])
+        out[f"y_{c}"] = np.concatenate([g.y for g in d.groups])
+        out[f"off_{c}"] = np.concatenate([[0], np.cumsum([g.n_rows for g in d.groups])]).astype(np.int64)
+        out[f"prior_{c}"] = np.stack([pr.mu, pr.sigma])
+        out[f"meta_{c}"] = np.array([seed, cap, neval, sweeps], dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, "hb_sweep.npz"), **out)
+
+
 if __name__ == "__main__":
     glm_fixture()
     diff_fixture()
@@ -345,6 +373,7 @@ if __name__ == "__main__":
     hb_fixture()
     denoise_fixture()
     rng_batch_fixture()
+    hb_sweep_fixture()
     for fn in sorted(os.listdir(HERE)):
         if fn.endswith(".npz"):
             print(fn, os.path.getsize(os.path.join(HERE, fn)))

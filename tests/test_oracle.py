@@ -253,3 +253,22 @@ def test_denoise_oracle_matches_reference_fixture():
         out, flips = go.denoise(noisy, float(w), float(bscale), int(sweeps), int(burnin), int(key[0]), int(key[1]))
         np.testing.assert_array_equal(out, z[f"out_{i}"], err_msg=f"case {i}")
         np.testing.assert_array_equal(flips / noisy.size, z[f"trace_{i}"], err_msg=f"case {i}")
+
+
+# ------------------------------------------------------------------ HB sweep (hb.py:110-168)
+@pytest.mark.parametrize("c", [0, 1])
+def test_hb_sweep_fixture_is_per_group_run_chain(c):
+    # the reference's own equivalence (hb.py:14-17): group m's chain == run_chain on owner (m,)
+    from oracle import sampler_oracle as so
+    z = golden("hb_sweep.npz")
+    x, y, off = z[f"x_{c}"], z[f"y_{c}"], z[f"off_{c}"]
+    mu, sigma = z[f"prior_{c}"]
+    seed, _, _, sweeps = (int(v) for v in z[f"meta_{c}"])
+    total = 0
+    for m in range(off.size - 1):
+        a, b = off[m], off[m + 1]
+        draws, evals = so.run_chain(x[a:b], y[a:b], mu, sigma, sweeps, 0, seed=seed,
+                                    rng=so.UniformStream(seed, owner=(m,)))
+        total += evals
+        np.testing.assert_allclose(draws, z[f"betas_{c}"][:, m, :], rtol=1e-12, atol=1e-14)
+    assert total == int(z[f"evals_{c}"])
