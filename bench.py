@@ -61,6 +61,8 @@ CONFIGS = {
     "c3": dict(groups=1000, k=20, mean_rows=2000, desc="config 3: G=1000 n_g~Poisson(2000) K=20 HB batched"),
     "c4": dict(h=8192, w=8192, model="ising", desc="config 4: 8192^2 periodic Ising, Philox4x32 (seed,sweep,site)"),
     "c4potts": dict(h=8192, w=8192, model="potts", desc="config 4 Potts q=4 variant, 8192^2 periodic"),
+    "c3sweep": dict(sweep_groups=1000, k=20, mean_rows=2000,
+                    desc="config 3 shape, hierarchical Gibbs sweep: G=1000 groups x K=20 slice updates per sweep"),
     "rng": dict(draws=10_000_000, desc="batch RNG: 10M Gamma(2,3) draws per step on one stream pair (rng.py:246-300)"),
 }
 
@@ -690,6 +692,68 @@ def run_gibbs(args, cfg):
             "cpu_baseline": None if args.no_cpu_baseline else cpu_baseline_other(args.config)}), flush=True)
 
 
+# ---------------------------------------------------------------------------- B200 arm: HB Gibbs sweep
+def run_hb_sweep(args, cfg):
+    """Device-resident hierarchical Gibbs sweeps (hb_sweep, hb.py:138-168) at the config-3 shape."""
+    import torch
+    from paper_1310_1537_b200.glm import DesignMatrix
+    from paper_1310_1537_b200.hb import HbDataset, HbState
+    from paper_1310_1537_b200.sampler import GaussianPrior
+    from paper_1310_1537_b200.synthetic import hb_design
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    x, y, off, _, mu, tau = hb_design(cfg["groups"], cfg["k"], seed=3, mean_rows=cfg["mean_rows"])
+    G, K = cfg["groups"], cfg["k"]
+    ds = HbDataset([DesignMatrix(x[off[g]:off[g + 1]], y[off[g]:off[g + 1]]) for g in range(G)])
+    prior = GaussianPrior(mu, np.full(K, tau))
+    st = HbState(ds, prior, seed=5, device=local)
+    st.sweeps(prior, args.warmup)
+    ev0 = st.total_evals
+    clocks = ClockSampler(local)
+    clocks.start()
+    kernel_ms, walls = [], []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        st.sweeps(prior, 1)
+        walls.append(time.perf_counter() - t0)
+        kernel_ms.append(st.last_kernel_ms)
+    clk = clocks.stop()
+    ms = statistics.mean(kernel_ms)
+    evals = (st.total_evals - ev0) / args.steps
+    n = int(off[-1])
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import sampler_oracle as so
+        sample = 20
+        t0 = time.perf_counter()
+        for g in range(sample):
+            so.run_chain(x[off[g]:off[g + 1]], y[off[g]:off[g + 1]], mu, np.full(K, tau), 1, 0,
+                         rng=so.UniformStream(5, owner=(g,)))
+        dt = (time.perf_counter() - t0) * G / sample
+        cpu = {"value": 1.0 / dt, "unit": "sweeps/s", "cores": 1, "kind": "port",
+               "sample": f"oracle/sampler_oracle.py run_chain (numpy restatement of the reference's per-group "
+                         f"slice-within-Gibbs, hb.py:127-135) for {sample} of {G} groups, 1 sweep, scaled x{G/sample:g}"}
+    peak, src = load_peaks()
+    row_bytes = 24  # xbeta, xt[k], y per row per conditional evaluation (L2-resident group working set)
+    if rank == 0:
+        print(json.dumps({
+            "metric": "hierarchical Gibbs sweeps/s (hb_sweep, every group's K coordinates once)",
+            "value": 1000.0 / ms, "unit": "sweeps/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SURVEY §8d config 3 generator, seed 3); streams seed 5, owner (g,)",
+            "config": {"workload": cfg["desc"], "rows": n, "K": K, "groups": G},
+            "coordinate_updates_per_s": G * K * 1000.0 / ms,
+            "conditional_evals_per_s": evals * 1000.0 / ms,
+            "roofline": {"bound": "latency (CTA-serial slice control flow) -- row-stream rate for context",
+                         "achieved": evals / G * n * row_bytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": evals / G * n * row_bytes / (ms * 1e-3) / 1e9 / peak, "traffic": None,
+                         "peak_source": src},
+            "e2e": {"value": 1.0 / statistics.mean(walls), "unit": "sweeps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 8 * G * (K + 2)},
+            "gpu_launches": args.steps, "clocks": clk, "cpu_baseline": cpu}), flush=True)
+    st.close()
+
+
 # ---------------------------------------------------------------------------- B200 arm: batch RNG
 def run_rng(args, cfg):
     """Device batch RNG: Gamma(2, 3) draws/s on one (uniform, normal) stream
@@ -797,6 +861,11 @@ def main():
         args.steps = args.steps or 20
         args.warmup = args.warmup if args.warmup is not None else 3
         run_chain_bench(args, cfg)
+    elif "sweep_groups" in cfg:
+        args.steps = args.steps or 20
+        args.warmup = args.warmup if args.warmup is not None else 3
+        cfg = dict(cfg, groups=cfg["sweep_groups"])
+        run_hb_sweep(args, cfg)
     elif "groups" in cfg:
         args.steps = args.steps or 200
         args.warmup = args.warmup if args.warmup is not None else 5

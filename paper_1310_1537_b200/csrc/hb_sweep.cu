@@ -56,8 +56,8 @@ __device__ __forceinline__ double hb_logprior(const HbsArgs& a, int k, double v)
   return __dmul_rn(__dmul_rn(-0.5, z), z);
 }
 
-template <int SF, int SN>
-__global__ void __launch_bounds__(kHbsThreads) hb_sweep_kernel(HbsArgs a) {
+template <int SF, int SN, int MINB>
+__global__ void __launch_bounds__(kHbsThreads, MINB) hb_sweep_kernel(HbsArgs a) {
   constexpr int NW = kHbsThreads / 32;
   extern __shared__ double sbeta[];  // [K]
   __shared__ double red[NW][kHbsMaxM];
@@ -473,9 +473,15 @@ int pm_hbs_sweeps(pm_hbs_t h, int32_t n_sweeps, int32_t neval, double slice_widt
   a.max_steps = max_steps;
   a.width = slice_width;
   const char* es = std::getenv("PM_HBS_SPEC");
-  const int spec = es ? std::atoi(es) : 2;
+  const int spec = es ? std::atoi(es) : 1;  // measured on B200 (tools/ab_hbs.sh): no speculation, 8 CTAs/SM
   const size_t smem = sizeof(double) * size_t(h->K);
-  void (*kfn)(HbsArgs) = spec >= 4 ? hb_sweep_kernel<4, 3> : spec >= 2 ? hb_sweep_kernel<2, 2> : hb_sweep_kernel<1, 1>;
+  // CTAs per SM the register budget must allow (1000 groups fit one wave at >= 7 per SM)
+  const char* eb = std::getenv("PM_HBS_MINB");
+  const int minb = eb ? std::atoi(eb) : 8;
+  void (*kfn)(HbsArgs);
+  if (spec >= 4) kfn = hb_sweep_kernel<4, 3, 4>;
+  else if (spec >= 2) kfn = minb >= 8 ? hb_sweep_kernel<2, 2, 8> : minb >= 7 ? hb_sweep_kernel<2, 2, 7> : hb_sweep_kernel<2, 2, 4>;
+  else kfn = minb >= 8 ? hb_sweep_kernel<1, 1, 8> : hb_sweep_kernel<1, 1, 4>;
   int per_sm = 0;
   PM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kHbsThreads, smem));
   if (per_sm < 1) return fail(PM_EDEVICE, "hb sweep kernel cannot be resident");

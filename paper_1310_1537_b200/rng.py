@@ -95,9 +95,12 @@ class DeviateBuffer:
         self._carry: float | None = None
         self._gen_pos = 0                     # stream index of the generator's next output
         self._block_start = -self.capacity    # stream index of data[0] (no block yet)
+        self._seek_to: int | None = None      # pending generator reposition (skip)
 
     def refill(self) -> None:
         """Fill data[0:capacity] with the next block of the base stream."""
+        if self._seek_to is not None:
+            self._apply_seek()
         self._block_start = self._gen_pos
         if self.kind is BufferKind.UNIFORM01:
             self.data[:] = self._gen.random(self.capacity)
@@ -174,20 +177,25 @@ class DeviateBuffer:
         if n <= self.capacity - self.cursor:
             self.cursor += n
         else:
-            # reposition the generator at the target index; the next use refills from there
+            # the generator is repositioned lazily, at the next refill (device paths skip
+            # thousands of streams per call and most are never read on the host)
             target = self.position + n
-            if self.kind is BufferKind.UNIFORM01:
-                _seek(self._gen, target)
-                self._carry = None
-            else:
-                # normal j is half of uniform pair j//2; an odd target starts on a carried sine
-                _seek(self._gen, target - (target & 1))
-                self._carry = float(_box_muller_pairs(self._gen, 1)[1]) if target & 1 else None
-                target += target & 1
-            self._gen_pos = target
-            self._block_start = self.position + n - self.capacity
+            self._seek_to = target
+            self._block_start = target - self.capacity
             self.cursor = self.capacity
         self.consumed += n
+
+    def _apply_seek(self) -> None:
+        target, self._seek_to = self._seek_to, None
+        if self.kind is BufferKind.UNIFORM01:
+            _seek(self._gen, target)
+            self._carry = None
+        else:
+            # normal j is half of uniform pair j//2; an odd target starts on a carried sine
+            _seek(self._gen, target - (target & 1))
+            self._carry = float(_box_muller_pairs(self._gen, 1)[1]) if target & 1 else None
+            target += target & 1
+        self._gen_pos = target
 
     def take_device(self, n: int, device: int = 0) -> np.ndarray:
         """The next n deviates generated on the device (pm_rng_fill); advances the buffer
