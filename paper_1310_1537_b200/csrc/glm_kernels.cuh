@@ -114,12 +114,29 @@ __device__ __forceinline__ void consume_tile(const XT* xs, const double* ys, int
     nll_acc += (valid && lane < R) ? nll : 0.0;
     if (GRAD) {
       w = valid ? w : 0.0;
+      // NS interleaved accumulator sets so at least ~8 independent DFMA chains are in flight
+      // (one set of KC chains would serialise on DFMA latency at small KC)
+      constexpr int NS = KC >= 8 ? 1 : ((8 / KC) < R ? (8 / KC) : R);
+      double ga[NS > 1 ? NS - 1 : 1][KC];
+#pragma unroll
+      for (int s = 0; s + 1 < NS; ++s)
+#pragma unroll
+        for (int j = 0; j < KC; ++j) ga[s][j] = 0.0;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const double wr = shfl_d(w, r);
+        if (r % NS == 0) {
 #pragma unroll
-        for (int j = 0; j < KC; ++j) g[j] = fma(wr, x[r][j], g[j]);
+          for (int j = 0; j < KC; ++j) g[j] = fma(wr, x[r][j], g[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < KC; ++j) ga[r % NS - 1][j] = fma(wr, x[r][j], ga[r % NS - 1][j]);
+        }
       }
+#pragma unroll
+      for (int s = 0; s + 1 < NS; ++s)
+#pragma unroll
+        for (int j = 0; j < KC; ++j) g[j] += ga[s][j];
     }
   }
 }

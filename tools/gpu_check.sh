@@ -6,7 +6,7 @@ rm -f gpurun_out/rc.txt
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/smi.txt 2>&1
 if [ "${TESTS:-1}" = "1" ]; then
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/rc.txt
-  for t in test_gpu_glm test_gpu_diff test_gpu_ising test_gpu_hb; do
+  for t in test_gpu_glm test_gpu_diff test_gpu_ising test_gpu_hb test_gpu_denoise test_gpu_rng test_gpu_hb_sweep test_cli; do
     timeout 900 python -m pytest tests/$t.py -m gpu -q > gpurun_out/$t.log 2>&1; echo "$t rc=$?" >> gpurun_out/rc.txt
   done
 fi
@@ -14,8 +14,8 @@ if [ "${BENCH:-1}" = "1" ]; then
   timeout 900 python bench.py > gpurun_out/bench_c1.log 2>&1; echo "bench rc=$?" >> gpurun_out/rc.txt
 fi
 if [ "${EXTRA:-1}" = "1" ]; then
-  for c in c1f32 c0 c2 c3 c4 c4potts; do
-    timeout 600 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_$c.log 2>&1; echo "bench $c rc=$?" >> gpurun_out/rc.txt
+  for c in c1f32 c0 c2 c3 c3sweep c4 c4potts rng; do
+    timeout 600 python bench.py --config $c ${EXTRA_ARGS:---no-cpu-baseline} > gpurun_out/bench_$c.log 2>&1; echo "bench $c rc=$?" >> gpurun_out/rc.txt
   done
 fi
 if [ "${PROFILE:-1}" = "1" ]; then
