@@ -22,6 +22,8 @@ constexpr int kMaxStages = 16;
 constexpr int kHbNCW = 4;
 constexpr int kHbThreads = (kHbNCW + 1) * 32;
 constexpr int kHbMaxStages = 6;
+constexpr int kHbRowsNCW = 7;                         // small-K row-per-lane path (1 CTA/SM)
+constexpr int kHbRowsThreads = (kHbRowsNCW + 1) * 32;
 constexpr int kWideThreads = 256;
 constexpr int kMaxKC = 8;                    // stream kernel handles K <= 256
 
@@ -707,14 +709,26 @@ struct pm_hb_s {
   double* out_g = nullptr;
   double* pin_in = nullptr;    // G*K + 2K
   double* pin_out = nullptr;   // G + G*K
+  // small-K row-per-lane path (even K <= 32): balanced tile ranges + segment fold
+  bool rows = false;
+  int rows_grid = 0, rows_stages = 0;
+  size_t rows_smem = 0;
+  int64_t n_tiles = 0;
+  int* seg_base = nullptr;     // [rows_grid + 1]
+  int* gseg = nullptr;         // [G + 1]
+  double* part = nullptr;      // [nseg][kHbRowsNCW][K+1]
 };
 
 namespace {
 
 void free_hb(pm_hb_s* h) {
   for (void* p : {(void*)h->X, (void*)h->y, (void*)h->poff, (void*)h->nrows, (void*)h->betas, (void*)h->mu_dev,
-                  (void*)h->sigma_dev, (void*)h->out_f, (void*)h->out_g})
+                  (void*)h->sigma_dev, (void*)h->out_f, (void*)h->out_g, (void*)h->seg_base, (void*)h->gseg,
+                  (void*)h->part})
     if (p) cudaFree(p);
+  h->seg_base = h->gseg = nullptr;
+  h->part = nullptr;
+  h->rows = false;
   if (h->pin_in) cudaFreeHost(h->pin_in);
   if (h->pin_out) cudaFreeHost(h->pin_out);
   h->X = h->y = nullptr;
@@ -734,6 +748,62 @@ cudaError_t launch_hb(const HbArgs& a, int grid, size_t smem, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   kern<<<grid, kHbThreads, smem, st>>>(a);
   return cudaGetLastError();
+}
+
+template <int KMAX, bool GRAD>
+cudaError_t launch_hb_rows(const pm_hb_s* h, const HbArgs& a, cudaStream_t st) {
+  static std::atomic<uint64_t> attr{0};
+  auto kern = hb_rows_kernel<KMAX, GRAD, kHbRowsNCW>;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), attr);
+  if (e != cudaSuccess) return e;
+  HbRowsArgs r;
+  r.X = a.X;
+  r.y = a.y;
+  r.poff = a.poff;
+  r.nrows = a.nrows;
+  r.seg_base = h->seg_base;
+  r.G = h->G;
+  r.K = h->K;
+  r.stages = h->rows_stages;
+  r.n_tiles = h->n_tiles;
+  r.betas = a.betas;
+  r.part = h->part;
+  kern<<<h->rows_grid, kHbRowsThreads, h->rows_smem, st>>>(r);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  hb_fold_kernel<GRAD><<<h->G, 64, 0, st>>>(h->part, h->gseg, kHbRowsNCW, h->K, a.betas, a.mu, a.sigma, a.out_f,
+                                            a.out_g);
+  return cudaGetLastError();
+}
+
+using HbRowsLaunch = cudaError_t (*)(const pm_hb_s*, const HbArgs&, cudaStream_t);
+
+template <bool GRAD>
+HbLaunch pick_hb(int kc);
+
+template <bool GRAD>
+HbRowsLaunch pick_hb_rows(int K) {
+  switch ((K + 3) / 4 * 4) {
+    case 4: return launch_hb_rows<4, GRAD>;
+    case 8: return launch_hb_rows<8, GRAD>;
+    case 12: return launch_hb_rows<12, GRAD>;
+    case 16: return launch_hb_rows<16, GRAD>;
+    case 20: return launch_hb_rows<20, GRAD>;
+    case 24: return launch_hb_rows<24, GRAD>;
+    case 28: return launch_hb_rows<28, GRAD>;
+    case 32: return launch_hb_rows<32, GRAD>;
+  }
+  return nullptr;
+}
+
+// one launch of whichever HB path the handle uses
+cudaError_t launch_hb_any(const pm_hb_s* h, const HbArgs& a, bool grad) {
+  if (h->rows) {
+    HbRowsLaunch fn = grad ? pick_hb_rows<true>(h->K) : pick_hb_rows<false>(h->K);
+    return fn(h, a, h->stream);
+  }
+  HbLaunch fn = grad ? pick_hb<true>((h->K + 31) / 32) : pick_hb<false>((h->K + 31) / 32);
+  return fn(a, h->G, h->smem, h->stream);
 }
 
 template <bool GRAD>
@@ -842,6 +912,44 @@ int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64_t* off
   while (S > 2 && fixed + S * per_stage > cap) --S;
   h->stages = S;
   h->smem = stream_smem_bytes(K, 8, S, kHbNCW);
+  // small-K path: equal contiguous tile ranges, one CTA per SM
+  const char* env_rows = std::getenv("PM_HB_ROWS");
+  if (K % 2 == 0 && K <= 32 && !(env_rows && env_rows[0] == '0')) {
+    const int C = h->sms;
+    const int64_t T = NP / kTileRows;
+    auto group_of = [&](int64_t tile) {
+      return int(std::upper_bound(poff.begin(), poff.end(), tile * kTileRows) - poff.begin()) - 1;
+    };
+    std::vector<int> seg_base(C + 1, 0), gseg(G + 1, -1);
+    int nseg = 0;
+    for (int c = 0; c < C; ++c) {
+      seg_base[c] = nseg;
+      const int64_t t0 = int64_t(c) * T / C, t1 = int64_t(c + 1) * T / C;
+      if (t0 >= t1) continue;
+      const int gf = group_of(t0), gl = group_of(t1 - 1);
+      for (int g2 = gf; g2 <= gl; ++g2) {
+        if (gseg[g2] < 0) gseg[g2] = nseg;
+        ++nseg;
+      }
+    }
+    seg_base[C] = nseg;
+    gseg[G] = nseg;
+    const size_t per = align_up(size_t(kTileRows) * K * 8, 128) + 32 * 8 + 2 * 8;
+    const size_t fixed_r = stream_smem_bytes(K, 8, 0, 0);
+    int Sr = 5 * kHbRowsNCW;
+    while (Sr > kHbRowsNCW && fixed_r + Sr * per > 200 * 1024) Sr -= kHbRowsNCW;
+    if (const char* es = std::getenv("PM_HB_ROWS_STAGES")) Sr = std::max(kHbRowsNCW, std::min(Sr, std::atoi(es)));
+    PM_CUDA(cudaMalloc(&h->seg_base, sizeof(int) * (C + 1)));
+    PM_CUDA(cudaMalloc(&h->gseg, sizeof(int) * (G + 1)));
+    PM_CUDA(cudaMalloc(&h->part, sizeof(double) * size_t(nseg) * kHbRowsNCW * (K + 1)));
+    PM_CUDA(cudaMemcpy(h->seg_base, seg_base.data(), sizeof(int) * (C + 1), cudaMemcpyHostToDevice));
+    PM_CUDA(cudaMemcpy(h->gseg, gseg.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice));
+    h->rows = true;
+    h->rows_grid = C;
+    h->rows_stages = Sr;
+    h->rows_smem = stream_smem_bytes(K, 8, Sr, 0);
+    h->n_tiles = T;
+  }
   return PM_OK;
 }
 
@@ -897,8 +1005,7 @@ int pm_hb_eval(pm_hb_t h, const double* betas, const double* mu, const double* s
   if (rc) return rc;
   const int G = h->G, K = h->K;
   const bool grad = want_grad != 0 && g_out != nullptr;
-  HbLaunch fn = grad ? pick_hb<true>((K + 31) / 32) : pick_hb<false>((K + 31) / 32);
-  cudaError_t e = fn(a, G, h->smem, h->stream);
+  cudaError_t e = launch_hb_any(h, a, grad);
   if (e != cudaSuccess) return cuda_fail(e, "hb kernel launch");
   PM_CUDA(cudaMemcpyAsync(h->pin_out, h->out_f, sizeof(double) * G, cudaMemcpyDeviceToHost, h->stream));
   if (grad)
@@ -925,13 +1032,12 @@ int pm_hb_time_evals(pm_hb_t h, const double* betas, const double* mu, const dou
   HbArgs a;
   int rc = hb_stage(h, betas, mu, sigma, a);
   if (rc) return rc;
-  HbLaunch fn = want_grad ? pick_hb<true>((h->K + 31) / 32) : pick_hb<false>((h->K + 31) / 32);
   cudaEvent_t e0, e1;
   PM_CUDA(cudaEventCreate(&e0));
   PM_CUDA(cudaEventCreate(&e1));
   PM_CUDA(cudaEventRecord(e0, h->stream));
   for (int i = 0; i < n; ++i) {
-    cudaError_t e = fn(a, h->G, h->smem, h->stream);
+    cudaError_t e = launch_hb_any(h, a, want_grad != 0);
     if (e != cudaSuccess) return cuda_fail(e, "hb kernel launch");
   }
   PM_CUDA(cudaEventRecord(e1, h->stream));

@@ -230,4 +230,200 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 3) hb_kernel(HbArgs a) {
   }
 }
 
+// ---------------------------------------------------------------- small-K hierarchical path
+// For even K <= 32 the column-per-lane layout leaves lanes idle (K=20: 12 of 32) and pays a
+// transpose-reduce per row; here each lane owns one ROW of a 32-row tile: its K values come
+// from shared memory as 16-byte loads, the dot product runs in two interleaved chains, the
+// logistic terms are computed once per row, and the gradient accumulates in K registers.
+// The padded tiles of all groups are split into equal contiguous ranges, one per CTA
+// (1 CTA/SM), so no wave quantisation; a CTA's range covers pieces ("segments") of a few
+// groups.  Every consumer warp writes one (nll, g[K]) partial per segment (zeros if it had
+// no tile there) and hb_fold_kernel sums the partials of each group in a fixed order
+// (segment, warp) and adds the prior: deterministic for a given device.
+struct HbRowsArgs {
+  const double* X;
+  const double* y;
+  const int64_t* poff;   // [G+1] padded row offsets (multiples of 32)
+  const int64_t* nrows;  // [G]
+  const int* seg_base;   // [grid+1] first segment of each CTA
+  int G, K, stages;
+  int64_t n_tiles;       // poff[G] / 32
+  const double* betas;   // [G][K]
+  double* part;          // [nseg][NCW][K+1]
+};
+
+template <int KMAX, bool GRAD>
+__device__ __forceinline__ void consume_tile_rows(const double* xs, const double* ys, int K, int lane, int64_t row0,
+                                                  int64_t row_limit, const double (&b)[KMAX], double (&g)[KMAX],
+                                                  double& nll_acc, uint64_t* empty) {
+  const double* xr = xs + lane * K;  // K even: 16-byte aligned rows
+  double x[KMAX];
+  double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+  for (int k = 0; k < KMAX; k += 2) {
+    if (k < K) {
+      const double2 v = *reinterpret_cast<const double2*>(xr + k);
+      x[k] = v.x;
+      x[k + 1] = v.y;
+    } else {
+      x[k] = 0.0;
+      x[k + 1] = 0.0;
+    }
+    t0 = fma(x[k], b[k], t0);
+    t1 = fma(x[k + 1], b[k + 1], t1);
+  }
+  const double yv = ys[lane];
+  mbar_arrive_after(empty, t0 + t1 + yv, lane, const_cast<double*>(xs));  // t0, t1, yv consume every load
+  double nll, w;
+  row_terms(t0 + t1, yv, nll, w);
+  const bool valid = row0 + lane < row_limit;
+  nll_acc += valid ? nll : 0.0;
+  if (GRAD) {
+    w = valid ? w : 0.0;
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) g[k] = fma(w, x[k], g[k]);
+  }
+}
+
+__device__ __forceinline__ int group_of_tile(const int64_t* poff, int G, int64_t tile) {
+  // largest g with poff[g] / 32 <= tile
+  int lo = 0, hi = G - 1;
+  const int64_t row = tile * kTileRows;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (poff[mid] <= row) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <int KMAX, bool GRAD, int NCW>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int K = a.K;
+  const int S = a.stages;
+  const StreamSmem sm = carve_stream_smem(smem_raw, K, sizeof(double), S, 0);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t C = gridDim.x, c = blockIdx.x;
+  const int64_t t0 = c * a.n_tiles / C, t1 = (c + 1) * a.n_tiles / C;
+  if (t0 >= t1) return;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int g_first = group_of_tile(a.poff, a.G, t0);
+  const int g_last = group_of_tile(a.poff, a.G, t1 - 1);
+  const int seg0 = a.seg_base[c];
+  const int64_t n_mine = t1 - t0;
+  const uint32_t tile_bytes = uint32_t(kTileRows) * K * sizeof(double);
+  const size_t tile_pitch = align_up(tile_bytes, 128);
+  const int nact = S < NCW ? S : NCW;
+  const int Se = S - S % nact;
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t n = 0;
+      for (int64_t i = 0; i < n_mine; ++i) {
+        if (n > 0) mbar_wait(&sm.empty[s], (n - 1) & 1);
+        const int64_t tile = t0 + i;
+        mbar_arrive_expect_tx(&sm.full[s], tile_bytes + 32 * sizeof(double));
+        bulk_g2s(sm.xs + size_t(s) * tile_pitch, a.X + tile * int64_t(kTileRows) * K, tile_bytes, &sm.full[s]);
+        bulk_g2s(sm.ys + size_t(s) * 32, a.y + tile * kTileRows, 32 * sizeof(double), &sm.full[s]);
+        if (++s == Se) {
+          s = 0;
+          ++n;
+        }
+      }
+    }
+    return;
+  }
+  const int cw = warp - 1;
+  if (cw >= nact) return;
+  int cur = g_first;
+  double b[KMAX], g[KMAX];
+  double nll = 0.0;
+  auto load_beta = [&](int grp) {
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      b[k] = k < K ? __ldg(a.betas + int64_t(grp) * K + k) : 0.0;
+      g[k] = 0.0;
+    }
+    nll = 0.0;
+  };
+  // partial of group `grp` (this warp's share of segment seg0 + grp - g_first)
+  auto flush = [&](int grp) {
+    double* dst = a.part + (size_t(seg0 + grp - g_first) * NCW + cw) * (K + 1);
+    const double ns = warp_sum(nll);
+    if (lane == 0) dst[0] = ns;
+    if (GRAD) {
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        const double v = warp_sum(g[k]);
+        if (lane == 0 && k < K) dst[1 + k] = v;
+      }
+    }
+  };
+  load_beta(cur);
+  int s = cw;
+  uint32_t n = 0;
+  for (int64_t i = cw; i < n_mine; i += nact) {
+    const int64_t tile = t0 + i;
+    while (tile * kTileRows >= a.poff[cur + 1]) {
+      flush(cur);
+      load_beta(++cur);
+    }
+    mbar_wait(&sm.full[s], n & 1);
+    consume_tile_rows<KMAX, GRAD>(reinterpret_cast<const double*>(sm.xs + size_t(s) * tile_pitch),
+                                  sm.ys + size_t(s) * 32, K, lane, tile * kTileRows, a.poff[cur] + a.nrows[cur], b, g,
+                                  nll, &sm.empty[s]);
+    s += nact;
+    if (s >= Se) {
+      s = cw;
+      ++n;
+    }
+  }
+  flush(cur);
+  while (cur < g_last) {  // segments after this warp's last tile: zero partials
+    load_beta(++cur);
+    flush(cur);
+  }
+}
+
+// Per group: fold the partials of its segments (gseg[g] .. gseg[g+1]-1) and warps in order.
+template <bool GRAD>
+__global__ void hb_fold_kernel(const double* part, const int* gseg, int nw, int K, const double* betas,
+                               const double* mu, const double* sigma, double* out_f, double* out_g) {
+  const int grp = blockIdx.x;
+  const int s0 = gseg[grp], s1 = gseg[grp + 1];
+  for (int c = threadIdx.x; c <= K; c += blockDim.x) {
+    if (c > 0 && !GRAD) break;
+    double acc = 0.0;
+    for (int s = s0; s < s1; ++s)
+      for (int w = 0; w < nw; ++w) acc += part[(size_t(s) * nw + w) * (K + 1) + c];
+    if (c == 0) {
+      double f = -acc;
+      if (mu) {
+        for (int k = 0; k < K; ++k) {
+          const double z = (betas[size_t(grp) * K + k] - mu[k]) / sigma[k];
+          f += -0.5 * z * z;
+        }
+      }
+      out_f[grp] = f;
+    } else {
+      const int k = c - 1;
+      double gk = acc;
+      if (mu) {
+        const double sg = sigma[k];
+        gk -= (betas[size_t(grp) * K + k] - mu[k]) / (sg * sg);
+      }
+      out_g[size_t(grp) * K + k] = gk;
+    }
+  }
+}
+
 }  // namespace pm

@@ -104,8 +104,11 @@ __device__ __forceinline__ void consume_tile(const XT* xs, const double* ys, int
     const int rr = sub * R + (lane & (R - 1));
     const double yv = ys[rr];
     if (sub == 32 / R - 1) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty);  // release semantics order this warp's smem reads
+      // the last sub-tile's loads feed v[] and yv (earlier sub-tiles were consumed before)
+      double dep = yv;
+#pragma unroll
+      for (int r = 0; r < R; ++r) dep += v[r];
+      mbar_arrive_after(empty, dep, lane, const_cast<XT*>(xs));
     }
     const double t = transpose_reduce<R>(v, lane);
     double nll, w;

@@ -86,6 +86,28 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 
+// Release a consumed shared-memory stage only after the warp's loads from it have LANDED.
+// Shared loads complete asynchronously: the warp waits on a load's scoreboard only when an
+// instruction reads its destination register, and neither __syncwarp nor the arrive reads
+// them -- so an arrive issued right after the loads can hand the stage to the producer (whose
+// next TMA copy overwrites it) while the loads are still in flight.  `dep` must be computed
+// from every loaded value; storing it into the stage being released (its own first 128
+// bytes: the warp is done reading them, and the producer overwrites the stage next) makes
+// the warp wait for all of them, and the store cannot move past the arrive (memory clobber).
+// (Measured: y values read from an overwritten stage, K=32 row-per-lane HB kernel, before
+// this guard.)  No extra shared memory: the stream kernels size their ring to the limit.
+// The producer refills the stage through the ASYNC proxy (TMA), so the generic-proxy
+// accesses above are ordered before it with fence.proxy.async by every lane (without it a
+// TMA write can land before this warp's earlier generic accesses to the stage take effect).
+__device__ __forceinline__ void mbar_arrive_after(uint64_t* bar, double dep, int lane, void* stage) {
+  reinterpret_cast<volatile uint32_t*>(stage)[lane] = __double2loint(dep);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0)
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+                 : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

@@ -60,3 +60,30 @@ def test_wide_k_and_validation(gpu):
         hb_log_posterior_grad(csr, betas[:3])
     with pytest.raises(ValueError):
         CsrGroups(x, y, np.array([0, 5, 5, x.shape[0]]))
+
+
+@pytest.mark.parametrize("k", [2, 4, 20, 22, 32])
+@pytest.mark.parametrize("layout", ["tiny_groups", "huge_groups", "single"])
+def test_row_per_lane_path_segments(gpu, k, layout, monkeypatch):
+    # even K <= 32 takes the row-per-lane kernel with balanced tile ranges: groups split across
+    # CTAs (huge), many groups inside one CTA's range (tiny), one group over the whole grid
+    gen = np.random.default_rng(k)
+    sizes = {"tiny_groups": gen.integers(1, 40, 5000), "huge_groups": [100_000, 37, 250_001],
+             "single": [77_777]}[layout]
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    x = gen.standard_normal((int(off[-1]), k))
+    y = (gen.random(int(off[-1])) < 0.45).astype(float)
+    betas = gen.normal(0, 0.3, (len(sizes), k))
+    mu, sigma = gen.normal(0, 0.5, k), np.full(k, 0.7)
+    prior = GaussianPrior(mu, sigma)
+    res = hb_log_posterior_grad(CsrGroups(x, y, off), betas, prior)
+    f = np.array([r.f for r in res])
+    g = np.stack([r.g for r in res])
+    fr, gr = gl.hb_log_posterior_grad(x, y, off, betas, mu, sigma)
+    check(f, g, fr, gr)
+    res_f = hb_log_posterior_grad(CsrGroups(x, y, off), betas, prior, want_grad=False)
+    np.testing.assert_array_equal(np.array([r.f for r in res_f]), f)
+    # the column-per-lane kernel agrees to rounding
+    monkeypatch.setenv("PM_HB_ROWS", "0")
+    res0 = hb_log_posterior_grad(CsrGroups(x, y, off), betas, prior)
+    check(np.array([r.f for r in res0]), np.stack([r.g for r in res0]), f, g)
