@@ -22,7 +22,7 @@ constexpr int kMaxStages = 16;
 constexpr int kHbNCW = 4;
 constexpr int kHbThreads = (kHbNCW + 1) * 32;
 constexpr int kHbMaxStages = 6;
-constexpr int kHbRowsNCW = 7;                         // small-K row-per-lane path (1 CTA/SM)
+constexpr int kHbRowsNCW = 15;                        // small-K row-per-lane path (1 CTA/SM)
 constexpr int kHbRowsThreads = (kHbRowsNCW + 1) * 32;
 constexpr int kWideThreads = 256;
 constexpr int kMaxKC = 8;                    // stream kernel handles K <= 256
@@ -711,7 +711,7 @@ struct pm_hb_s {
   double* pin_out = nullptr;   // G + G*K
   // small-K row-per-lane path (even K <= 32): balanced tile ranges + segment fold
   bool rows = false;
-  int rows_grid = 0, rows_stages = 0;
+  int rows_grid = 0, rows_stages = 0, rows_ncw = 7, rows_tps = 1;
   size_t rows_smem = 0;
   int64_t n_tiles = 0;
   int* seg_base = nullptr;     // [rows_grid + 1]
@@ -750,10 +750,10 @@ cudaError_t launch_hb(const HbArgs& a, int grid, size_t smem, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int KMAX, bool GRAD>
-cudaError_t launch_hb_rows(const pm_hb_s* h, const HbArgs& a, cudaStream_t st) {
+template <int KMAX, bool GRAD, int NCW>
+cudaError_t launch_hb_rows_n(const pm_hb_s* h, const HbArgs& a, cudaStream_t st) {
   static std::atomic<uint64_t> attr{0};
-  auto kern = hb_rows_kernel<KMAX, GRAD, kHbRowsNCW>;
+  auto kern = hb_rows_kernel<KMAX, GRAD, NCW>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), attr);
   if (e != cudaSuccess) return e;
   HbRowsArgs r;
@@ -765,15 +765,20 @@ cudaError_t launch_hb_rows(const pm_hb_s* h, const HbArgs& a, cudaStream_t st) {
   r.G = h->G;
   r.K = h->K;
   r.stages = h->rows_stages;
+  r.tps = h->rows_tps;
   r.n_tiles = h->n_tiles;
   r.betas = a.betas;
   r.part = h->part;
-  kern<<<h->rows_grid, kHbRowsThreads, h->rows_smem, st>>>(r);
+  kern<<<h->rows_grid, (NCW + 1) * 32, h->rows_smem, st>>>(r);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  hb_fold_kernel<GRAD><<<h->G, 64, 0, st>>>(h->part, h->gseg, kHbRowsNCW, h->K, a.betas, a.mu, a.sigma, a.out_f,
-                                            a.out_g);
+  hb_fold_kernel<GRAD><<<h->G, 64, 0, st>>>(h->part, h->gseg, NCW, h->K, a.betas, a.mu, a.sigma, a.out_f, a.out_g);
   return cudaGetLastError();
+}
+
+template <int KMAX, bool GRAD>
+cudaError_t launch_hb_rows(const pm_hb_s* h, const HbArgs& a, cudaStream_t st) {
+  return h->rows_ncw == 7 ? launch_hb_rows_n<KMAX, GRAD, 7>(h, a, st) : launch_hb_rows_n<KMAX, GRAD, 15>(h, a, st);
 }
 
 using HbRowsLaunch = cudaError_t (*)(const pm_hb_s*, const HbArgs&, cudaStream_t);
@@ -934,20 +939,29 @@ int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64_t* off
     }
     seg_base[C] = nseg;
     gseg[G] = nseg;
-    const size_t per = align_up(size_t(kTileRows) * K * 8, 128) + 32 * 8 + 2 * 8;
-    const size_t fixed_r = stream_smem_bytes(K, 8, 0, 0);
-    int Sr = 5 * kHbRowsNCW;
-    while (Sr > kHbRowsNCW && fixed_r + Sr * per > 200 * 1024) Sr -= kHbRowsNCW;
-    if (const char* es = std::getenv("PM_HB_ROWS_STAGES")) Sr = std::max(kHbRowsNCW, std::min(Sr, std::atoi(es)));
+    // consumer warps (7 or 15), tiles per stage, stages (a multiple of the consumer count,
+    // at least two per warp when they fit): knobs PM_HB_ROWS_NCW / _TPS / _STAGES for A/B
+    const char* e_ncw = std::getenv("PM_HB_ROWS_NCW");
+    const char* e_tps = std::getenv("PM_HB_ROWS_TPS");
+    const char* e_st = std::getenv("PM_HB_ROWS_STAGES");
+    const int ncw = (e_ncw && std::atoi(e_ncw) == 15) ? 15 : 7;
+    int tps = e_tps ? std::max(1, std::min(8, std::atoi(e_tps))) : 2;
+    const size_t cap = 200 * 1024;
+    while (tps > 1 && stream_smem_bytes(K, 8, ncw * tps, ncw) > cap) --tps;
+    int Sr = 4 * ncw;
+    while (Sr > ncw && stream_smem_bytes(K, 8, Sr * tps, ncw) > cap) Sr -= ncw;
+    if (e_st) Sr = std::max(ncw, std::min(Sr, std::atoi(e_st) / ncw * ncw));
     PM_CUDA(cudaMalloc(&h->seg_base, sizeof(int) * (C + 1)));
     PM_CUDA(cudaMalloc(&h->gseg, sizeof(int) * (G + 1)));
-    PM_CUDA(cudaMalloc(&h->part, sizeof(double) * size_t(nseg) * kHbRowsNCW * (K + 1)));
+    PM_CUDA(cudaMalloc(&h->part, sizeof(double) * size_t(nseg) * ncw * (K + 1)));
     PM_CUDA(cudaMemcpy(h->seg_base, seg_base.data(), sizeof(int) * (C + 1), cudaMemcpyHostToDevice));
     PM_CUDA(cudaMemcpy(h->gseg, gseg.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice));
     h->rows = true;
     h->rows_grid = C;
+    h->rows_ncw = ncw;
+    h->rows_tps = tps;
     h->rows_stages = Sr;
-    h->rows_smem = stream_smem_bytes(K, 8, Sr, 0);
+    h->rows_smem = stream_smem_bytes(K, 8, Sr * tps, ncw);
     h->n_tiles = T;
   }
   return PM_OK;

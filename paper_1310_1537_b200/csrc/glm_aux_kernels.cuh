@@ -246,16 +246,20 @@ struct HbRowsArgs {
   const int64_t* poff;   // [G+1] padded row offsets (multiples of 32)
   const int64_t* nrows;  // [G]
   const int* seg_base;   // [grid+1] first segment of each CTA
-  int G, K, stages;
+  int G, K, stages, tps;
   int64_t n_tiles;       // poff[G] / 32
   const double* betas;   // [G][K]
   double* part;          // [nseg][NCW][K+1]
 };
 
+// b: this warp's copy of the group's beta in shared memory (all lanes read the same address:
+// broadcast), so only x[] and g[] occupy registers and 15 consumer warps fit per SM.
+// `dep` accumulates a value computed from every shared load of the tile; the caller releases
+// the stage with mbar_arrive_after(dep) once all of the stage's tiles are consumed.
 template <int KMAX, bool GRAD>
 __device__ __forceinline__ void consume_tile_rows(const double* xs, const double* ys, int K, int lane, int64_t row0,
-                                                  int64_t row_limit, const double (&b)[KMAX], double (&g)[KMAX],
-                                                  double& nll_acc, uint64_t* empty) {
+                                                  int64_t row_limit, const double* b, double (&g)[KMAX],
+                                                  double& nll_acc, double& dep) {
   const double* xr = xs + lane * K;  // K even: 16-byte aligned rows
   double x[KMAX];
   double t0 = 0.0, t1 = 0.0;
@@ -263,17 +267,18 @@ __device__ __forceinline__ void consume_tile_rows(const double* xs, const double
   for (int k = 0; k < KMAX; k += 2) {
     if (k < K) {
       const double2 v = *reinterpret_cast<const double2*>(xr + k);
+      const double2 bb = *reinterpret_cast<const double2*>(b + k);
       x[k] = v.x;
       x[k + 1] = v.y;
+      t0 = fma(x[k], bb.x, t0);
+      t1 = fma(x[k + 1], bb.y, t1);
     } else {
       x[k] = 0.0;
       x[k + 1] = 0.0;
     }
-    t0 = fma(x[k], b[k], t0);
-    t1 = fma(x[k + 1], b[k + 1], t1);
   }
   const double yv = ys[lane];
-  mbar_arrive_after(empty, t0 + t1 + yv, lane, const_cast<double*>(xs));  // t0, t1, yv consume every load
+  dep += t0 + t1 + yv;  // t0, t1, yv consume every load of this tile
   double nll, w;
   row_terms(t0 + t1, yv, nll, w);
   const bool valid = row0 + lane < row_limit;
@@ -302,7 +307,10 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int K = a.K;
   const int S = a.stages;
-  const StreamSmem sm = carve_stream_smem(smem_raw, K, sizeof(double), S, 0);
+  const int TPS = a.tps;  // 32-row tiles per stage: one bulk copy moves TPS consecutive tiles
+  // carve S*TPS tile slots (stage s = slots s*TPS ..): contiguous, since 32*K*8 is a multiple
+  // of 128 for even K; only the first S barrier pairs are used.  wg: per-warp beta copies.
+  const StreamSmem sm = carve_stream_smem(smem_raw, K, sizeof(double), S * TPS, NCW);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t C = gridDim.x, c = blockIdx.x;
@@ -320,20 +328,22 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a
   const int g_last = group_of_tile(a.poff, a.G, t1 - 1);
   const int seg0 = a.seg_base[c];
   const int64_t n_mine = t1 - t0;
+  const int64_t n_units = (n_mine + TPS - 1) / TPS;
   const uint32_t tile_bytes = uint32_t(kTileRows) * K * sizeof(double);
-  const size_t tile_pitch = align_up(tile_bytes, 128);
+  const size_t stage_pitch = size_t(tile_bytes) * TPS;
   const int nact = S < NCW ? S : NCW;
   const int Se = S - S % nact;
   if (warp == 0) {
     if (lane == 0) {
       int s = 0;
       uint32_t n = 0;
-      for (int64_t i = 0; i < n_mine; ++i) {
+      for (int64_t i = 0; i < n_units; ++i) {
         if (n > 0) mbar_wait(&sm.empty[s], (n - 1) & 1);
-        const int64_t tile = t0 + i;
-        mbar_arrive_expect_tx(&sm.full[s], tile_bytes + 32 * sizeof(double));
-        bulk_g2s(sm.xs + size_t(s) * tile_pitch, a.X + tile * int64_t(kTileRows) * K, tile_bytes, &sm.full[s]);
-        bulk_g2s(sm.ys + size_t(s) * 32, a.y + tile * kTileRows, 32 * sizeof(double), &sm.full[s]);
+        const int64_t tile = t0 + i * TPS;
+        const uint32_t nt = uint32_t(t1 - tile < TPS ? t1 - tile : TPS);
+        mbar_arrive_expect_tx(&sm.full[s], nt * (tile_bytes + 32 * sizeof(double)));
+        bulk_g2s(sm.xs + size_t(s) * stage_pitch, a.X + tile * int64_t(kTileRows) * K, nt * tile_bytes, &sm.full[s]);
+        bulk_g2s(sm.ys + size_t(s) * 32 * TPS, a.y + tile * kTileRows, nt * 32 * sizeof(double), &sm.full[s]);
         if (++s == Se) {
           s = 0;
           ++n;
@@ -345,14 +355,15 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a
   const int cw = warp - 1;
   if (cw >= nact) return;
   int cur = g_first;
-  double b[KMAX], g[KMAX];
+  double* b = sm.wg + size_t(cw) * K;
+  double g[KMAX];
   double nll = 0.0;
   auto load_beta = [&](int grp) {
+    __syncwarp();  // previous group's reads of b are done
+    for (int k = lane; k < K; k += 32) b[k] = __ldg(a.betas + int64_t(grp) * K + k);
+    __syncwarp();
 #pragma unroll
-    for (int k = 0; k < KMAX; ++k) {
-      b[k] = k < K ? __ldg(a.betas + int64_t(grp) * K + k) : 0.0;
-      g[k] = 0.0;
-    }
+    for (int k = 0; k < KMAX; ++k) g[k] = 0.0;
     nll = 0.0;
   };
   // partial of group `grp` (this warp's share of segment seg0 + grp - g_first)
@@ -371,16 +382,26 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a
   load_beta(cur);
   int s = cw;
   uint32_t n = 0;
-  for (int64_t i = cw; i < n_mine; i += nact) {
-    const int64_t tile = t0 + i;
-    while (tile * kTileRows >= a.poff[cur + 1]) {
-      flush(cur);
-      load_beta(++cur);
-    }
+  int64_t next_start = a.poff[cur + 1], row_limit = a.poff[cur] + a.nrows[cur];
+  for (int64_t i = cw; i < n_units; i += nact) {
+    const int64_t tile0 = t0 + i * TPS;
+    const int nt = int(t1 - tile0 < TPS ? t1 - tile0 : TPS);
     mbar_wait(&sm.full[s], n & 1);
-    consume_tile_rows<KMAX, GRAD>(reinterpret_cast<const double*>(sm.xs + size_t(s) * tile_pitch),
-                                  sm.ys + size_t(s) * 32, K, lane, tile * kTileRows, a.poff[cur] + a.nrows[cur], b, g,
-                                  nll, &sm.empty[s]);
+    const double* xst = reinterpret_cast<const double*>(sm.xs + size_t(s) * stage_pitch);
+    const double* yst = sm.ys + size_t(s) * 32 * TPS;
+    double dep = 0.0;
+    for (int j = 0; j < nt; ++j) {
+      const int64_t row0 = (tile0 + j) * kTileRows;
+      while (row0 >= next_start) {
+        flush(cur);
+        load_beta(++cur);
+        next_start = a.poff[cur + 1];
+        row_limit = a.poff[cur] + a.nrows[cur];
+      }
+      consume_tile_rows<KMAX, GRAD>(xst + size_t(j) * kTileRows * K, yst + 32 * j, K, lane, row0, row_limit, b, g,
+                                    nll, dep);
+    }
+    mbar_arrive_after(&sm.empty[s], dep, lane, const_cast<double*>(xst));
     s += nact;
     if (s >= Se) {
       s = cw;
