@@ -23,11 +23,12 @@ PM_X_F64, PM_X_F32 = 0, 1
 PM_BOUNDARY_FREE, PM_BOUNDARY_PERIODIC = 0, 1
 PM_MODEL_ISING, PM_MODEL_POTTS4 = 0, 1
 PM_RNG_UNIFORMS, PM_RNG_NUMPY_PHILOX, PM_RNG_PHILOX4X32 = 0, 1, 2
-KIND_STREAM, KIND_WIDE = 1, 2
+KIND_STREAM, KIND_WIDE, KIND_ROWS = 1, 2, 3
 MAX_DELTAS = 16
 
 LIB_NAME = "libpmb200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# PM_LIB_PATH selects an A/B build variant of the same ABI (csrc/Makefile LIB=...)
+LIB_PATH = os.environ.get("PM_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 _dp = POINTER(c_double)
 _i64p = POINTER(c_int64)

@@ -27,7 +27,7 @@ constexpr int kHbRowsThreads = (kHbRowsNCW + 1) * 32;
 constexpr int kWideThreads = 256;
 constexpr int kMaxKC = 8;                    // stream kernel handles K <= 256
 
-enum KernelKind { KIND_NONE = 0, KIND_STREAM = 1, KIND_WIDE = 2 };
+enum KernelKind { KIND_NONE = 0, KIND_STREAM = 1, KIND_WIDE = 2, KIND_ROWS = 3 };
 
 int max_optin_smem(int device) {
   int v = 0;
@@ -79,7 +79,7 @@ struct pm_glm_s {
   double* beta_pinned = nullptr;
   // geometry
   int kind = KIND_NONE;
-  int grid = 0, threads = 0, stages = 0;
+  int grid = 0, threads = 0, stages = 0, tps = 1;
   size_t smem = 0;
   bool launched = false;
   int last_want_grad = 1;
@@ -155,11 +155,71 @@ cudaError_t launch_wide(const GlmArgs& a, int grid, int threads, size_t smem, cu
   return cudaGetLastError();
 }
 
+// ---- small-K row-per-lane kernel (fp64, even K <= 32) -----------------------------
+using RowsLaunch = cudaError_t (*)(const GlmArgs&, const double*, int, size_t, int, cudaStream_t);
+
+template <int KMAX, bool GRAD>
+cudaError_t launch_rows(const GlmArgs& a, const double* beta, int grid, size_t smem, int tps, cudaStream_t st) {
+  static std::atomic<uint64_t> attr{0};
+  auto kern = glm_rows_kernel<KMAX, GRAD, kNCW>;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), attr);
+  if (e != cudaSuccess) return e;
+  BetaPack<1> bp;
+  for (int k = 0; k < 32; ++k) bp.v[k] = (k < a.K) ? beta[k] : 0.0;
+  kern<<<grid, kStreamThreads, smem, st>>>(a, bp, tps);
+  return cudaGetLastError();
+}
+
+template <bool GRAD>
+RowsLaunch pick_rows(int K) {
+  switch (K) {  // exact even K: the row loops and the swizzle are compile-time
+    case 2: return launch_rows<2, GRAD>;
+    case 4: return launch_rows<4, GRAD>;
+    case 6: return launch_rows<6, GRAD>;
+    case 8: return launch_rows<8, GRAD>;
+    case 10: return launch_rows<10, GRAD>;
+    case 12: return launch_rows<12, GRAD>;
+    case 14: return launch_rows<14, GRAD>;
+    case 16: return launch_rows<16, GRAD>;
+    case 18: return launch_rows<18, GRAD>;
+    case 20: return launch_rows<20, GRAD>;
+    case 22: return launch_rows<22, GRAD>;
+    case 24: return launch_rows<24, GRAD>;
+    case 26: return launch_rows<26, GRAD>;
+    case 28: return launch_rows<28, GRAD>;
+    case 30: return launch_rows<30, GRAD>;
+    case 32: return launch_rows<32, GRAD>;
+  }
+  return nullptr;
+}
+
 int choose_geometry(pm_glm_s* h) {
   const int xs = (h->xtype == PM_X_F64) ? 8 : 4;
   const int kc = (h->K + 31) / 32;
   const int budget = std::min(max_optin_smem(h->device), 232448) - 1024;
   h->kind = KIND_NONE;
+  const char* env_rows = std::getenv("PM_GLM_ROWS");
+  // row-per-lane kernel: fp64, even K <= 30, and enough tiles to fill the machine (measured on
+  // B200, tools/ab_rows_k.py: 1.3-2x faster than the column kernel at N = 1e7 for K <= 30; at
+  // K = 32 and at N ~ 1e5 the column kernel is as fast or faster).  PM_GLM_ROWS=0/1 forces.
+  const bool rows_forced = env_rows && env_rows[0] == '1';
+  const bool rows_ok = h->xtype == PM_X_F64 && h->K % 2 == 0 && h->K <= 32;
+  if (rows_ok && !(env_rows && env_rows[0] == '0') &&
+      (rows_forced || (h->K <= 30 && h->n_tiles >= int64_t(32) * h->sms))) {
+    // two tiles per stage when 2 stages per consumer warp still fit, else one
+    int tps = stream_smem_bytes(h->K, 8, 2 * kNCW * 2, kNCW) <= size_t(budget) ? 2 : 1;
+    int S = 4 * kNCW;
+    while (S > kNCW && stream_smem_bytes(h->K, 8, S * tps, kNCW) > size_t(budget)) S -= kNCW;
+    if (stream_smem_bytes(h->K, 8, S * tps, kNCW) <= size_t(budget)) {
+      h->kind = KIND_ROWS;
+      h->stages = S;
+      h->tps = tps;
+      h->threads = kStreamThreads;
+      h->smem = stream_smem_bytes(h->K, 8, S * tps, kNCW);
+      h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, h->n_tiles));
+      return PM_OK;
+    }
+  }
   if (kc <= kMaxKC) {
     const size_t fixed = stream_smem_bytes(h->K, xs, 0, kNCW);
     const size_t per_stage = stream_smem_bytes(h->K, xs, 1, 0) - stream_smem_bytes(h->K, xs, 0, 0);
@@ -222,6 +282,9 @@ int enqueue_eval(pm_glm_s* h, const double* beta, bool with_prior, bool grad, do
   if (h->kind == KIND_STREAM) {
     StreamLaunch fn = pick_stream_any(h->xtype, (h->K + 31) / 32, grad);
     e = fn(a, beta, h->grid, h->smem, st);
+  } else if (h->kind == KIND_ROWS) {
+    RowsLaunch fn = grad ? pick_rows<true>(h->K) : pick_rows<false>(h->K);
+    e = fn(a, beta, h->grid, h->smem, h->tps, st);
   } else {
     std::memcpy(h->beta_pinned, beta, sizeof(double) * h->K);
     e = cudaMemcpyAsync(h->beta_dev, h->beta_pinned, sizeof(double) * h->K, cudaMemcpyHostToDevice, st);
@@ -788,14 +851,22 @@ HbLaunch pick_hb(int kc);
 
 template <bool GRAD>
 HbRowsLaunch pick_hb_rows(int K) {
-  switch ((K + 3) / 4 * 4) {
+  switch (K) {  // exact even K: the row loops and the swizzle are compile-time
+    case 2: return launch_hb_rows<2, GRAD>;
     case 4: return launch_hb_rows<4, GRAD>;
+    case 6: return launch_hb_rows<6, GRAD>;
     case 8: return launch_hb_rows<8, GRAD>;
+    case 10: return launch_hb_rows<10, GRAD>;
     case 12: return launch_hb_rows<12, GRAD>;
+    case 14: return launch_hb_rows<14, GRAD>;
     case 16: return launch_hb_rows<16, GRAD>;
+    case 18: return launch_hb_rows<18, GRAD>;
     case 20: return launch_hb_rows<20, GRAD>;
+    case 22: return launch_hb_rows<22, GRAD>;
     case 24: return launch_hb_rows<24, GRAD>;
+    case 26: return launch_hb_rows<26, GRAD>;
     case 28: return launch_hb_rows<28, GRAD>;
+    case 30: return launch_hb_rows<30, GRAD>;
     case 32: return launch_hb_rows<32, GRAD>;
   }
   return nullptr;

@@ -256,26 +256,37 @@ struct HbRowsArgs {
 // broadcast), so only x[] and g[] occupy registers and 15 consumer warps fit per SM.
 // `dep` accumulates a value computed from every shared load of the tile; the caller releases
 // the stage with mbar_arrive_after(dep) once all of the stage's tiles are consumed.
+//
+// Bank conflicts: lane l reads its row in 16-byte chunks; with Q = K/2 chunks per row, the
+// 8 lanes of a 128-byte wavefront start Q chunks apart.  When Q is a multiple of 8 (K = 16,
+// 32) they all hit the same bank group (8-way conflict; measured 2x slower), so those
+// shapes XOR-swizzle: register slot q holds chunk q ^ sw with sw = lane & 7 (a permutation
+// inside each aligned group of 8 chunks), and rows_unrotate() maps the gradient slots back.
+// Other even K keep static offsets (2- and 4-way conflicts measured harmless).
+// KMAX is the exact (even) K of the instantiation; the runtime K must equal it.
+template <int KMAX>
+struct RowsSwizzle {
+  static constexpr bool value = (KMAX / 2) % 8 == 0;
+};
+
 template <int KMAX, bool GRAD>
-__device__ __forceinline__ void consume_tile_rows(const double* xs, const double* ys, int K, int lane, int64_t row0,
-                                                  int64_t row_limit, const double* b, double (&g)[KMAX],
-                                                  double& nll_acc, double& dep) {
-  const double* xr = xs + lane * K;  // K even: 16-byte aligned rows
+__device__ __forceinline__ void consume_tile_rows(const double* xs, const double* ys, int K, int sw, int lane,
+                                                  int64_t row0, int64_t row_limit, const double* b,
+                                                  double (&g)[KMAX], double& nll_acc, double& dep) {
+  constexpr bool SW = RowsSwizzle<KMAX>::value;
+  const double2* xr = reinterpret_cast<const double2*>(xs + lane * KMAX);  // 16-byte aligned rows
+  const double2* b2 = reinterpret_cast<const double2*>(b);
   double x[KMAX];
   double t0 = 0.0, t1 = 0.0;
 #pragma unroll
-  for (int k = 0; k < KMAX; k += 2) {
-    if (k < K) {
-      const double2 v = *reinterpret_cast<const double2*>(xr + k);
-      const double2 bb = *reinterpret_cast<const double2*>(b + k);
-      x[k] = v.x;
-      x[k + 1] = v.y;
-      t0 = fma(x[k], bb.x, t0);
-      t1 = fma(x[k + 1], bb.y, t1);
-    } else {
-      x[k] = 0.0;
-      x[k + 1] = 0.0;
-    }
+  for (int q = 0; q < KMAX / 2; ++q) {
+    const int c = SW ? (q ^ sw) : q;
+    const double2 v = xr[c];
+    const double2 bb = b2[c];
+    x[2 * q] = v.x;
+    x[2 * q + 1] = v.y;
+    t0 = fma(v.x, bb.x, t0);
+    t1 = fma(v.y, bb.y, t1);
   }
   const double yv = ys[lane];
   dep += t0 + t1 + yv;  // t0, t1, yv consume every load of this tile
@@ -287,6 +298,33 @@ __device__ __forceinline__ void consume_tile_rows(const double* xs, const double
     w = valid ? w : 0.0;
 #pragma unroll
     for (int k = 0; k < KMAX; ++k) g[k] = fma(w, x[k], g[k]);
+  }
+}
+
+// Column totals of the swizzled per-lane gradient slots: column pair (2c, 2c+1) sits in slot
+// c ^ sw; a select over the 8 slots of c's group picks it, then the fixed butterfly sums the
+// lanes.  out(k, v) receives column k's warp total in every lane.
+template <int KMAX, class Out>
+__device__ __forceinline__ void rows_unrotate(const double (&g)[KMAX], int K, int sw, Out out) {
+  if constexpr (!RowsSwizzle<KMAX>::value) {
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) out(k, warp_sum(g[k]));
+  } else {
+#pragma unroll
+    for (int cc = 0; cc < KMAX / 2; ++cc) {
+      const int s = cc ^ sw;
+      double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int q = (cc & ~7) | j;
+        if (q == s) {
+          v0 = g[2 * q];
+          v1 = g[2 * q + 1];
+        }
+      }
+      out(2 * cc, warp_sum(v0));
+      out(2 * cc + 1, warp_sum(v1));
+    }
   }
 }
 
@@ -367,17 +405,15 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a
     nll = 0.0;
   };
   // partial of group `grp` (this warp's share of segment seg0 + grp - g_first)
+  const int q0 = RowsSwizzle<KMAX>::value ? (lane & 7) : 0;  // chunk swizzle (consume_tile_rows)
   auto flush = [&](int grp) {
     double* dst = a.part + (size_t(seg0 + grp - g_first) * NCW + cw) * (K + 1);
     const double ns = warp_sum(nll);
     if (lane == 0) dst[0] = ns;
-    if (GRAD) {
-#pragma unroll
-      for (int k = 0; k < KMAX; ++k) {
-        const double v = warp_sum(g[k]);
-        if (lane == 0 && k < K) dst[1 + k] = v;
-      }
-    }
+    if (GRAD)
+      rows_unrotate<KMAX>(g, K, q0, [&](int k, double v) {
+        if (lane == 0) dst[1 + k] = v;
+      });
   };
   load_beta(cur);
   int s = cw;
@@ -398,8 +434,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a
         next_start = a.poff[cur + 1];
         row_limit = a.poff[cur] + a.nrows[cur];
       }
-      consume_tile_rows<KMAX, GRAD>(xst + size_t(j) * kTileRows * K, yst + 32 * j, K, lane, row0, row_limit, b, g,
-                                    nll, dep);
+      consume_tile_rows<KMAX, GRAD>(xst + size_t(j) * kTileRows * K, yst + 32 * j, K, q0, lane, row0, row_limit, b,
+                                    g, nll, dep);
     }
     mbar_arrive_after(&sm.empty[s], dep, lane, const_cast<double*>(xst));
     s += nact;
@@ -413,6 +449,98 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a
     load_beta(++cur);
     flush(cur);
   }
+}
+
+// ---------------------------------------------------------------- K1 small-K row-per-lane variant
+// The flat evaluation (glm.py:367-372) for fp64 X with even K <= 32: each CTA streams an
+// equal contiguous range of the padded tiles, TPS tiles per stage, and every consumer lane
+// owns one row (consume_tile_rows; beta broadcast from shared memory).  Per-warp partials
+// go through the same deterministic CTA fold and last-CTA finish as glm_stream_kernel.
+template <int KMAX, bool GRAD, int NCW>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1) glm_rows_kernel(GlmArgs a, BetaPack<1> beta, int tps) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int K = a.K;
+  const int S = a.stages;
+  const int TPS = tps;
+  const StreamSmem sm = carve_stream_smem(smem_raw, K, sizeof(double), S * TPS, NCW);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  for (int k = threadIdx.x; k < K; k += blockDim.x) sm.sbeta[k] = beta.v[k];
+  __syncthreads();
+  const int64_t C = gridDim.x, c = blockIdx.x;
+  const int64_t t0 = c * a.n_tiles / C, t1 = (c + 1) * a.n_tiles / C;
+  const int64_t n_units = (t1 - t0 + TPS - 1) / TPS;
+  const uint32_t tile_bytes = uint32_t(kTileRows) * K * sizeof(double);
+  const size_t stage_pitch = size_t(tile_bytes) * TPS;
+  const int nact = S < NCW ? S : NCW;
+  const int Se = S - S % nact;
+  const double* X = static_cast<const double*>(a.X);
+  const int q0 = RowsSwizzle<KMAX>::value ? (lane & 7) : 0;  // chunk swizzle (consume_tile_rows)
+  double g[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) g[k] = 0.0;
+  double nll = 0.0;
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_first();
+      int s = 0;
+      uint32_t n = 0;
+      for (int64_t i = 0; i < n_units; ++i) {
+        if (n > 0) mbar_wait(&sm.empty[s], (n - 1) & 1);
+        const int64_t tile = t0 + i * TPS;
+        const uint32_t nt = uint32_t(t1 - tile < TPS ? t1 - tile : TPS);
+        mbar_arrive_expect_tx(&sm.full[s], nt * (tile_bytes + 32 * sizeof(double)));
+        if (a.evict_first)
+          bulk_g2s_hint(sm.xs + size_t(s) * stage_pitch, X + tile * int64_t(kTileRows) * K, nt * tile_bytes,
+                        &sm.full[s], pol);
+        else
+          bulk_g2s(sm.xs + size_t(s) * stage_pitch, X + tile * int64_t(kTileRows) * K, nt * tile_bytes, &sm.full[s]);
+        bulk_g2s(sm.ys + size_t(s) * 32 * TPS, a.y + tile * kTileRows, nt * 32 * sizeof(double), &sm.full[s]);
+        if (++s == Se) {
+          s = 0;
+          ++n;
+        }
+      }
+    }
+  } else if (warp - 1 < nact) {
+    const int cw = warp - 1;
+    int s = cw;
+    uint32_t n = 0;
+    for (int64_t i = cw; i < n_units; i += nact) {
+      const int64_t tile0 = t0 + i * TPS;
+      const int nt = int(t1 - tile0 < TPS ? t1 - tile0 : TPS);
+      mbar_wait(&sm.full[s], n & 1);
+      const double* xst = reinterpret_cast<const double*>(sm.xs + size_t(s) * stage_pitch);
+      const double* yst = sm.ys + size_t(s) * 32 * TPS;
+      double dep = 0.0;
+      for (int j = 0; j < nt; ++j)
+        consume_tile_rows<KMAX, GRAD>(xst + size_t(j) * kTileRows * K, yst + 32 * j, K, q0, lane,
+                                      (tile0 + j) * kTileRows, a.n_rows, sm.sbeta, g, nll, dep);
+      mbar_arrive_after(&sm.empty[s], dep, lane, const_cast<double*>(xst));
+      s += nact;
+      if (s >= Se) {
+        s = cw;
+        ++n;
+      }
+    }
+  }
+  if (warp > 0) {  // every consumer warp (idle ones write zeros): fixed-order butterflies
+    const int cw = warp - 1;
+    const double ws = warp_sum(nll);
+    if (lane == 0) sm.wf[cw] = -ws;
+    if (GRAD)
+      rows_unrotate<KMAX>(g, K, q0, [&](int k, double v) {
+        if (lane == 0) sm.wg[size_t(cw) * K + k] = v;
+      });
+  }
+  cta_reduce_finalize(a, sm, NCW, GRAD);
 }
 
 // Per group: fold the partials of its segments (gseg[g] .. gseg[g+1]-1) and warps in order.

@@ -114,6 +114,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 // try_wait with a suspend-time hint: the thread sleeps in hardware until the phase
 // completes (or ~the hint elapses) instead of re-polling (each poll costs issue slots).
+#ifndef PM_MBAR_HINT_NS
+#define PM_MBAR_HINT_NS 1000000
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -121,7 +124,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(uint32_t(PM_MBAR_HINT_NS))
       : "memory");
   return ok != 0;
 }

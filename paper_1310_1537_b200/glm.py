@@ -113,7 +113,7 @@ class GlmDevice:
         _lib.call("pm_glm_geometry", self._h, ctypes.byref(g), ctypes.byref(t), ctypes.byref(s),
                   ctypes.byref(sm), ctypes.byref(k))
         return {"grid": g.value, "threads": t.value, "stages": s.value, "smem_bytes": sm.value,
-                "kernel": {1: "stream", 2: "wide"}.get(k.value, "none")}
+                "kernel": {1: "stream", 2: "wide", 3: "rows"}.get(k.value, "none")}
 
     def stream(self) -> int:
         p = ctypes.c_void_p()

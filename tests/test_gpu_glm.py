@@ -194,3 +194,29 @@ def test_config1_full_size_properties(gpu):
     b = glm.loglike_grad(DesignMatrix(x[half:], y[half:]), beta)
     assert rel(r.f, a.f + b.f) < TOL and grel(r.g, a.g + b.g) < TOL
     assert abs(r.f) > 0 and np.all(np.isfinite(r.g))
+
+
+@pytest.mark.parametrize("k", [2, 4, 6, 20, 22, 30, 32])
+@pytest.mark.parametrize("n", [1, 33, 64, 1000, 250_007])
+def test_row_per_lane_kernel_against_oracle_and_stream_kernel(gpu, n, k, monkeypatch):
+    # fp64 with even K <= 32 runs the row-per-lane kernel (KIND_ROWS): equal contiguous tile
+    # ranges per CTA, two tiles per stage; compare with the oracle and the column kernel
+    monkeypatch.setenv("PM_GLM_ROWS", "1")  # forced: the default picks it only for K <= 30 at large N
+    gen = np.random.default_rng(n + k)
+    x = gen.standard_normal((n, k))
+    y = (gen.random(n) < 0.4).astype(float)
+    beta = gen.normal(0, 0.3, k)
+    prior = GaussianPrior(gen.normal(0, 0.5, k), np.full(k, 2.0))
+    d = DesignMatrix(x, y)
+    r = glm.log_posterior_grad(d, beta, prior)
+    assert d.on_device(0).geometry()["kernel"] == "rows"
+    f_ref, g_ref = gl.log_posterior_grad(x, y, beta, prior.mu, prior.sigma)
+    assert rel(r.f, f_ref) < TOL and grel(r.g, g_ref) < TOL
+    assert glm.loglike(d, beta) == glm.loglike_grad(d, beta).f
+    again = glm.log_posterior_grad(d, beta, prior)
+    assert again.f == r.f and np.array_equal(again.g, r.g)
+    monkeypatch.setenv("PM_GLM_ROWS", "0")
+    d2 = DesignMatrix(x, y)
+    r2 = glm.log_posterior_grad(d2, beta, prior)
+    assert d2.on_device(0).geometry()["kernel"] == "stream"
+    assert rel(r.f, r2.f) < TOL and grel(r.g, r2.g) < TOL
