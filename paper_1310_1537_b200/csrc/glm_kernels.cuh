@@ -335,7 +335,8 @@ __device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& s
 }
 
 // K1 + K2: persistent fused single-pass kernel, one CTA per SM.
-template <typename XT, int KC, bool GRAD, int NCW>
+// R: rows per register sub-tile (SubRows default; smaller R frees registers for more warps)
+template <typename XT, int KC, bool GRAD, int NCW, int R = SubRows<KC, GRAD>::value>
 __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     glm_stream_kernel(GlmArgs a, BetaPack<KC> beta) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -362,8 +363,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     g[j] = 0.0;
   }
   double nll = 0.0;
-  stream_tiles<XT, KC, GRAD, NCW>(static_cast<const XT*>(a.X), a.y, K, blockIdx.x, a.n_tiles, gridDim.x,
-                                  a.n_rows, S, sm, breg, g, nll, a.evict_first != 0);
+  stream_tiles<XT, KC, GRAD, NCW, R>(static_cast<const XT*>(a.X), a.y, K, blockIdx.x, a.n_tiles, gridDim.x,
+                                     a.n_rows, S, sm, breg, g, nll, a.evict_first != 0);
   if (warp > 0) {
     const int cw = warp - 1;
     const double wsum = warp_sum(nll);
