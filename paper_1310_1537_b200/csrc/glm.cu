@@ -182,18 +182,29 @@ cudaError_t launch_wide(const GlmArgs& a, int grid, int threads, size_t smem, cu
 }
 
 // ---- small-K row-per-lane kernel (fp64, even K <= 32) -----------------------------
-using RowsLaunch = cudaError_t (*)(const GlmArgs&, const double*, int, size_t, int, cudaStream_t);
+using RowsLaunch = cudaError_t (*)(const GlmArgs&, const double*, int, size_t, int, int, cudaStream_t);
 
-template <int KMAX, bool GRAD>
-cudaError_t launch_rows(const GlmArgs& a, const double* beta, int grid, size_t smem, int tps, cudaStream_t st) {
+template <int KMAX, bool GRAD, int NCW>
+cudaError_t launch_rows_n(const GlmArgs& a, const double* beta, int grid, size_t smem, int tps, cudaStream_t st) {
   static std::atomic<uint64_t> attr{0};
-  auto kern = glm_rows_kernel<KMAX, GRAD, kNCW>;
+  auto kern = glm_rows_kernel<KMAX, GRAD, NCW>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), attr);
   if (e != cudaSuccess) return e;
   BetaPack<1> bp;
   for (int k = 0; k < 32; ++k) bp.v[k] = (k < a.K) ? beta[k] : 0.0;
-  kern<<<grid, kStreamThreads, smem, st>>>(a, bp, tps);
+  kern<<<grid, (NCW + 1) * 32, smem, st>>>(a, bp, tps);
   return cudaGetLastError();
+}
+
+// ncw = consumer warps: 15 (512 threads, <= 128 registers) for K <= 16, where the per-row
+// transcendental chain rather than HBM bounds the kernel, else 7
+template <int KMAX, bool GRAD>
+cudaError_t launch_rows(const GlmArgs& a, const double* beta, int grid, size_t smem, int tps, int ncw,
+                        cudaStream_t st) {
+  if constexpr (KMAX <= 16) {
+    if (ncw == 15) return launch_rows_n<KMAX, GRAD, 15>(a, beta, grid, smem, tps, st);
+  }
+  return launch_rows_n<KMAX, GRAD, kNCW>(a, beta, grid, smem, tps, st);
 }
 
 template <bool GRAD>
@@ -232,16 +243,32 @@ int choose_geometry(pm_glm_s* h) {
   const bool rows_ok = h->xtype == PM_X_F64 && h->K % 2 == 0 && h->K <= 32;
   if (rows_ok && !(env_rows && env_rows[0] == '0') &&
       (rows_forced || (h->K <= 30 && h->n_tiles >= int64_t(32) * h->sms))) {
-    // two tiles per stage when 2 stages per consumer warp still fit, else one
-    int tps = stream_smem_bytes(h->K, 8, 2 * kNCW * 2, kNCW) <= size_t(budget) ? 2 : 1;
-    int S = 4 * kNCW;
-    while (S > kNCW && stream_smem_bytes(h->K, 8, S * tps, kNCW) > size_t(budget)) S -= kNCW;
-    if (stream_smem_bytes(h->K, 8, S * tps, kNCW) <= size_t(budget)) {
+    // 7 consumer warps (15 measured slower at every K); stages of ~8 KB (TPS tiles per bulk
+    // copy: the single producer thread's per-copy cost bounds small-K shapes otherwise)
+    const char* e_ncw = std::getenv("PM_ROWS_NCW");
+    const int ncw = (e_ncw && std::atoi(e_ncw) == 15 && h->K <= 16) ? 15 : kNCW;
+    // measured (tools/ab_rows_tps.py, profiles/r01_ab_rows_tps.txt): 1 tile per copy halves
+    // the throughput; >= 4 tiles reach the HBM bound for K >= 12.  Prefer 2 stages per warp
+    // with >= 4 tiles each, else 1 stage per warp with as many tiles (<= 16) as fit.
+    const char* e_tps = std::getenv("PM_ROWS_TPS");
+    auto fits = [&](int stages, int t) { return stream_smem_bytes(h->K, 8, stages * t, ncw) <= size_t(budget); };
+    int tps = 16;
+    while (tps > 1 && !fits(2 * ncw, tps)) --tps;
+    if (tps < 4) {
+      tps = 16;
+      while (tps > 1 && !fits(ncw, tps)) --tps;
+    }
+    if (e_tps) tps = std::max(1, std::min(16, std::atoi(e_tps)));
+    while (tps > 1 && !fits(ncw, tps)) --tps;
+    int S = 4 * ncw;
+    while (S > ncw && stream_smem_bytes(h->K, 8, S * tps, ncw) > size_t(budget)) S -= ncw;
+    if (stream_smem_bytes(h->K, 8, S * tps, ncw) <= size_t(budget)) {
       h->kind = KIND_ROWS;
       h->stages = S;
       h->tps = tps;
-      h->threads = kStreamThreads;
-      h->smem = stream_smem_bytes(h->K, 8, S * tps, kNCW);
+      h->ncw = ncw;
+      h->threads = (ncw + 1) * 32;
+      h->smem = stream_smem_bytes(h->K, 8, S * tps, ncw);
       h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, h->n_tiles));
       return PM_OK;
     }
@@ -325,7 +352,7 @@ int enqueue_eval(pm_glm_s* h, const double* beta, bool with_prior, bool grad, do
     e = fn(a, beta, h->grid, h->smem, st);
   } else if (h->kind == KIND_ROWS) {
     RowsLaunch fn = grad ? pick_rows<true>(h->K) : pick_rows<false>(h->K);
-    e = fn(a, beta, h->grid, h->smem, h->tps, st);
+    e = fn(a, beta, h->grid, h->smem, h->tps, h->ncw, st);
   } else {
     std::memcpy(h->beta_pinned, beta, sizeof(double) * h->K);
     e = cudaMemcpyAsync(h->beta_dev, h->beta_pinned, sizeof(double) * h->K, cudaMemcpyHostToDevice, st);
