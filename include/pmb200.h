@@ -99,9 +99,14 @@ PM_API int pm_glm_wait(pm_glm_t h, double* f_out, double* g_out);
 
 /* Device-output form for collectives: writes (f, g[K]) as K+1 doubles to the device
  * buffer dev_out on `stream` (a cudaStream_t, NULL = the handle's own stream) without
- * synchronising; the caller reduces the partials across ranks (NCCL) and adds the prior. */
-PM_API int pm_glm_eval_device(pm_glm_t h, const double* beta, int want_grad, double* dev_out,
+ * synchronising; the caller reduces the partials across ranks (NCCL).  with_prior adds the
+ * handle's prior terms in the kernel (exactly one rank does, so the fold holds it once). */
+PM_API int pm_glm_eval_device(pm_glm_t h, const double* beta, int with_prior, int want_grad, double* dev_out,
                        void* stream);
+/* out[c] = in[0][c] + in[1][c] + ... + in[world-1][c] in ascending row order (the reference's
+ * ascending-worker merge, glm.py:243-250), c < width; device pointers, one launch on `stream`
+ * (NULL = the legacy default stream).  Bitwise identical on every rank given the same input. */
+PM_API int pm_fold_rows(const double* in_dev, int32_t world, int32_t width, double* out_dev, void* stream);
 
 /* Benchmark helper: n back-to-back launches (beta row i of betas[n][K]) bracketed by CUDA
  * events on the handle's stream; *total_ms = elapsed device time. */

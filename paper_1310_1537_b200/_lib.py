@@ -50,7 +50,8 @@ SIGNATURES = {
     "pm_glm_eval": (c_int, [c_void_p, _dp, c_int, c_int, _dp, _dp]),
     "pm_glm_launch": (c_int, [c_void_p, _dp, c_int, c_int]),
     "pm_glm_wait": (c_int, [c_void_p, _dp, _dp]),
-    "pm_glm_eval_device": (c_int, [c_void_p, _dp, c_int, c_void_p, c_void_p]),
+    "pm_glm_eval_device": (c_int, [c_void_p, _dp, c_int, c_int, c_void_p, c_void_p]),
+    "pm_fold_rows": (c_int, [c_void_p, c_int32, c_int32, c_void_p, c_void_p]),
     "pm_glm_time_launches": (c_int, [c_void_p, _dp, c_int32, c_int, c_int, POINTER(ctypes.c_float)]),
     "pm_glm_stream": (c_int, [c_void_p, POINTER(c_void_p)]),
     "pm_glm_geometry": (c_int, [c_void_p, _ip, _ip, _ip, POINTER(c_size_t), _ip]),

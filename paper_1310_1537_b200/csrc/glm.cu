@@ -530,25 +530,51 @@ int pm_glm_eval(pm_glm_t h, const double* beta, int with_prior, int want_grad, d
   return pm_glm_wait(h, f_out, g_out);
 }
 
-int pm_glm_eval_device(pm_glm_t h, const double* beta, int want_grad, double* dev_out, void* stream) {
+int pm_glm_eval_device(pm_glm_t h, const double* beta, int with_prior, int want_grad, double* dev_out,
+                       void* stream) {
   if (!h) return fail(PM_EINVAL, "null handle");
   if (!dev_out) return fail(PM_EINVAL, "dev_out is null");
   std::lock_guard<std::mutex> lk(h->mu);
   if (h->K == 0) return fail(PM_ESTATE, "no data uploaded");
   int rc = check_beta(h, beta);
   if (rc) return rc;
+  if (with_prior && !h->has_prior) return fail(PM_ESTATE, "no prior set (pm_glm_set_prior)");
   DeviceGuard g(h->device);
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
   if (st != h->stream) {  // order against earlier work on the handle (shared scratch)
     PM_CUDA(cudaEventRecord(h->ev_a, h->stream));
     PM_CUDA(cudaStreamWaitEvent(st, h->ev_a, 0));
   }
-  rc = enqueue_eval(h, beta, false, want_grad != 0, dev_out, st);
+  rc = enqueue_eval(h, beta, with_prior != 0, want_grad != 0, dev_out, st);
   if (rc) return rc;
   if (st != h->stream) {
     PM_CUDA(cudaEventRecord(h->ev_b, st));
     PM_CUDA(cudaStreamWaitEvent(h->stream, h->ev_b, 0));
   }
+  return PM_OK;
+}
+
+}  // extern "C"
+
+namespace {
+__global__ void fold_rows_kernel(const double* __restrict__ in, int world, int width, double* __restrict__ out) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < width; c += gridDim.x * blockDim.x) {
+    double acc = in[c];
+    for (int r = 1; r < world; ++r) acc += in[size_t(r) * width + c];
+    out[c] = acc;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int pm_fold_rows(const double* in_dev, int32_t world, int32_t width, double* out_dev, void* stream) {
+  if (!in_dev || !out_dev) return fail(PM_EINVAL, "null argument");
+  if (world < 1 || width < 1) return fail(PM_EINVAL, "need world >= 1 and width >= 1");
+  const int threads = 128;
+  const int blocks = std::min(1024, (width + threads - 1) / threads);
+  fold_rows_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(in_dev, world, width, out_dev);
+  PM_CUDA(cudaGetLastError());
   return PM_OK;
 }
 

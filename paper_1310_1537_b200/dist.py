@@ -16,6 +16,8 @@ with the gloo backend on CPU tensors in tests/test_dist_gloo.py.
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
 from .glm import DesignMatrix, GradResult, _check_beta
@@ -39,60 +41,57 @@ def ordered_sum(gathered):
 
 
 def gather_partials(part, group=None):
-    """All-gather every rank's (K+1) partial and fold them in rank order."""
+    """All-gather every rank's (K+1) partial and fold them in rank order.
+
+    NCCL: one all_gather_into_tensor + one fold launch (pm_fold_rows) on the current
+    stream; gloo (CPU tensors, the tests): the same ascending-rank fold in torch.
+    """
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
     if dist.get_backend(group) == "nccl":
         out = torch.empty((world,) + tuple(part.shape), dtype=part.dtype, device=part.device)
         dist.all_gather_into_tensor(out, part.contiguous(), group=group)
-    else:
-        parts = [torch.empty_like(part) for _ in range(world)]
-        dist.all_gather(parts, part.contiguous(), group=group)
-        out = torch.stack(parts)
-    return ordered_sum(out)
-
-
-def prior_terms_torch(beta_t, mu_t, sigma_t):
-    z = (beta_t - mu_t) / sigma_t
-    f = -0.5 * (z * z)
-    # ascending-k sequential sum, like the device finaliser (glm_kernels.cuh)
-    fsum = f[0].clone()
-    for k in range(1, f.shape[0]):
-        fsum += f[k]
-    return fsum, -(beta_t - mu_t) / (sigma_t * sigma_t)
+        from . import _lib
+        tot = torch.empty_like(part)
+        stream = torch.cuda.current_stream(part.device).cuda_stream
+        _lib.call("pm_fold_rows", ctypes.c_void_p(out.data_ptr()), world, part.numel(),
+                  ctypes.c_void_p(tot.data_ptr()), ctypes.c_void_p(stream or None))
+        return tot
+    parts = [torch.empty_like(part) for _ in range(world)]
+    dist.all_gather(parts, part.contiguous(), group=group)
+    return ordered_sum(torch.stack(parts))
 
 
 class DistributedDesign:
-    """This rank's row shard on its GPU, evaluated with one NCCL exchange per call."""
+    """This rank's row shard on its GPU: one kernel, one NCCL all-gather and one fold launch
+    per evaluation.  Rank 0's kernel adds the prior terms (the same device finaliser as the
+    single-GPU path), so the rank-ordered fold holds them exactly once."""
 
     def __init__(self, local: DesignMatrix, device: int, x_storage: str = "f64", group=None):
         import torch
+        import torch.distributed as dist
         self.local = local
         self.device = device
         self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.dev = local.on_device(device, x_storage)
         self.k = local.n_cols
         self._buf = torch.empty(self.k + 1, dtype=torch.float64, device=f"cuda:{device}")
 
-    def _partial(self, beta: np.ndarray):
+    def _partial(self, beta: np.ndarray, prior=None):
         import torch
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        self.dev.eval_device(beta, True, self._buf.data_ptr(), stream)
+        with_prior = prior is not None and self.rank == 0
+        if with_prior:
+            self.dev.set_prior(prior.mu, prior.sigma)
+        self.dev.eval_device(beta, True, self._buf.data_ptr(), stream, with_prior=with_prior)
         return self._buf
 
     def log_posterior_grad_device(self, beta, prior=None):
         """(f, g) as a device tensor of K+1 doubles, identical on every rank."""
-        import torch
         beta = _check_beta(beta, self.k)
-        tot = gather_partials(self._partial(beta), self.group)
-        if prior is not None:
-            dev = tot.device
-            bt = torch.from_numpy(beta).to(dev, non_blocking=True)
-            pf, pg = prior_terms_torch(bt, torch.from_numpy(prior.mu).to(dev), torch.from_numpy(prior.sigma).to(dev))
-            tot[0] += pf
-            tot[1:] += pg
-        return tot
+        return gather_partials(self._partial(beta, prior), self.group)
 
     def log_posterior_grad(self, beta, prior=None) -> GradResult:
         out = self.log_posterior_grad_device(beta, prior).cpu().numpy()

@@ -156,8 +156,10 @@ class GlmDevice:
             self.launch(beta, with_prior, want_grad)
             return self.wait(want_grad)
 
-    def eval_device(self, beta: np.ndarray, want_grad: bool, dev_out_ptr: int, stream: int = 0) -> None:
-        _lib.call("pm_glm_eval_device", self._h, _lib.dptr(beta), int(want_grad),
+    def eval_device(self, beta: np.ndarray, want_grad: bool, dev_out_ptr: int, stream: int = 0,
+                    with_prior: bool = False) -> None:
+        """(f, g) as K+1 doubles into device memory on `stream`, no synchronisation."""
+        _lib.call("pm_glm_eval_device", self._h, _lib.dptr(beta), int(with_prior), int(want_grad),
                   ctypes.c_void_p(dev_out_ptr), ctypes.c_void_p(stream or None))
 
     def close(self) -> None:

@@ -6,7 +6,7 @@ rm -f gpurun_out/rc.txt
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/smi.txt 2>&1
 if [ "${TESTS:-1}" = "1" ]; then
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/rc.txt
-  for t in test_gpu_glm test_gpu_diff test_gpu_ising test_gpu_hb test_gpu_denoise test_gpu_rng test_gpu_hb_sweep test_cli; do
+  for t in test_gpu_glm test_gpu_diff test_gpu_ising test_gpu_hb test_gpu_denoise test_gpu_rng test_gpu_hb_sweep test_gpu_dist test_cli; do
     timeout 900 python -m pytest tests/$t.py -m gpu -q > gpurun_out/$t.log 2>&1; echo "$t rc=$?" >> gpurun_out/rc.txt
   done
 fi
