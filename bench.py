@@ -342,7 +342,19 @@ def run_glm(args, cfg):
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if ws > 1:
+    # the rank path (DistributedDesign: NCCL all-gather + ordered fold) runs for N > 1, and at
+    # N = 1 with --force-dist (a 1-rank NCCL group) so the multi-GPU code is exercised on one GPU
+    dist_mode = ws > 1 or args.force_dist
+    if dist_mode:
+        if ws == 1:
+            import socket
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            if "MASTER_PORT" not in os.environ:
+                with socket.socket() as s:
+                    s.bind(("127.0.0.1", 0))
+                    os.environ["MASTER_PORT"] = str(s.getsockname()[1])
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n_full, k = cfg["n"], cfg["k"]
     a, b = partition(n_full, ws)[rank]
@@ -359,7 +371,8 @@ def run_glm(args, cfg):
     dev = data.on_device(local, cfg["x_storage"])
     geo = dev.geometry()
 
-    if ws > 1:
+    dev.set_prior(prior.mu, prior.sigma)  # every rank: the kernel-only timing below adds it
+    if dist_mode:
         from paper_1310_1537_b200.dist import DistributedDesign
         dd = DistributedDesign(data, device=local, x_storage=cfg["x_storage"])
 
@@ -369,8 +382,6 @@ def run_glm(args, cfg):
         def step_e2e(beta):
             return dd.log_posterior_grad(beta, prior)
     else:
-        dev.set_prior(prior.mu, prior.sigma)
-
         def step_dev(beta):
             dev.launch(beta, True, True)
 
@@ -378,7 +389,7 @@ def run_glm(args, cfg):
             return pglm.log_posterior_grad(data, beta, prior, plan)
 
     def barrier():
-        if ws > 1:
+        if dist_mode:
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize(local)
 
@@ -401,24 +412,36 @@ def run_glm(args, cfg):
         scrub.zero_()                                  # 512 MiB write evicts X and y from L2
         torch.cuda.synchronize(local)
 
-    if ws == 1 and flush_l2:
+    if not dist_mode and flush_l2:
         # one launch at a time, L2 flushed before each, CUDA events around the launch only
         dev_ms = 0.0
         for i in range(steps):
             flush()
             dev_ms += dev.time_launches(block[i:i + 1], with_prior=True, want_grad=True)
-    elif ws == 1:
+    elif not dist_mode:
         # K launches bracketed by CUDA events on the launching (handle) stream
         dev_ms = dev.time_launches(block, with_prior=True, want_grad=True)
     else:
+        # rank steps (kernel + all-gather + fold) on torch's stream, events on that stream
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         tstream = torch.cuda.current_stream(local)
-        ev0.record(tstream)
-        for i in range(steps):
-            step_dev(block[i])
-        ev1.record(tstream)
-        torch.cuda.synchronize(local)
-        dev_ms = ev0.elapsed_time(ev1)
+        if flush_l2:
+            dev_ms = 0.0
+            for i in range(steps):
+                flush()
+                dist.barrier(device_ids=[local])
+                ev0.record(tstream)
+                step_dev(block[i])
+                ev1.record(tstream)
+                torch.cuda.synchronize(local)
+                dev_ms += ev0.elapsed_time(ev1)
+        else:
+            ev0.record(tstream)
+            for i in range(steps):
+                step_dev(block[i])
+            ev1.record(tstream)
+            torch.cuda.synchronize(local)
+            dev_ms = ev0.elapsed_time(ev1)
     barrier()
     clk = clocks.stop()
 
@@ -444,7 +467,7 @@ def run_glm(args, cfg):
 
     # max over ranks
     t = torch.tensor([dev_ms, e2e_s, kern_ms], dtype=torch.float64, device=f"cuda:{local}")
-    if ws > 1:
+    if dist_mode:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dev_ms, e2e_s, kern_ms = (float(v) for v in t.cpu())
 
@@ -478,15 +501,19 @@ def run_glm(args, cfg):
                                    f"threads, {geo['stages']} TMA stages, {geo['smem_bytes']} B smem)"},
             "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": 8 * k,
                     "d2h_bytes_per_step": 8 * (k + 1),
-                    "path": "paper_1310_1537_b200.glm.log_posterior_grad (C-ABI pm_glm_launch/wait; beta in "
-                            "kernel params, (f,g) written to mapped pinned host memory)"},
-            "gpu_launches": steps,
+                    "path": ("paper_1310_1537_b200.dist.DistributedDesign.log_posterior_grad (per rank: kernel, "
+                             "NCCL all-gather of the (K+1) partials, ordered fold, (f,g) to host)" if dist_mode else
+                             "paper_1310_1537_b200.glm.log_posterior_grad (C-ABI pm_glm_launch/wait; beta in "
+                             "kernel params, (f,g) written to mapped pinned host memory)")},
+            "gpu_launches": steps * (2 if dist_mode else 1),   # + the fold launch per step (NCCL not counted)
             "clocks": clk,
         }
+        if dist_mode:
+            line["config"]["collective"] = "NCCL all_gather_into_tensor of K+1 doubles + pm_fold_rows per step"
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(cfg, n_full)
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if dist_mode:
         dist.destroy_process_group()
 
 
@@ -832,6 +859,8 @@ def main():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--config", default="c1", choices=sorted(CONFIGS))
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--force-dist", action="store_true",
+                   help="GLM configs: use the per-rank NCCL path even at N=1 (a 1-rank group)")
     # internal: CPU baseline subprocess
     p.add_argument("--cpu-worker", action="store_true", help=argparse.SUPPRESS)
     p.add_argument("--sample-rows", type=int, default=0, help=argparse.SUPPRESS)

@@ -40,6 +40,14 @@ def ordered_sum(gathered):
     return acc
 
 
+def torch_stream_handle(device) -> int:
+    """cudaStream_t of torch's current stream on `device` for the C ABI.  torch reports the
+    legacy default stream as 0, which the ABI reads as "the handle's own stream"; pass
+    cudaStreamLegacy (0x1) instead so the launch really lands on torch's stream."""
+    import torch
+    return torch.cuda.current_stream(device).cuda_stream or 1
+
+
 def gather_partials(part, group=None):
     """All-gather every rank's (K+1) partial and fold them in rank order.
 
@@ -54,9 +62,8 @@ def gather_partials(part, group=None):
         dist.all_gather_into_tensor(out, part.contiguous(), group=group)
         from . import _lib
         tot = torch.empty_like(part)
-        stream = torch.cuda.current_stream(part.device).cuda_stream
         _lib.call("pm_fold_rows", ctypes.c_void_p(out.data_ptr()), world, part.numel(),
-                  ctypes.c_void_p(tot.data_ptr()), ctypes.c_void_p(stream or None))
+                  ctypes.c_void_p(tot.data_ptr()), ctypes.c_void_p(torch_stream_handle(part.device)))
         return tot
     parts = [torch.empty_like(part) for _ in range(world)]
     dist.all_gather(parts, part.contiguous(), group=group)
@@ -80,8 +87,7 @@ class DistributedDesign:
         self._buf = torch.empty(self.k + 1, dtype=torch.float64, device=f"cuda:{device}")
 
     def _partial(self, beta: np.ndarray, prior=None):
-        import torch
-        stream = torch.cuda.current_stream(self.device).cuda_stream
+        stream = torch_stream_handle(self.device)
         with_prior = prior is not None and self.rank == 0
         if with_prior:
             self.dev.set_prior(prior.mu, prior.sigma)
@@ -168,6 +174,8 @@ class LatticeStrip:
         self._lib.call("pm_lat_set_spins", self._h, self._lib.i8ptr(s))
 
     def get_spins(self) -> np.ndarray:
+        import torch
+        torch.cuda.synchronize(self.device)  # half-sweeps and exchanges run on torch's stream
         out = np.empty((self.rows, self.width), dtype=np.int8)
         self._lib.call("pm_lat_get_spins", self._h, self._lib.i8ptr(out))
         return out
@@ -189,8 +197,7 @@ class LatticeStrip:
     def half_sweep(self, colour: int, seed: int, sweep: int) -> None:
         import ctypes
 
-        import torch
-        stream = torch.cuda.current_stream(self.device).cuda_stream
+        stream = torch_stream_handle(self.device)
         self._lib.call("pm_lat_strip_half_sweep", self._h, int(colour), ctypes.c_uint64(seed),
                        ctypes.c_uint64(sweep), ctypes.c_void_p(stream))
 

@@ -62,3 +62,44 @@ def test_nccl_single_rank_matches_single_gpu_path(gpu):
         assert torch.equal(out, ref)
     finally:
         dist.destroy_process_group()
+
+
+def test_nccl_single_rank_back_to_back_and_strip(gpu):
+    # many evaluations queued back to back on torch's (legacy default) stream must each see
+    # their own kernel's partial: the C ABI gets cudaStreamLegacy, not NULL (= handle stream)
+    import torch
+    import torch.distributed as dist
+    from paper_1310_1537_b200.dist import DistributedDesign, LatticeStrip, strip_sweeps
+    from paper_1310_1537_b200.ising import IsingLattice, color_lattice, gibbs_sweeps
+    from paper_1310_1537_b200.rng import SitePhilox
+    from paper_1310_1537_b200.synthetic import ising_spins
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(free_port())
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        gen = np.random.default_rng(5)
+        n, k = 2_000_000, 100
+        x = gen.standard_normal((n, k))
+        y = (gen.random(n) < 0.5).astype(float)
+        d = DesignMatrix(x, y)
+        dd = DistributedDesign(d, device=0)
+        prior = GaussianPrior.isotropic(k, 0.0, 10.0)
+        betas = gen.normal(0, 0.1, (12, k))
+        outs = [dd.log_posterior_grad_device(b, prior) for b in betas]   # queued, no host sync
+        torch.cuda.synchronize()
+        for b, o in zip(betas, outs):
+            single = glm.log_posterior_grad(d, b, prior)
+            o = o.cpu().numpy()
+            assert o[0] == single.f and np.array_equal(o[1:], single.g)
+        # a 1-rank strip: half-sweeps and the wrap-around halo copies on torch's stream
+        s0 = ising_spins(64, 128, seed=3)
+        strip = LatticeStrip(64, 128, 0, 64, 0, model="ising", w=0.6)
+        strip.set_spins(s0)
+        strip_sweeps(strip, 25, 77, 0, 0, 1)
+        lat = IsingLattice(s0, np.zeros(s0.shape), 0.6, boundary="periodic")
+        gibbs_sweeps(lat, color_lattice(lat), SitePhilox(77), 25)
+        np.testing.assert_array_equal(strip.get_spins(), lat.s)
+        strip.close()
+    finally:
+        dist.destroy_process_group()
