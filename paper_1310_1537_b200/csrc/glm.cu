@@ -77,6 +77,7 @@ struct pm_glm_s {
   double* out_dev = nullptr;    // device alias of out_host
   double* beta_dev = nullptr;   // [K] (wide kernel)
   double* beta_pinned = nullptr;
+  double* xt_cache = nullptr;   // [K][n_pad] transposed X, shared by the workspaces
   // geometry
   int kind = KIND_NONE;
   int grid = 0, threads = 0, stages = 0, tps = 1, ncw = 7;
@@ -96,6 +97,8 @@ void free_glm_data(pm_glm_s* h) {
   if (h->beta_pinned) cudaFreeHost(h->beta_pinned);
   if (h->prior_mu) cudaFree(h->prior_mu);
   if (h->prior_sigma) cudaFree(h->prior_sigma);
+  if (h->xt_cache) cudaFree(h->xt_cache);
+  h->xt_cache = nullptr;
   h->X = nullptr;
   h->y = nullptr;
   h->partials = nullptr;
@@ -651,8 +654,7 @@ cudaError_t launch_diff(const DiffArgs& a, const DeltaPack& dp, int grid, cudaSt
 }
 
 void free_ws(pm_ws_s* w) {
-  if (w->xbeta) cudaFree(w->xbeta);
-  if (w->xt) cudaFree(w->xt);
+  if (w->xbeta) cudaFree(w->xbeta);  // w->xt is the handle's shared transposed copy
   if (w->tmp) cudaFree(w->tmp);
   if (w->beta_dev) cudaFree(w->beta_dev);
   if (w->partials) cudaFree(w->partials);
@@ -692,7 +694,11 @@ int pm_ws_create(pm_glm_t h, const double* beta0, pm_ws_t* out) {
   };
   chk(cudaMalloc(&w->xbeta, sizeof(double) * np));
   chk(cudaMalloc(&w->tmp, sizeof(double) * np));
-  chk(cudaMalloc(&w->xt, sizeof(double) * size_t(K) * np));
+  // X^T (GlmWorkspace.xt, glm.py:473) depends only on the immutable design: built once per
+  // handle and shared read-only by all of its workspaces (repeat chains skip the transpose)
+  const bool build_xt = h->xt_cache == nullptr;
+  if (build_xt) chk(cudaMalloc(&h->xt_cache, sizeof(double) * size_t(K) * np));
+  w->xt = h->xt_cache;
   chk(cudaMalloc(&w->beta_dev, sizeof(double) * K));
   w->grid = (int)std::max<int64_t>(1, std::min<int64_t>(int64_t(h->sms) * 4, (n + 255) / 256));
   chk(cudaMalloc(&w->partials, sizeof(double) * size_t(w->grid) * kMaxDeltas));
@@ -710,10 +716,13 @@ int pm_ws_create(pm_glm_t h, const double* beta0, pm_ws_t* out) {
   chk(cudaMemcpyAsync(w->beta_dev, beta0, sizeof(double) * K, cudaMemcpyHostToDevice, h->stream));
   chk(launch_xbeta(h, w->beta_dev, w->xbeta));
   dim3 tg(unsigned((n + 31) / 32), unsigned((K + 31) / 32));
-  if (h->xtype == PM_X_F64)
-    transpose_kernel<double><<<tg, 256, 0, h->stream>>>(static_cast<const double*>(h->X), n, K, w->xt, np);
-  else
-    transpose_kernel<float><<<tg, 256, 0, h->stream>>>(static_cast<const float*>(h->X), n, K, w->xt, np);
+  if (build_xt && e == cudaSuccess) {
+    chk(cudaMemsetAsync(h->xt_cache, 0, sizeof(double) * size_t(K) * np, h->stream));  // padding rows
+    if (h->xtype == PM_X_F64)
+      transpose_kernel<double><<<tg, 256, 0, h->stream>>>(static_cast<const double*>(h->X), n, K, w->xt, np);
+    else
+      transpose_kernel<float><<<tg, 256, 0, h->stream>>>(static_cast<const float*>(h->X), n, K, w->xt, np);
+  }
   chk(cudaGetLastError());
   chk(cudaStreamSynchronize(h->stream));
   if (e != cudaSuccess) {
