@@ -91,6 +91,16 @@ class IsingLattice:
         spins = 2 * image01.astype(np.int8) - 1
         return cls(spins, bias_scale * spins.astype(np.float64), w)
 
+    def log_weight(self, s=None) -> float:
+        """Log of the unnormalised stationary probability of state s (ising.py:84-93):
+        (b.s + w * sum over lattice edges of s_i s_j) / 2, whose single-site conditionals
+        are expit(b_i + w * neighbour sum).  Periodic lattices include the wrap edges."""
+        sf = (self.s if s is None else np.asarray(s)).astype(np.float64)
+        edges = float(np.sum(sf[1:, :] * sf[:-1, :]) + np.sum(sf[:, 1:] * sf[:, :-1]))
+        if self.boundary == "periodic":
+            edges += float(np.sum(sf[0, :] * sf[-1, :]) + np.sum(sf[:, 0] * sf[:, -1]))
+        return 0.5 * (float(np.sum(self.b * sf)) + self.w * edges)
+
 
 class PottsLattice:
     """q=4 Potts lattice: states 0..3, P(a | rest) proportional to exp(coupling * n_a)."""
@@ -207,6 +217,7 @@ class ColorPartition:
         flat_color = (np.add.outer(np.arange(h), np.arange(w)) % 2).ravel()
         self.colors = [np.flatnonzero(flat_color == c) for c in (0, 1)]
         model = _lib.PM_MODEL_POTTS4 if isinstance(lat, PottsLattice) else _lib.PM_MODEL_ISING
+        self._periodic = lat.boundary == "periodic"
         self.device = LatticeDevice(h, w, lat.boundary, model, device)
         if model == _lib.PM_MODEL_ISING:
             b = np.ascontiguousarray(lat.b, dtype=np.float64)
@@ -228,6 +239,19 @@ class ColorPartition:
 
     def unpack_into(self, lat) -> None:
         lat.s[...] = self.device.get_spins()
+
+    @property
+    def packed_s(self) -> list[np.ndarray]:
+        """Per-colour values in packed (scan) order, float64 (ising.py:134-136); a host copy
+        of the device state."""
+        flat = self.device.get_spins().ravel().astype(np.float64)
+        return [flat[self.colors[c]] for c in (0, 1)]
+
+    def neighbor_spin_sum(self, c: int) -> np.ndarray:
+        """Exact neighbour sums of colour c's sites in packed order (ising.py:148-150), from
+        the device state; 0 outside a free boundary, wrap-around when periodic."""
+        s = self.device.get_spins()
+        return _neighbour_sum_grid(s, self._periodic).ravel()[self.colors[c]]
 
 
 def color_lattice(lat, device: int = 0) -> ColorPartition:

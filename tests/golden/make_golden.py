@@ -154,6 +154,12 @@ def ising_fixture():
     for _ in range(60):
         ris.gibbs_sweep(lat, part, buf)
     out["img_s1"] = lat.s.copy()
+    # partition accessors and the stationary log weight (ising.py:84-93, 134-150)
+    out["img_nsum0"], out["img_nsum1"] = part.neighbor_spin_sum(0), part.neighbor_spin_sum(1)
+    out["img_packed0"], out["img_packed1"] = part.packed_s[0].copy(), part.packed_s[1].copy()
+    out["img_logw"] = np.float64(lat.log_weight())
+    out["logw_cases"] = np.array([ris.IsingLattice(out[f"s1_{i}"], out[f"b_{i}"], float(out[f"w_{i}"])).log_weight()
+                                  for i in range(len(cases))])
     out["n_cases"] = len(cases)
     np.savez_compressed(os.path.join(HERE, "ising.npz"), **out)
 

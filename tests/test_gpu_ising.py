@@ -201,3 +201,19 @@ def test_strips_match_single_lattice(gpu, n_strips, model):
     else:
         ref = go.potts_sweeps(full, 1.0986, True, sweeps, go.RNG_PHILOX4X32, seed, 0, 0)
     np.testing.assert_array_equal(got, ref)
+
+
+def test_partition_accessors_match_reference(gpu):
+    # ColorPartition.packed_s / neighbor_spin_sum (ising.py:134-150) after the reference's
+    # 60-sweep image trajectory, read back from the device state
+    z = golden("ising.npz")
+    lat = IsingLattice(z["img_s0"], z["img_b"], 1.0)
+    part = color_lattice(lat)
+    buf = DeviateBuffer(BufferKind.UNIFORM01, seed=9)
+    gibbs_sweeps(lat, part, buf, 60)
+    np.testing.assert_array_equal(lat.s, z["img_s1"])
+    np.testing.assert_array_equal(part.neighbor_spin_sum(0), z["img_nsum0"])
+    np.testing.assert_array_equal(part.neighbor_spin_sum(1), z["img_nsum1"])
+    np.testing.assert_array_equal(part.packed_s[0], z["img_packed0"])
+    np.testing.assert_array_equal(part.packed_s[1], z["img_packed1"])
+    assert lat.log_weight() == float(z["img_logw"])

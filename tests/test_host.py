@@ -132,3 +132,30 @@ def test_device_calls_fail_loudly_without_gpu():
     from paper_1310_1537_b200.glm import loglike_grad
     with pytest.raises(RuntimeError, match="no CUDA device"):
         loglike_grad(d, np.zeros(2))
+
+
+def test_log_weight_matches_reference_fixture():
+    # IsingLattice.log_weight (ising.py:84-93) on the reference's own trajectories
+    from paper_1310_1537_b200.ising import IsingLattice
+    z = golden("ising.npz")
+    for i in range(int(z["n_cases"])):
+        lat = IsingLattice(z[f"s1_{i}"], z[f"b_{i}"], float(z[f"w_{i}"]))
+        assert lat.log_weight() == pytest.approx(float(z["logw_cases"][i]), rel=1e-14, abs=1e-12)
+    lat = IsingLattice(z["img_s1"], z["img_b"], 1.0)
+    assert lat.log_weight() == pytest.approx(float(z["img_logw"]), rel=1e-14)
+    # explicit state argument and a periodic lattice counting the wrap edges
+    s = np.array([[1, -1], [1, 1]], dtype=np.int8)
+    per = IsingLattice(s, np.zeros((2, 2)), 0.5, boundary="periodic")
+    assert per.log_weight() == 0.5 * 0.5 * (2 * (1 * 1 + (-1) * 1) + 2 * (1 * -1 + 1 * 1))
+
+
+def test_run_region_contract():
+    from paper_1310_1537_b200.instrumentation import counters
+    from paper_1310_1537_b200.parallel import run_region
+    before = counters.snapshot() if hasattr(counters, "snapshot") else None
+    out = run_region([lambda i=i: i * i for i in range(6)])
+    assert out == [0, 1, 4, 9, 16, 25]
+    # nested regions run inline and still return in order
+    assert run_region([lambda: run_region([lambda: 1, lambda: 2]), lambda: [3]]) == [[1, 2], [3]]
+    assert run_region([]) == []
+    del before
