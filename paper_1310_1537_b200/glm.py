@@ -26,6 +26,7 @@ from dataclasses import dataclass
 from enum import Enum
 
 import numpy as np
+from scipy.special import expit  # noqa: F401  (module attribute of the reference glm as well)
 
 from . import _lib
 from . import parallel
