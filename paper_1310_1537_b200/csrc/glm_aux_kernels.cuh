@@ -56,12 +56,14 @@ __global__ void __launch_bounds__(256) diff_eval_kernel(DiffArgs a, DeltaPack dp
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w][threadIdx.x];
     a.partials[size_t(blockIdx.x) * kMaxDeltas + threadIdx.x] = s;
   }
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) flag = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
+  if (threadIdx.x == 0) {  // one acq_rel ticket publishes / acquires the CTA partials (see K1)
+    unsigned t;
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(a.counter) : "memory");
+    flag = (t == gridDim.x - 1);
+  }
   __syncthreads();
   if (!flag) return;
-  __threadfence();
   if (threadIdx.x < M) {
     double s0 = 0.0, s1 = 0.0;
     int b = 0;

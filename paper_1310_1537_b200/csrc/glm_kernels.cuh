@@ -289,15 +289,21 @@ __device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& s
     }
     mine[c] = acc;
   }
-  __threadfence();
+#ifdef PM_AB_NO_FINALIZE  // A/B timing experiment only: CTA partials, no cross-CTA finish
+  return;
+#endif
+  // One acq_rel ticket by thread 0 after the CTA barrier publishes the whole CTA's partial
+  // (PTX fences are cumulative over writes ordered before them by bar.sync) and, in the last
+  // CTA, acquires every other CTA's; replaces two per-thread __threadfence() (MEMBAR +
+  // L1 invalidation), measured ~4 us of a c0 launch.
   __syncthreads();
   if (tid == 0) {
-    const unsigned t = atomicAdd(a.counter, 1u);
+    unsigned t;
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(a.counter) : "memory");
     *sm.flag = (t == gridDim.x - 1) ? 1 : 0;
   }
   __syncthreads();
   if (*sm.flag == 0) return;
-  __threadfence();
   const int G = gridDim.x;
   const int lane = tid & 31, nwarps = blockDim.x >> 5;
   if (a.with_prior) {  // -0.5 z_k^2 (sampler.py:55-58) computed in parallel into the free wg scratch
@@ -307,28 +313,44 @@ __device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& s
     }
     __syncthreads();
   }
-  // column totals in a fixed order: one warp per column, lane l folds CTAs l, l+32, ...
-  // (all loads independent, so one L2 round trip per 32 CTAs), then the fixed butterfly
-  for (int c = tid >> 5; c <= K; c += nwarps) {
-    if (c > 0 && !grad) break;
-    double part = 0.0;
-    for (int b = lane; b < G; b += 32) part += __ldcg(a.partials + size_t(b) * (K + 1) + c);
-    const double tot = warp_sum(part);
-    if (lane != 0) continue;
-    if (c == 0) {
-      double f = tot;  // partials already hold -sum(nll) = L
-      if (a.with_prior) {
-        for (int k = 0; k < K; ++k) f += sm.wg[k];  // prior terms, ascending k
+  // column totals in a fixed order: one warp per column, lane l folds CTAs l, l+32, ...,
+  // then the fixed butterfly.  A warp takes CU of its columns at once so their L2 loads are
+  // all in flight together (one round trip instead of CU; this finish is on the critical
+  // path of every launch).  The per-column summation order is unchanged.
+  constexpr int CU = 4;
+  const int ncols = grad ? K + 1 : 1;
+  for (int c0 = tid >> 5; c0 < ncols; c0 += nwarps * CU) {
+    double part[CU];
+#pragma unroll
+    for (int u = 0; u < CU; ++u) part[u] = 0.0;
+    for (int b = lane; b < G; b += 32) {
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        const int c = c0 + u * nwarps;
+        if (c < ncols) part[u] += __ldcg(a.partials + size_t(b) * (K + 1) + c);
       }
-      a.out[0] = f;
-    } else {
-      const int k = c - 1;
-      double gk = tot;
-      if (a.with_prior) {
-        const double sg = a.prior_sigma[k];
-        gk -= (sm.sbeta[k] - a.prior_mu[k]) / (sg * sg);
+    }
+#pragma unroll
+    for (int u = 0; u < CU; ++u) {
+      const int c = c0 + u * nwarps;
+      if (c >= ncols) break;
+      const double tot = warp_sum(part[u]);
+      if (lane != 0) continue;
+      if (c == 0) {
+        double f = tot;  // partials already hold -sum(nll) = L
+        if (a.with_prior) {
+          for (int k = 0; k < K; ++k) f += sm.wg[k];  // prior terms, ascending k
+        }
+        a.out[0] = f;
+      } else {
+        const int k = c - 1;
+        double gk = tot;
+        if (a.with_prior) {
+          const double sg = a.prior_sigma[k];
+          gk -= (sm.sbeta[k] - a.prior_mu[k]) / (sg * sg);
+        }
+        a.out[c] = gk;
       }
-      a.out[c] = gk;
     }
   }
   if (tid == 0) *a.counter = 0u;  // re-arm for the next launch (kernel boundary orders it)
