@@ -7,11 +7,13 @@ step, prior N(0, 10^2)), the largest configuration that fits one GPU (8.08 GB of
 One step = one log-posterior + gradient evaluation over all N rows.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--config c1|c1f32|c0|c3|c4|c4potts]
+                    [--config c1|c1f32|c0|c2|c3|c3sweep|c4|c4potts|rng] [--force-dist]
 
 N>1 runs one process per GPU under torch.distributed.run (NCCL): rows are split by
 the reference's partition rule, each rank streams its shard and the (K+1)-double
-partials are all-gathered and summed in rank order.
+partials are all-gathered and summed in rank order (--force-dist runs that rank path
+as a 1-rank group on one GPU).  c4 at N>1 splits the lattice into row strips with halo
+exchange; the other configs are replicas.
 
 `--impl reference` times the reference algorithm's CPU implementation on this host
 (the numpy restatement in oracle/glm_oracle.py, PLF over all host threads, OpenBLAS
@@ -23,7 +25,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess

@@ -6,7 +6,6 @@ import argparse
 import os
 import sys
 
-import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1310_1537_b200 import glm  # noqa: E402
