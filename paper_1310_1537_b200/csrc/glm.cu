@@ -81,6 +81,7 @@ struct pm_glm_s {
   // geometry
   int kind = KIND_NONE;
   int grid = 0, threads = 0, stages = 0, tps = 1, ncw = 7;
+  int pairs = 0;  // fp32-X consumer layout (glm_stream_kernel PAIRS)
   size_t smem = 0;
   bool launched = false;
   int last_want_grad = 1;
@@ -116,10 +117,10 @@ void free_glm_data(pm_glm_s* h) {
 // ---- stream kernel dispatch table ------------------------------------------------
 using StreamLaunch = cudaError_t (*)(const GlmArgs&, const double*, int, size_t, cudaStream_t);
 
-template <typename XT, int KC, bool GRAD>
+template <typename XT, int KC, bool GRAD, int PAIRS = 0>
 cudaError_t launch_stream(const GlmArgs& a, const double* beta, int grid, size_t smem, cudaStream_t st) {
   static std::atomic<uint64_t> attr{0};
-  auto kern = glm_stream_kernel<XT, KC, GRAD, kNCW>;
+  auto kern = glm_stream_kernel<XT, KC, GRAD, kNCW, SubRows<KC, GRAD>::value, kTileRows, PAIRS>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), attr);
   if (e != cudaSuccess) return e;
   BetaPack<KC> bp;
@@ -143,19 +144,36 @@ StreamLaunch pick_stream(int kc) {
   return nullptr;
 }
 
-StreamLaunch pick_stream_any(int xtype, int kc, bool grad) {
+template <bool GRAD>
+StreamLaunch pick_stream_pairs(int kc, int pairs) {  // fp32-X, pairs layouts (even kc)
+  if (pairs == 2) {
+    if (kc == 2) return launch_stream<float, 2, GRAD, 2>;
+    if (kc == 4) return launch_stream<float, 4, GRAD, 2>;
+    return nullptr;
+  }
+  switch (kc) {
+    case 2: return launch_stream<float, 2, GRAD, 1>;
+    case 4: return launch_stream<float, 4, GRAD, 1>;
+    case 6: return launch_stream<float, 6, GRAD, 1>;
+    case 8: return launch_stream<float, 8, GRAD, 1>;
+  }
+  return nullptr;
+}
+
+StreamLaunch pick_stream_any(int xtype, int kc, bool grad, int pairs) {
   if (xtype == PM_X_F64) return grad ? pick_stream<double, true>(kc) : pick_stream<double, false>(kc);
+  if (pairs) return grad ? pick_stream_pairs<true>(kc, pairs) : pick_stream_pairs<false>(kc, pairs);
   return grad ? pick_stream<float, true>(kc) : pick_stream<float, false>(kc);
 }
 
 // 15 consumer warps (512 threads, <= 128 registers) with half-height register sub-tiles:
 // twice the warps to hide the latency chains of the compute-bound fp32-X variant.
 constexpr int kNCW15 = 15;
-template <typename XT, int KC, bool GRAD>
+template <typename XT, int KC, bool GRAD, int PAIRS>
 cudaError_t launch_stream15(const GlmArgs& a, const double* beta, int grid, size_t smem, cudaStream_t st) {
   static std::atomic<uint64_t> attr{0};
   constexpr int R = !GRAD ? 16 : (KC <= 2 ? 16 : 8);
-  auto kern = glm_stream_kernel<XT, KC, GRAD, kNCW15, R>;
+  auto kern = glm_stream_kernel<XT, KC, GRAD, kNCW15, R, kTileRows, PAIRS>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), attr);
   if (e != cudaSuccess) return e;
   BetaPack<KC> bp;
@@ -164,12 +182,17 @@ cudaError_t launch_stream15(const GlmArgs& a, const double* beta, int grid, size
   return cudaGetLastError();
 }
 
-StreamLaunch pick_stream15(int kc, bool grad) {  // fp32-X only
+StreamLaunch pick_stream15(int kc, bool grad, int pairs) {  // fp32-X only
+  if (pairs) {
+    if (kc == 2) return grad ? launch_stream15<float, 2, true, 1> : launch_stream15<float, 2, false, 1>;
+    if (kc == 4) return grad ? launch_stream15<float, 4, true, 1> : launch_stream15<float, 4, false, 1>;
+    return nullptr;
+  }
   switch (kc) {
-    case 1: return grad ? launch_stream15<float, 1, true> : launch_stream15<float, 1, false>;
-    case 2: return grad ? launch_stream15<float, 2, true> : launch_stream15<float, 2, false>;
-    case 3: return grad ? launch_stream15<float, 3, true> : launch_stream15<float, 3, false>;
-    case 4: return grad ? launch_stream15<float, 4, true> : launch_stream15<float, 4, false>;
+    case 1: return grad ? launch_stream15<float, 1, true, 0> : launch_stream15<float, 1, false, 0>;
+    case 2: return grad ? launch_stream15<float, 2, true, 0> : launch_stream15<float, 2, false, 0>;
+    case 3: return grad ? launch_stream15<float, 3, true, 0> : launch_stream15<float, 3, false, 0>;
+    case 4: return grad ? launch_stream15<float, 4, true, 0> : launch_stream15<float, 4, false, 0>;
   }
   return nullptr;
 }
@@ -238,6 +261,7 @@ int choose_geometry(pm_glm_s* h) {
   const int kc = (h->K + 31) / 32;
   const int budget = std::min(max_optin_smem(h->device), 232448) - 1024;
   h->kind = KIND_NONE;
+  h->pairs = 0;
   const char* env_rows = std::getenv("PM_GLM_ROWS");
   // row-per-lane kernel: fp64, even K <= 30, and enough tiles to fill the machine (measured on
   // B200, tools/ab_rows_k.py: 1.3-2x faster than the column kernel at N = 1e7 for K <= 30; at
@@ -290,9 +314,21 @@ int choose_geometry(pm_glm_s* h) {
       h->smem = stream_smem_bytes(h->K, xs, S, kNCW);
       h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, h->n_tiles));
     }
-    // fp32-X, K <= 128: 15 consumer warps (measured +2 % at c1f32; PM_STREAM_NCW=7 disables)
+    // fp32-X, even K with an even register count: the pairs consumer layout
+    // (consume_tile_pairs; PM_F32_PAIRS=0 disables for A/B)
+    // 1 = sub-tile pairs (default; +5.5 % over columns at c1f32), 2 = whole-tile consumer
+    // (KC 2 or 4, 7 warps; measured 11 % slower than pairs at K=100: the re-read stage is held
+    // for the whole tile and 2 stages per warp expose the refill latency), 0 = columns
+    const char* epr = std::getenv("PM_F32_PAIRS");
+    const int pmode = epr ? std::atoi(epr) : 1;
+    h->pairs = 0;
+    if (h->kind == KIND_STREAM && h->xtype == PM_X_F32 && h->K % 2 == 0 && kc % 2 == 0 && pmode > 0)
+      h->pairs = (pmode == 2 && kc <= 4) ? 2 : 1;
+    // fp32-X, K <= 128: 15 consumer warps, one 32-row stage each (PM_STREAM_NCW=7 disables;
+    // measured: 16-row stages, 2 per warp, are 26 % slower -- per-stage overheads dominate)
     const char* e15 = std::getenv("PM_STREAM_NCW");
-    if (h->kind == KIND_STREAM && h->xtype == PM_X_F32 && kc <= 4 && !(e15 && std::atoi(e15) == 7)) {
+    if (h->kind == KIND_STREAM && h->xtype == PM_X_F32 && kc <= 4 && h->pairs != 2 &&
+        !(e15 && std::atoi(e15) == 7)) {
       const size_t fixed15 = stream_smem_bytes(h->K, xs, 0, kNCW15);
       int S15 = int((budget - (long)fixed15) / (long)per_stage);
       S15 -= S15 % kNCW15;
@@ -349,23 +385,38 @@ int check_beta(pm_glm_s* h, const double* beta) {
 int enqueue_eval(pm_glm_s* h, const double* beta, bool with_prior, bool grad, double* out, cudaStream_t st) {
   GlmArgs a = make_args(h, with_prior, out);
   cudaError_t e;
-  if (h->kind == KIND_STREAM) {
-    StreamLaunch fn = h->ncw == kNCW15 ? pick_stream15((h->K + 31) / 32, grad)
-                                       : pick_stream_any(h->xtype, (h->K + 31) / 32, grad);
+  // the fp32-X stream kernel widens X by integer ops to x * 2^-896 and scales beta by 2^896
+  // (glm_kernels.cuh ld_x_scaled); a beta that large would overflow, so it takes the wide
+  // kernel (plain conversions) instead -- same results, slower, never hit by real chains
+  bool wide_fallback = false;
+  if (h->kind == KIND_STREAM && h->xtype == PM_X_F32) {
+    for (int k = 0; k < h->K; ++k) wide_fallback |= !(std::fabs(beta[k]) < 0x1p100);
+  }
+  if (h->kind == KIND_STREAM && !wide_fallback) {
+    StreamLaunch fn = h->ncw == kNCW15 ? pick_stream15((h->K + 31) / 32, grad, h->pairs)
+                                       : pick_stream_any(h->xtype, (h->K + 31) / 32, grad, h->pairs);
     e = fn(a, beta, h->grid, h->smem, st);
   } else if (h->kind == KIND_ROWS) {
     RowsLaunch fn = grad ? pick_rows<true>(h->K) : pick_rows<false>(h->K);
     e = fn(a, beta, h->grid, h->smem, h->tps, h->ncw, st);
   } else {
+    int grid = h->grid, threads = h->threads;
+    size_t smem = h->smem;
+    if (wide_fallback) {
+      const int nw = kWideThreads / 32;
+      grid = (int)std::max<int64_t>(1, std::min<int64_t>(int64_t(h->sms) * 2, (h->n_rows + nw - 1) / nw));
+      threads = nw * 32;
+      smem = stream_smem_bytes(h->K, 4, 0, nw);  // K <= 256 here: always fits
+    }
     std::memcpy(h->beta_pinned, beta, sizeof(double) * h->K);
     e = cudaMemcpyAsync(h->beta_dev, h->beta_pinned, sizeof(double) * h->K, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) {
       if (h->xtype == PM_X_F64)
-        e = grad ? launch_wide<double, true>(a, h->grid, h->threads, h->smem, st)
-                 : launch_wide<double, false>(a, h->grid, h->threads, h->smem, st);
+        e = grad ? launch_wide<double, true>(a, grid, threads, smem, st)
+                 : launch_wide<double, false>(a, grid, threads, smem, st);
       else
-        e = grad ? launch_wide<float, true>(a, h->grid, h->threads, h->smem, st)
-                 : launch_wide<float, false>(a, h->grid, h->threads, h->smem, st);
+        e = grad ? launch_wide<float, true>(a, grid, threads, smem, st)
+                 : launch_wide<float, false>(a, grid, threads, smem, st);
     }
   }
   if (e != cudaSuccess) return cuda_fail(e, "glm kernel launch");
@@ -468,7 +519,7 @@ int pm_glm_upload(pm_glm_t h, const void* X, int x_dtype, const double* y, int64
     free_glm_data(h);
     return rc;
   }
-  h->partials_cap = std::max(h->grid, 1);
+  h->partials_cap = std::max(std::max(h->grid, 1), 2 * h->sms);  // the fp32 wide fallback uses 2 x SMs
   PM_CUDA(cudaMalloc(&h->partials, sizeof(double) * size_t(h->partials_cap) * (n_cols + 1)));
   PM_CUDA(cudaMalloc(&h->beta_dev, sizeof(double) * n_cols));
   PM_CUDA(cudaHostAlloc(&h->out_host, sizeof(double) * (n_cols + 1), cudaHostAllocMapped | cudaHostAllocPortable));

@@ -69,6 +69,40 @@ __device__ __forceinline__ double ld_x(const XT* p) {
   return static_cast<double>(*p);
 }
 
+// fp32-X widening without F2F.F64.F32 (an XU-pipe op at a quarter of the ALU rate, the
+// measured limiter of the fp32-X stream kernel): the fp32 bit pattern s|e8|m23 becomes the
+// fp64 words hi = s|000|e8|m[22:3], lo = m[2:0] << 29, i.e. exactly x * 2^-896 for EVERY
+// finite x (zero and subnormals included: an fp32 subnormal lands on the fp64 subnormal of
+// the same scaled value).  Two ALU ops + one shift.  The caller multiplies beta and the
+// per-row residual by 2^896 (exact), so x'beta' = x beta and w' x' = w x bit for bit: the
+// results are identical to the F2F form.  Used when |beta| < 2^100 (host-checked).
+constexpr double kF32Unscale = 0x1p896;
+__device__ __forceinline__ double ld_x_scaled(const float* p) {
+  const uint32_t b = *reinterpret_cast<const uint32_t*>(p);
+  const uint32_t hi = uint32_t(int32_t(b) >> 3) & 0x8FFFFFFFu;
+  return __hiloint2double(int(hi), int(b << 29));
+}
+__device__ __forceinline__ double ld_x_scaled(const double* p) { return *p; }
+
+template <typename XT>
+struct XScale {  // factor applied to beta and to the row residual for scaled loads
+  static constexpr double value = 1.0;
+};
+template <>
+struct XScale<float> {
+#ifdef PM_F32_F2F
+  static constexpr double value = 1.0;
+#else
+  static constexpr double value = kF32Unscale;
+#endif
+};
+
+template <typename XT>
+__device__ __forceinline__ double ld_x_stream(const XT* p) {
+  if constexpr (XScale<XT>::value != 1.0) return ld_x_scaled(p);
+  return ld_x(p);
+}
+
 // Rows per register-resident sub-tile: x[R][KC] stays in registers from the dot product to
 // the gradient update, so shared memory is read once; R*KC <= 64 doubles per lane.
 template <int KC, bool GRAD>
@@ -82,12 +116,12 @@ struct SubRows {
 // Each row's transcendental terms are computed by 32/R lanes; only lane < R counts f.
 // `empty` (the stage's release barrier) is arrived on as soon as the last sub-tile's values
 // are in registers, so the producer can refill the stage while this warp still computes.
-template <typename XT, int KC, bool GRAD, int R = SubRows<KC, GRAD>::value>
+template <typename XT, int KC, bool GRAD, int R = SubRows<KC, GRAD>::value, int TR = kTileRows>
 __device__ __forceinline__ void consume_tile(const XT* xs, const double* ys, int K, int lane, int64_t row0,
                                              int64_t row_limit, const double (&breg)[KC], double (&g)[KC],
                                              double& nll_acc, uint64_t* empty) {
 #pragma unroll 1
-  for (int sub = 0; sub < 32 / R; ++sub) {
+  for (int sub = 0; sub < TR / R; ++sub) {
     const XT* xb = xs + (sub * R) * K + lane;
     double x[R][KC];
     double v[R];
@@ -96,14 +130,14 @@ __device__ __forceinline__ void consume_tile(const XT* xs, const double* ys, int
       double acc = 0.0;
 #pragma unroll
       for (int j = 0; j < KC; ++j) {
-        x[r][j] = (j < KC - 1 || lane + 32 * j < K) ? ld_x(xb + r * K + 32 * j) : 0.0;
+        x[r][j] = (j < KC - 1 || lane + 32 * j < K) ? ld_x_stream(xb + r * K + 32 * j) : 0.0;
         acc = fma(x[r][j], breg[j], acc);
       }
       v[r] = acc;
     }
     const int rr = sub * R + (lane & (R - 1));
     const double yv = ys[rr];
-    if (sub == 32 / R - 1) {
+    if (sub == TR / R - 1) {
       // the last sub-tile's loads feed v[] and yv (earlier sub-tiles were consumed before)
       double dep = yv;
 #pragma unroll
@@ -117,6 +151,7 @@ __device__ __forceinline__ void consume_tile(const XT* xs, const double* ys, int
     nll_acc += (valid && lane < R) ? nll : 0.0;
     if (GRAD) {
       w = valid ? w : 0.0;
+      if constexpr (XScale<XT>::value != 1.0) w *= XScale<XT>::value;  // exact (power of two)
       // NS interleaved accumulator sets so at least ~8 independent DFMA chains are in flight
       // (one set of KC chains would serialise on DFMA latency at small KC)
       constexpr int NS = KC >= 8 ? 1 : ((8 / KC) < R ? (8 / KC) : R);
@@ -144,6 +179,241 @@ __device__ __forceinline__ void consume_tile(const XT* xs, const double* ys, int
   }
 }
 
+// fp32-X consumer: column PAIRS per lane and XOR-permuted rows (K even, ceil(K/32) even).
+// Lane l owns columns 64c + 2l + e (c < KC/2, e < 2): one 8-byte shared load per (row, c)
+// instead of two 4-byte ones.  Slot r of lane l holds row r ^ (l & (R-1)) of the sub-tile
+// (a per-lane row offset, roff[r]), so the transpose-reduce needs no selects: at level s a
+// lane keeps slots [0, s) and adds the partner's (lane ^ s) slots [s, 2s), which hold exactly
+// the same rows.  Lane l ends with the dot product of row l & (R-1); the residual of the row
+// in slot r lives in lane l ^ r.  Bitwise deterministic for a fixed geometry; the per-row
+// arithmetic (product + sum orders) differs from consume_tile only in the lane summation tree.
+template <int KC, bool GRAD, int R, int TR>
+__device__ __forceinline__ void consume_tile_pairs(const float* xs, const double* ys, int K, int lane, int64_t row0,
+                                                   int64_t row_limit, const double (&breg)[KC], double (&g)[KC],
+                                                   double& nll_acc, uint64_t* empty, const uint32_t (&roff)[R]) {
+  static_assert(KC % 2 == 0, "pairs layout needs an even register count");
+  constexpr int KP = KC / 2;
+  const bool last_ok = 64 * (KP - 1) + 2 * lane < K;
+#pragma unroll 1
+  for (int sub = 0; sub < TR / R; ++sub) {
+    const char* xb = reinterpret_cast<const char*>(xs) + size_t(sub) * R * K * sizeof(float);
+    double x[R][KC];
+    double v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint2* pr = reinterpret_cast<const uint2*>(xb + roff[r]);
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c < KP; ++c) {
+        uint2 u = make_uint2(0u, 0u);
+        if (c < KP - 1 || last_ok) u = pr[32 * c];
+#if defined(PM_F32_F2F)
+        x[r][2 * c] = double(__uint_as_float(u.x));
+        x[r][2 * c + 1] = double(__uint_as_float(u.y));
+#elif defined(PM_F32_MIX)  // A/B: one F2F (XU pipe, unscaled) + one integer widening per pair
+        x[r][2 * c] = double(__uint_as_float(u.x));
+        x[r][2 * c + 1] = ld_x_scaled(reinterpret_cast<const float*>(&u.y));
+#else
+        x[r][2 * c] = ld_x_scaled(reinterpret_cast<const float*>(&u.x));
+        x[r][2 * c + 1] = ld_x_scaled(reinterpret_cast<const float*>(&u.y));
+#endif
+        acc = fma(x[r][2 * c], breg[2 * c], acc);
+        acc = fma(x[r][2 * c + 1], breg[2 * c + 1], acc);
+      }
+      v[r] = acc;
+    }
+    const int rr = sub * R + (lane & (R - 1));
+    const double yv = ys[rr];
+    if (sub == TR / R - 1) {
+      double dep = yv;
+#pragma unroll
+      for (int r = 0; r < R; ++r) dep += v[r];
+      mbar_arrive_after(empty, dep, lane, const_cast<float*>(xs));
+    }
+#pragma unroll
+    for (int st = R / 2; st >= 1; st >>= 1) {
+#pragma unroll
+      for (int i = 0; i < st; ++i) v[i] += shfl_xor_d(v[i + st], st);
+    }
+    double t = v[0];
+#pragma unroll
+    for (int m = R; m < 32; m <<= 1) t += shfl_xor_d(t, m);
+    double nll, w;
+    row_terms(t, yv, nll, w);
+    const bool valid = row0 + rr < row_limit;
+    nll_acc += (valid && lane < R) ? nll : 0.0;
+    if (GRAD) {
+      w = valid ? w : 0.0;
+#ifndef PM_F32_MIX
+      w *= XScale<float>::value;  // exact (power of two)
+#endif
+      constexpr int NS = KC >= 8 ? 1 : ((8 / KC) < R ? (8 / KC) : R);
+      double ga[NS > 1 ? NS - 1 : 1][KC];
+#pragma unroll
+      for (int s2 = 0; s2 + 1 < NS; ++s2)
+#pragma unroll
+        for (int j = 0; j < KC; ++j) ga[s2][j] = 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double wr0 = r == 0 ? w : shfl_xor_d(w, r);
+#ifdef PM_F32_MIX
+        const double wr1 = wr0 * XScale<float>::value;  // odd registers hold x * 2^-896
+#else
+        const double wr1 = wr0;
+#endif
+        if (r % NS == 0) {
+#pragma unroll
+          for (int j = 0; j < KC; ++j) g[j] = fma((j & 1) ? wr1 : wr0, x[r][j], g[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < KC; ++j)
+            ga[r % NS - 1][j] = fma((j & 1) ? wr1 : wr0, x[r][j], ga[r % NS - 1][j]);
+        }
+      }
+#pragma unroll
+      for (int s2 = 0; s2 + 1 < NS; ++s2)
+#pragma unroll
+        for (int j = 0; j < KC; ++j) g[j] += ga[s2][j];
+    }
+  }
+}
+
+// fp32-X whole-tile consumer (pairs layout, KC in {2, 4}, 7 consumer warps, 2 stages per
+// warp).  A tile's 32 rows are taken as 4 blocks of 8 XOR-permuted rows (as in
+// consume_tile_pairs); the 8-lane partial sums of the 4 blocks are then reduced across lane
+// bits 3 and 4 with a select transpose, so lane l ends with the full dot product of tile row
+// l: the logistic terms are evaluated ONCE per row (32 distinct rows per warp evaluation,
+// instead of 32/R lanes repeating each row -- that latency chain bounded the sub-tile
+// consumers).  HOLD (KC = 2): the raw fp32 words stay in registers and the stage is released
+// right after the dot products; otherwise (KC = 4, the registers do not fit) the gradient
+// pass re-reads the stage and releases it afterwards.  Widening: integer ops for the dot
+// products (x * 2^-896 against beta * 2^896), F2F for a re-read gradient pass (balances the
+// ALU and XU pipes; both exact, so the results do not depend on the choice).
+template <int KC, bool GRAD>
+__device__ __forceinline__ void consume_tile_f32full(const float* xs, const double* ys, int K, int lane,
+                                                     int64_t row0, int64_t row_limit, const double (&breg)[KC],
+                                                     double (&g)[KC], double& nll_acc, uint64_t* empty,
+                                                     const uint32_t (&roff)[8]) {
+  static_assert(KC == 2 || KC == 4, "whole-tile fp32 consumer: KC 2 or 4");
+  constexpr int KP = KC / 2;
+  constexpr bool HOLD = KC == 2;
+  const bool last_ok = 64 * (KP - 1) + 2 * lane < K;
+  const int b = lane & 7;
+  const char* xb = reinterpret_cast<const char*>(xs);
+  const uint32_t blk = uint32_t(8 * K * sizeof(float));
+  auto load = [&](int s, int r, int c) -> uint2 {
+    uint2 u = make_uint2(0u, 0u);
+    if (c < KP - 1 || last_ok) u = reinterpret_cast<const uint2*>(xb + s * blk + roff[r])[32 * c];
+    return u;
+  };
+  uint2 xr[HOLD ? 4 : 1][8][KP];
+  if constexpr (HOLD) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < KP; ++c) xr[s][r][c] = load(s, r, c);
+  }
+  const double yv = ys[lane];
+  double vs[4];
+  double dep = yv;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    double v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c < KP; ++c) {
+        const uint2 u = HOLD ? xr[HOLD ? s : 0][r][c] : load(s, r, c);
+        acc = fma(ld_x_scaled(reinterpret_cast<const float*>(&u.x)), breg[2 * c], acc);
+        acc = fma(ld_x_scaled(reinterpret_cast<const float*>(&u.y)), breg[2 * c + 1], acc);
+      }
+      v[r] = acc;
+      dep += acc;
+    }
+#pragma unroll
+    for (int st = 4; st >= 1; st >>= 1) {
+#pragma unroll
+      for (int i = 0; i < st; ++i) v[i] += shfl_xor_d(v[i + st], st);
+    }
+    vs[s] = v[0];  // block s, row 8s + b, summed over the 8 lanes sharing lane bits 3-4
+  }
+  if (HOLD || !GRAD) mbar_arrive_after(empty, dep, lane, const_cast<float*>(xs));  // all words consumed
+  // across lane bits 4 then 3: lane l keeps block (l >> 3), i.e. tile row l
+  {
+    const bool up = (lane & 16) != 0;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const double send = up ? vs[i] : vs[i + 2];
+      const double keep = up ? vs[i + 2] : vs[i];
+      vs[i] = keep + shfl_xor_d(send, 16);
+    }
+    const bool up1 = (lane & 8) != 0;
+    const double send = up1 ? vs[0] : vs[1];
+    const double keep = up1 ? vs[1] : vs[0];
+    vs[0] = keep + shfl_xor_d(send, 8);
+  }
+  const double t = vs[0];
+  double nll, w;
+  row_terms(t, yv, nll, w);
+  const bool valid = row0 + lane < row_limit;
+  nll_acc += valid ? nll : 0.0;
+  if (GRAD) {
+    // HOLD widens by integer ops (x * 2^-896): scale w by 2^896 (exact); else F2F (unscaled)
+    w = valid ? (HOLD ? w * kF32Unscale : w) : 0.0;
+    constexpr int NS = KC == 2 ? 4 : 2;
+    double ga[NS - 1][KC];
+#pragma unroll
+    for (int s2 = 0; s2 + 1 < NS; ++s2)
+#pragma unroll
+      for (int j = 0; j < KC; ++j) ga[s2][j] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const double wr = __shfl_sync(0xffffffffu, w, 8 * s + (r ^ b));
+        const int set = (8 * s + r) % NS;
+#pragma unroll
+        for (int c = 0; c < KP; ++c) {
+          double x0, x1;
+          if constexpr (HOLD) {
+            x0 = ld_x_scaled(reinterpret_cast<const float*>(&xr[s][r][c].x));
+            x1 = ld_x_scaled(reinterpret_cast<const float*>(&xr[s][r][c].y));
+          } else {
+            const uint2 u = load(s, r, c);
+            x0 = double(__uint_as_float(u.x));
+            x1 = double(__uint_as_float(u.y));
+          }
+          if (set == 0) {
+            g[2 * c] = fma(wr, x0, g[2 * c]);
+            g[2 * c + 1] = fma(wr, x1, g[2 * c + 1]);
+          } else {
+            ga[set - 1][2 * c] = fma(wr, x0, ga[set - 1][2 * c]);
+            ga[set - 1][2 * c + 1] = fma(wr, x1, ga[set - 1][2 * c + 1]);
+          }
+        }
+      }
+#pragma unroll
+    for (int s2 = 0; s2 + 1 < NS; ++s2)
+#pragma unroll
+      for (int j = 0; j < KC; ++j) g[j] += ga[s2][j];
+    if constexpr (!HOLD) {
+      double dg = 0.0;
+#pragma unroll
+      for (int j = 0; j < KC; ++j) dg += g[j];  // depends on every re-read word
+      mbar_arrive_after(empty, dg, lane, const_cast<float*>(xs));
+    }
+  }
+}
+
+// Column owned by register j of `lane` in the two consumer layouts.
+template <bool PAIRS>
+__device__ __forceinline__ int lane_col(int lane, int j) {
+  return PAIRS ? 64 * (j >> 1) + 2 * lane + (j & 1) : lane + 32 * j;
+}
+
 // Shared-memory carve-up of the streaming kernels.
 struct StreamSmem {
   unsigned char* xs;  // [S][tile_bytes]
@@ -158,10 +428,11 @@ struct StreamSmem {
 
 __host__ __device__ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-__host__ __device__ inline size_t stream_smem_bytes(int K, int xsize, int S, int nw) {
-  size_t tile = size_t(kTileRows) * K * xsize;
+// tr = rows per stage (a 32-row tile, or half of one for the 2-stages-per-warp fp32-X variant)
+__host__ __device__ inline size_t stream_smem_bytes(int K, int xsize, int S, int nw, int tr = kTileRows) {
+  size_t tile = size_t(tr) * K * xsize;
   size_t b = align_up(tile, 128) * S;
-  b += size_t(S) * 32 * sizeof(double);
+  b += size_t(S) * tr * sizeof(double);
   b += size_t(2 * S) * sizeof(uint64_t);
   b += align_up(size_t(K) * sizeof(double), 16);
   b += size_t(nw) * K * sizeof(double);
@@ -169,14 +440,15 @@ __host__ __device__ inline size_t stream_smem_bytes(int K, int xsize, int S, int
   return b;
 }
 
-__device__ inline StreamSmem carve_stream_smem(unsigned char* base, int K, int xsize, int S, int nw) {
+__device__ inline StreamSmem carve_stream_smem(unsigned char* base, int K, int xsize, int S, int nw,
+                                               int tr = kTileRows) {
   StreamSmem s;
-  size_t tile = align_up(size_t(kTileRows) * K * xsize, 128);
+  size_t tile = align_up(size_t(tr) * K * xsize, 128);
   unsigned char* p = base;
   s.xs = p;
   p += tile * S;
   s.ys = reinterpret_cast<double*>(p);
-  p += size_t(S) * 32 * sizeof(double);
+  p += size_t(S) * tr * sizeof(double);
   s.full = reinterpret_cast<uint64_t*>(p);
   p += size_t(S) * sizeof(uint64_t);
   s.empty = reinterpret_cast<uint64_t*>(p);
@@ -191,10 +463,12 @@ __device__ inline StreamSmem carve_stream_smem(unsigned char* base, int K, int x
   return s;
 }
 
-// Producer/consumer ring over the tiles tile_begin, tile_begin+stride, ... < tile_end.
+// Producer/consumer ring over the tiles tile_begin, tile_begin+stride, ... < tile_end
+// (a "tile" here is one stage: TR consecutive rows).
 // Warp 0 lane 0 issues TMA bulk copies; warps 1..NCW consume tiles round-robin.
 // Rows with global (padded) index >= row_limit are masked (padding).
-template <typename XT, int KC, bool GRAD, int NCW, int R = SubRows<KC, GRAD>::value>
+template <typename XT, int KC, bool GRAD, int NCW, int R = SubRows<KC, GRAD>::value, int TR = kTileRows,
+          int PAIRS = 0>
 __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const double* __restrict__ y, int K,
                                              int64_t tile_begin, int64_t tile_end, int64_t stride,
                                              int64_t row_limit, int S, const StreamSmem& sm,
@@ -202,7 +476,7 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
                                              bool evict_first) {
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t tile_elems = uint32_t(kTileRows) * K;
+  const uint32_t tile_elems = uint32_t(TR) * K;
   const uint32_t tile_bytes = tile_elems * sizeof(XT);
   const size_t tile_pitch = align_up(tile_bytes, 128);
   if (tile_begin >= tile_end) return;
@@ -221,14 +495,14 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
       for (int64_t i = 0; i < n_mine; ++i) {
         if (n > 0) mbar_wait(&sm.empty[s], (n - 1) & 1);
         const int64_t tile = tile_begin + i * stride;
-        mbar_arrive_expect_tx(&sm.full[s], tile_bytes + 32 * sizeof(double));
+        mbar_arrive_expect_tx(&sm.full[s], tile_bytes + TR * sizeof(double));
         const XT* src = X + tile * int64_t(tile_elems);
         if (evict_first) {
           bulk_g2s_hint(sm.xs + size_t(s) * tile_pitch, src, tile_bytes, &sm.full[s], pol);
         } else {
           bulk_g2s(sm.xs + size_t(s) * tile_pitch, src, tile_bytes, &sm.full[s]);
         }
-        bulk_g2s(sm.ys + size_t(s) * 32, y + tile * kTileRows, 32 * sizeof(double), &sm.full[s]);
+        bulk_g2s(sm.ys + size_t(s) * TR, y + tile * TR, TR * sizeof(double), &sm.full[s]);
         if (++s == Se) {
           s = 0;
           ++n;
@@ -241,12 +515,28 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
   if (cw >= nact) return;
   int s = cw;       // i % Se for i = cw + m*nact (Se is a multiple of nact)
   uint32_t n = 0;   // i / Se
+  constexpr int RO = PAIRS == 2 ? 8 : (PAIRS ? R : 1);
+  uint32_t roff[RO];  // pairs layouts: byte offset of slot r's row + this lane's pair
+  if constexpr (PAIRS != 0) {
+#pragma unroll
+    for (int r = 0; r < RO; ++r) roff[r] = uint32_t(((r ^ (lane & (RO - 1))) * K + 2 * lane) * sizeof(XT));
+  }
   for (int64_t i = cw; i < n_mine; i += nact) {
     mbar_wait(&sm.full[s], n & 1);
     const int64_t tile = tile_begin + i * stride;
-    consume_tile<XT, KC, GRAD, R>(reinterpret_cast<const XT*>(sm.xs + size_t(s) * tile_pitch),
-                               sm.ys + size_t(s) * 32, K, lane, tile * kTileRows, row_limit, breg, g, nll_acc,
-                               &sm.empty[s]);
+    if constexpr (PAIRS == 2) {
+      consume_tile_f32full<KC, GRAD>(reinterpret_cast<const float*>(sm.xs + size_t(s) * tile_pitch),
+                                     sm.ys + size_t(s) * TR, K, lane, tile * TR, row_limit, breg, g, nll_acc,
+                                     &sm.empty[s], roff);
+    } else if constexpr (PAIRS == 1) {
+      consume_tile_pairs<KC, GRAD, R, TR>(reinterpret_cast<const float*>(sm.xs + size_t(s) * tile_pitch),
+                                          sm.ys + size_t(s) * TR, K, lane, tile * TR, row_limit, breg, g,
+                                          nll_acc, &sm.empty[s], roff);
+    } else {
+      consume_tile<XT, KC, GRAD, R, TR>(reinterpret_cast<const XT*>(sm.xs + size_t(s) * tile_pitch),
+                                        sm.ys + size_t(s) * TR, K, lane, tile * TR, row_limit, breg, g, nll_acc,
+                                        &sm.empty[s]);
+    }
     s += nact;
     if (s >= Se) {
       s = cw;
@@ -358,13 +648,16 @@ __device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& s
 
 // K1 + K2: persistent fused single-pass kernel, one CTA per SM.
 // R: rows per register sub-tile (SubRows default; smaller R frees registers for more warps)
-template <typename XT, int KC, bool GRAD, int NCW, int R = SubRows<KC, GRAD>::value>
+// TR: rows per stage (32, or 16 so that 15 consumer warps can own 2 stages each)
+// PAIRS: fp32-X consumer layouts -- 1: consume_tile_pairs, 2: consume_tile_f32full
+template <typename XT, int KC, bool GRAD, int NCW, int R = SubRows<KC, GRAD>::value, int TR = kTileRows,
+          int PAIRS = 0>
 __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     glm_stream_kernel(GlmArgs a, BetaPack<KC> beta) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int K = a.K;
   const int S = a.stages;
-  const StreamSmem sm = carve_stream_smem(smem_raw, K, sizeof(XT), S, NCW);
+  const StreamSmem sm = carve_stream_smem(smem_raw, K, sizeof(XT), S, NCW, TR);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -380,12 +673,18 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   double breg[KC], g[KC];
 #pragma unroll
   for (int j = 0; j < KC; ++j) {
-    const int c = lane + 32 * j;
-    breg[j] = (c < K) ? beta.v[c] : 0.0;
+    const int c = lane_col<PAIRS != 0>(lane, j);
+#ifdef PM_F32_MIX
+    const double sc = (PAIRS && (j & 1) == 0) ? 1.0 : XScale<XT>::value;
+#else
+    const double sc = XScale<XT>::value;
+#endif
+    breg[j] = (c < K) ? beta.v[c] * sc : 0.0;  // exact (power of two)
     g[j] = 0.0;
   }
   double nll = 0.0;
-  stream_tiles<XT, KC, GRAD, NCW, R>(static_cast<const XT*>(a.X), a.y, K, blockIdx.x, a.n_tiles, gridDim.x,
+  stream_tiles<XT, KC, GRAD, NCW, R, TR, PAIRS>(static_cast<const XT*>(a.X), a.y, K, blockIdx.x,
+                                         a.n_tiles * (kTileRows / TR), gridDim.x,
                                      a.n_rows, S, sm, breg, g, nll, a.evict_first != 0);
   if (warp > 0) {
     const int cw = warp - 1;
@@ -394,7 +693,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     if (GRAD) {
 #pragma unroll
       for (int j = 0; j < KC; ++j) {
-        const int c = lane + 32 * j;
+        const int c = lane_col<PAIRS != 0>(lane, j);
         if (c < K) sm.wg[size_t(cw) * K + c] = g[j];
       }
     }

@@ -220,3 +220,53 @@ def test_row_per_lane_kernel_against_oracle_and_stream_kernel(gpu, n, k, monkeyp
     r2 = glm.log_posterior_grad(d2, beta, prior)
     assert d2.on_device(0).geometry()["kernel"] == "stream"
     assert rel(r.f, r2.f) < TOL and grel(r.g, r2.g) < TOL
+
+
+@pytest.mark.parametrize("pairs", ["2", "1", "0"])
+def test_fp32_storage_all_layouts(gpu, monkeypatch, pairs):
+    """fp32-X over K values that select every stream-kernel consumer layout (column per lane,
+    column pairs with XOR-permuted rows, 7 or 15 consumer warps, the wide kernel), f only and
+    f + g, against the oracle on the fp32-rounded X (1e-10)."""
+    monkeypatch.setenv("PM_F32_PAIRS", pairs)
+    gen = np.random.default_rng(77)
+    for k in (1, 2, 31, 40, 64, 66, 100, 128, 130, 192, 256, 300):
+        n = 3001 + 37 * k
+        x = gen.standard_normal((n, k))
+        x[:, 0] = 1.0
+        y = (gen.random(n) < 0.4).astype(np.float64)
+        beta = gen.normal(0, 0.3, k)
+        d = DesignMatrix(x, y)
+        plan = ExecPlan(x_storage="f32")
+        x32 = x.astype(np.float32).astype(np.float64)
+        f, g = gl.loglike_grad(x32, y, beta)
+        r = glm.loglike_grad(d, beta, plan)
+        assert rel(r.f, f) < TOL and grel(r.g, g) < TOL, k
+        assert rel(glm.loglike(d, beta, plan), f) < TOL, k
+        d.release_device()
+
+
+def test_fp32_widening_edge_values(gpu):
+    """The fp32-X kernels widen X with integer ops (x * 2^-896, beta * 2^896): zeros, signed
+    zeros, fp32 subnormals, the extreme normals and a beta too large for the scaling (routed
+    to the wide kernel) all match the oracle on the fp32-rounded X."""
+    gen = np.random.default_rng(5)
+    n, k = 4099, 100
+    x = gen.standard_normal((n, k)).astype(np.float32)
+    x[:, 0] = 1.0
+    x[::7, 3] = 0.0
+    x[1::7, 4] = -0.0
+    x[::5, 5] = np.float32(1e-42)  # subnormal
+    x[1::5, 6] = -np.float32(3e-39)  # subnormal
+    x[2::5, 7] = np.float32(1.17549435e-38)  # smallest normal
+    x[3::11, 8] = np.float32(3.0e38)
+    x[4::11, 9] = -np.float32(3.0e38)
+    y = (gen.random(n) < 0.5).astype(np.float64)
+    x64 = x.astype(np.float64)
+    d = DesignMatrix(x64, y)
+    plan = ExecPlan(x_storage="f32")
+    for beta in (gen.normal(0, 0.1, k) * (np.arange(k) < 8),
+                 np.r_[gen.normal(0, 1e-40, 10), np.zeros(k - 10)],
+                 np.r_[np.zeros(10), 2.0 ** 110, np.zeros(k - 11)]):
+        f, g = gl.loglike_grad(x64, y, beta)
+        r = glm.loglike_grad(d, beta, plan)
+        assert rel(r.f, f) < TOL and grel(r.g, g) < TOL
