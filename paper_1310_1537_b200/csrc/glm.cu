@@ -929,6 +929,9 @@ struct pm_hb_s {
   // small-K row-per-lane path (even K <= 32): balanced tile ranges + segment fold
   bool rows = false;
   int rows_grid = 0, rows_stages = 0, rows_ncw = 7, rows_tps = 1;
+  int rows_contig = 1, rows_fused = 1;  // PM_HB_CONTIG / PM_HB_FUSED = 0 for A/B
+  int* cta_g0 = nullptr;        // [rows_grid] first group of each CTA
+  unsigned* gcount = nullptr;   // [G] fused-fold tickets
   size_t rows_smem = 0;
   int64_t n_tiles = 0;
   int* seg_base = nullptr;     // [rows_grid + 1]
@@ -941,9 +944,10 @@ namespace {
 void free_hb(pm_hb_s* h) {
   for (void* p : {(void*)h->X, (void*)h->y, (void*)h->poff, (void*)h->nrows, (void*)h->betas, (void*)h->mu_dev,
                   (void*)h->sigma_dev, (void*)h->out_f, (void*)h->out_g, (void*)h->seg_base, (void*)h->gseg,
-                  (void*)h->part})
+                  (void*)h->part, (void*)h->cta_g0, (void*)h->gcount})
     if (p) cudaFree(p);
-  h->seg_base = h->gseg = nullptr;
+  h->seg_base = h->gseg = h->cta_g0 = nullptr;
+  h->gcount = nullptr;
   h->part = nullptr;
   h->rows = false;
   if (h->pin_in) cudaFreeHost(h->pin_in);
@@ -983,12 +987,21 @@ cudaError_t launch_hb_rows_n(const pm_hb_s* h, const HbArgs& a, cudaStream_t st)
   r.K = h->K;
   r.stages = h->rows_stages;
   r.tps = h->rows_tps;
+  r.contig = h->rows_contig;
+  r.fused = h->rows_fused;
   r.n_tiles = h->n_tiles;
   r.betas = a.betas;
   r.part = h->part;
+  r.cta_g0 = h->cta_g0;
+  r.gseg = h->gseg;
+  r.gcount = h->gcount;
+  r.mu = a.mu;
+  r.sigma = a.sigma;
+  r.out_f = a.out_f;
+  r.out_g = a.out_g;
   kern<<<h->rows_grid, (NCW + 1) * 32, h->rows_smem, st>>>(r);
   e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || h->rows_fused) return e;
   hb_fold_kernel<GRAD><<<h->G, 64, 0, st>>>(h->part, h->gseg, NCW, h->K, a.betas, a.mu, a.sigma, a.out_f, a.out_g);
   return cudaGetLastError();
 }
@@ -1150,13 +1163,14 @@ int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64_t* off
     auto group_of = [&](int64_t tile) {
       return int(std::upper_bound(poff.begin(), poff.end(), tile * kTileRows) - poff.begin()) - 1;
     };
-    std::vector<int> seg_base(C + 1, 0), gseg(G + 1, -1);
+    std::vector<int> seg_base(C + 1, 0), gseg(G + 1, -1), cta_g0(C, 0);
     int nseg = 0;
     for (int c = 0; c < C; ++c) {
       seg_base[c] = nseg;
       const int64_t t0 = int64_t(c) * T / C, t1 = int64_t(c + 1) * T / C;
       if (t0 >= t1) continue;
       const int gf = group_of(t0), gl = group_of(t1 - 1);
+      cta_g0[c] = gf;
       for (int g2 = gf; g2 <= gl; ++g2) {
         if (gseg[g2] < 0) gseg[g2] = nseg;
         ++nseg;
@@ -1181,6 +1195,14 @@ int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64_t* off
     PM_CUDA(cudaMalloc(&h->part, sizeof(double) * size_t(nseg) * ncw * (K + 1)));
     PM_CUDA(cudaMemcpy(h->seg_base, seg_base.data(), sizeof(int) * (C + 1), cudaMemcpyHostToDevice));
     PM_CUDA(cudaMemcpy(h->gseg, gseg.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice));
+    PM_CUDA(cudaMalloc(&h->cta_g0, sizeof(int) * C));
+    PM_CUDA(cudaMemcpy(h->cta_g0, cta_g0.data(), sizeof(int) * C, cudaMemcpyHostToDevice));
+    PM_CUDA(cudaMalloc(&h->gcount, sizeof(unsigned) * G));
+    PM_CUDA(cudaMemset(h->gcount, 0, sizeof(unsigned) * G));
+    const char* e_contig = std::getenv("PM_HB_CONTIG");
+    const char* e_fused = std::getenv("PM_HB_FUSED");
+    h->rows_contig = (e_contig && e_contig[0] == '0') ? 0 : 1;
+    h->rows_fused = (e_fused && e_fused[0] == '0') ? 0 : 1;
     h->rows = true;
     h->rows_grid = C;
     h->rows_ncw = ncw;

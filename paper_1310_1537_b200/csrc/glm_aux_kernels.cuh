@@ -249,9 +249,18 @@ struct HbRowsArgs {
   const int64_t* nrows;  // [G]
   const int* seg_base;   // [grid+1] first segment of each CTA
   int G, K, stages, tps;
+  int contig;            // 1: contiguous unit range per consumer warp; 0: round-robin
+  int fused;             // 1: fold in the same launch (per-group tickets); 0: hb_fold_kernel
   int64_t n_tiles;       // poff[G] / 32
   const double* betas;   // [G][K]
   double* part;          // [nseg][NCW][K+1]
+  const int* cta_g0;     // [grid] first group of each CTA's tile range
+  const int* gseg;       // [G+1] first segment of each group
+  unsigned* gcount;      // [G] tickets, zero between launches
+  const double* mu;      // fused fold: prior (nullable) and outputs
+  const double* sigma;
+  double* out_f;
+  double* out_g;
 };
 
 // b: this warp's copy of the group's beta in shared memory (all lanes read the same address:
@@ -342,6 +351,54 @@ __device__ __forceinline__ int group_of_tile(const int64_t* poff, int G, int64_t
   return lo;
 }
 
+// Per group: fold the partials of its segments (gseg[g] .. gseg[g+1]-1) and warps in that
+// order, add the prior (sampler.py:55-58), write f and g.  Threads tid, tid+nt, ... take the
+// columns; shared by hb_fold_kernel and the fused tail of hb_rows_kernel (identical bits).
+template <bool GRAD, bool CG>
+__device__ __forceinline__ void hb_fold_group(const double* part, const int* gseg, int nw, int K,
+                                              const double* betas, const double* mu, const double* sigma,
+                                              double* out_f, double* out_g, int grp, int tid, int nt) {
+  const int s0 = gseg[grp], s1 = gseg[grp + 1];
+  for (int c = tid; c <= K; c += nt) {
+    if (c > 0 && !GRAD) break;
+    double acc = 0.0;
+    for (int s = s0; s < s1; ++s)
+      for (int w = 0; w < nw; ++w) {
+        const double* p = part + (size_t(s) * nw + w) * (K + 1) + c;
+        acc += CG ? __ldcg(p) : *p;
+      }
+    if (c == 0) {
+      double f = -acc;
+      if (mu) {
+        for (int k = 0; k < K; ++k) {
+          const double z = (betas[size_t(grp) * K + k] - mu[k]) / sigma[k];
+          f += -0.5 * z * z;
+        }
+      }
+      out_f[grp] = f;
+    } else {
+      const int k = c - 1;
+      double gk = acc;
+      if (mu) {
+        const double sg = sigma[k];
+        gk -= (betas[size_t(grp) * K + k] - mu[k]) / (sg * sg);
+      }
+      out_g[size_t(grp) * K + k] = gk;
+    }
+  }
+}
+
+// first group of the tile range starting at `tile`, searched inside [lo, hi]
+__device__ __forceinline__ int group_of_tile_in(const int64_t* poff, int lo, int hi, int64_t tile) {
+  const int64_t row = tile * kTileRows;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (poff[mid] <= row) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
 template <int KMAX, bool GRAD, int NCW>
 __global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -364,92 +421,166 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a
     fence_mbar_init();
   }
   __syncthreads();
-  const int g_first = group_of_tile(a.poff, a.G, t0);
-  const int g_last = group_of_tile(a.poff, a.G, t1 - 1);
-  const int seg0 = a.seg_base[c];
   const int64_t n_mine = t1 - t0;
   const int64_t n_units = (n_mine + TPS - 1) / TPS;
   const uint32_t tile_bytes = uint32_t(kTileRows) * K * sizeof(double);
   const size_t stage_pitch = size_t(tile_bytes) * TPS;
   const int nact = S < NCW ? S : NCW;
-  const int Se = S - S % nact;
+  const int spw = S / nact;  // stages per consumer warp: warp w owns stages w, w + nact, ...
+  // Each consumer warp takes a CONTIGUOUS share of the CTA's units (a.contig = 1), so a warp
+  // crosses ~1-2 group boundaries per launch instead of every group of the CTA (each crossing
+  // costs a partial flush and a beta reload); a.contig = 0: round-robin, unit w + m*nact.
+  const int64_t q = n_units / nact;
+  const int rr = int(n_units - q * nact);
+  const int cw = warp - 1;
   if (warp == 0) {
     if (lane == 0) {
-      int s = 0;
-      uint32_t n = 0;
-      for (int64_t i = 0; i < n_units; ++i) {
-        if (n > 0) mbar_wait(&sm.empty[s], (n - 1) & 1);
-        const int64_t tile = t0 + i * TPS;
-        const uint32_t nt = uint32_t(t1 - tile < TPS ? t1 - tile : TPS);
-        mbar_arrive_expect_tx(&sm.full[s], nt * (tile_bytes + 32 * sizeof(double)));
-        bulk_g2s(sm.xs + size_t(s) * stage_pitch, a.X + tile * int64_t(kTileRows) * K, nt * tile_bytes, &sm.full[s]);
-        bulk_g2s(sm.ys + size_t(s) * 32 * TPS, a.y + tile * kTileRows, nt * 32 * sizeof(double), &sm.full[s]);
-        if (++s == Se) {
-          s = 0;
+      // the single producer thread is on the critical path: no divisions and no dependent
+      // global loads before its first copy (the per-warp first unit / count are rebuilt
+      // incrementally, Bresenham style)
+      const int64_t m_max = (n_units + nact - 1) / nact;
+      const int64_t step = a.contig ? 1 : nact;
+      int ms = 0;       // m % spw
+      uint32_t n = 0;   // m / spw
+      for (int64_t m = 0; m < m_max; ++m) {
+        int64_t u0 = 0;
+        int acc = 0;
+        for (int w = 0; w < nact; ++w) {
+          int64_t first, cnt;
+          if (a.contig) {
+            int64_t nxt = u0 + q;
+            acc += rr;
+            if (acc >= nact) {
+              acc -= nact;
+              ++nxt;
+            }
+            first = u0;
+            cnt = nxt - u0;
+            u0 = nxt;
+          } else {
+            first = w;
+            cnt = q + (w < rr ? 1 : 0);
+          }
+          if (m >= cnt) continue;
+          const int64_t u = first + m * step;
+          const int s = w + nact * ms;
+          if (n > 0) mbar_wait(&sm.empty[s], (n - 1) & 1);
+          const int64_t tile = t0 + u * TPS;
+          const uint32_t nt = uint32_t(t1 - tile < TPS ? t1 - tile : TPS);
+          mbar_arrive_expect_tx(&sm.full[s], nt * (tile_bytes + 32 * sizeof(double)));
+          bulk_g2s(sm.xs + size_t(s) * stage_pitch, a.X + tile * int64_t(kTileRows) * K, nt * tile_bytes,
+                   &sm.full[s]);
+          bulk_g2s(sm.ys + size_t(s) * 32 * TPS, a.y + tile * kTileRows, nt * 32 * sizeof(double), &sm.full[s]);
+        }
+        if (++ms == spw) {
+          ms = 0;
           ++n;
         }
       }
     }
-    return;
   }
-  const int cw = warp - 1;
-  if (cw >= nact) return;
-  int cur = g_first;
-  double* b = sm.wg + size_t(cw) * K;
-  double g[KMAX];
-  double nll = 0.0;
-  auto load_beta = [&](int grp) {
-    __syncwarp();  // previous group's reads of b are done
-    for (int k = lane; k < K; k += 32) b[k] = __ldg(a.betas + int64_t(grp) * K + k);
-    __syncwarp();
+  // the CTA's groups and segments (host-computed; loaded after the producer started)
+  const int g_first = a.cta_g0[c];
+  const int seg0 = a.seg_base[c];
+  const int g_last = g_first + (a.seg_base[c + 1] - seg0) - 1;
+  if (warp > 0 && cw < nact) {
+    double* b = sm.wg + size_t(cw) * K;
+    double g[KMAX];
+    double nll = 0.0;
+    auto load_beta = [&](int grp) {
+      __syncwarp();  // previous group's reads of b are done
+      for (int k = lane; k < K; k += 32) b[k] = __ldg(a.betas + int64_t(grp) * K + k);
+      __syncwarp();
 #pragma unroll
-    for (int k = 0; k < KMAX; ++k) g[k] = 0.0;
-    nll = 0.0;
-  };
-  // partial of group `grp` (this warp's share of segment seg0 + grp - g_first)
-  const int q0 = RowsSwizzle<KMAX>::value ? (lane & 7) : 0;  // chunk swizzle (consume_tile_rows)
-  auto flush = [&](int grp) {
-    double* dst = a.part + (size_t(seg0 + grp - g_first) * NCW + cw) * (K + 1);
-    const double ns = warp_sum(nll);
-    if (lane == 0) dst[0] = ns;
-    if (GRAD)
-      rows_unrotate<KMAX>(g, K, q0, [&](int k, double v) {
-        if (lane == 0) dst[1 + k] = v;
-      });
-  };
-  load_beta(cur);
-  int s = cw;
-  uint32_t n = 0;
-  int64_t next_start = a.poff[cur + 1], row_limit = a.poff[cur] + a.nrows[cur];
-  for (int64_t i = cw; i < n_units; i += nact) {
-    const int64_t tile0 = t0 + i * TPS;
-    const int nt = int(t1 - tile0 < TPS ? t1 - tile0 : TPS);
-    mbar_wait(&sm.full[s], n & 1);
-    const double* xst = reinterpret_cast<const double*>(sm.xs + size_t(s) * stage_pitch);
-    const double* yst = sm.ys + size_t(s) * 32 * TPS;
-    double dep = 0.0;
-    for (int j = 0; j < nt; ++j) {
-      const int64_t row0 = (tile0 + j) * kTileRows;
-      while (row0 >= next_start) {
-        flush(cur);
-        load_beta(++cur);
-        next_start = a.poff[cur + 1];
-        row_limit = a.poff[cur] + a.nrows[cur];
+      for (int k = 0; k < KMAX; ++k) g[k] = 0.0;
+      nll = 0.0;
+    };
+    // partial of group `grp` (this warp's share of segment seg0 + grp - g_first)
+    const int q0 = RowsSwizzle<KMAX>::value ? (lane & 7) : 0;  // chunk swizzle (consume_tile_rows)
+    auto slot = [&](int grp) { return a.part + (size_t(seg0 + grp - g_first) * NCW + cw) * (K + 1); };
+    auto flush = [&](int grp) {
+      double* dst = slot(grp);
+      const double ns = warp_sum(nll);
+      if (lane == 0) dst[0] = ns;
+      if (GRAD)
+        rows_unrotate<KMAX>(g, K, q0, [&](int k, double v) {
+          if (lane == 0) dst[1 + k] = v;
+        });
+    };
+    auto zero_fill = [&](int grp) {  // a segment of the CTA this warp has no rows of
+      double* dst = slot(grp);
+      for (int k = lane; k <= K; k += 32) dst[k] = 0.0;
+    };
+    const int64_t u_first = a.contig ? int64_t(cw) * q + (int64_t(cw) * rr) / nact : cw;
+    const int64_t n_w = a.contig ? int64_t(cw + 1) * q + (int64_t(cw + 1) * rr) / nact - u_first
+                                 : q + (cw < rr ? 1 : 0);
+    const int64_t u_step = a.contig ? 1 : nact;
+    if (n_w <= 0) {
+      for (int grp = g_first; grp <= g_last; ++grp) zero_fill(grp);
+    } else {
+      int cur = group_of_tile_in(a.poff, g_first, g_last, t0 + u_first * TPS);
+      for (int grp = g_first; grp < cur; ++grp) zero_fill(grp);
+      load_beta(cur);
+      int s = cw;
+      uint32_t n = 0;
+      int64_t next_start = a.poff[cur + 1], row_limit = a.poff[cur] + a.nrows[cur];
+      for (int64_t m = 0; m < n_w; ++m) {
+        const int64_t u = u_first + m * u_step;
+        const int64_t tile0 = t0 + u * TPS;
+        const int nt = int(t1 - tile0 < TPS ? t1 - tile0 : TPS);
+        mbar_wait(&sm.full[s], n & 1);
+        const double* xst = reinterpret_cast<const double*>(sm.xs + size_t(s) * stage_pitch);
+        const double* yst = sm.ys + size_t(s) * 32 * TPS;
+        double dep = 0.0;
+        for (int j = 0; j < nt; ++j) {
+          const int64_t row0 = (tile0 + j) * kTileRows;
+          while (row0 >= next_start) {
+            flush(cur);
+            load_beta(++cur);
+            next_start = a.poff[cur + 1];
+            row_limit = a.poff[cur] + a.nrows[cur];
+          }
+          consume_tile_rows<KMAX, GRAD>(xst + size_t(j) * kTileRows * K, yst + 32 * j, K, q0, lane, row0,
+                                        row_limit, b, g, nll, dep);
+        }
+        mbar_arrive_after(&sm.empty[s], dep, lane, const_cast<double*>(xst));
+        s += nact;
+        if (s >= nact * spw) {
+          s = cw;
+          ++n;
+        }
       }
-      consume_tile_rows<KMAX, GRAD>(xst + size_t(j) * kTileRows * K, yst + 32 * j, K, q0, lane, row0, row_limit, b,
-                                    g, nll, dep);
-    }
-    mbar_arrive_after(&sm.empty[s], dep, lane, const_cast<double*>(xst));
-    s += nact;
-    if (s >= Se) {
-      s = cw;
-      ++n;
+      flush(cur);
+      for (int grp = cur + 1; grp <= g_last; ++grp) zero_fill(grp);  // segments after this warp's rows
     }
   }
-  flush(cur);
-  while (cur < g_last) {  // segments after this warp's last tile: zero partials
-    load_beta(++cur);
-    flush(cur);
+  if (!a.fused) return;
+  // Fused fold: one acq_rel ticket per group this CTA touched (thread i takes groups
+  // g_first + i, ...; the CTA barrier before it orders every warp's partial stores, PTX
+  // fences being cumulative); the CTA that completes a group (count = its segments, one per
+  // CTA overlapping it) folds it, warp per group, in hb_fold_kernel's order.  Replaces the
+  // second launch.  The list of groups to fold reuses the (drained) stage memory.
+  int* list = reinterpret_cast<int*>(sm.xs);  // <= blockDim.x entries per chunk
+  int* nlist = list + blockDim.x;
+  for (int gc = g_first; gc <= g_last; gc += blockDim.x) {
+    __syncthreads();  // partial stores done (first chunk) / previous chunk's list consumed
+    if (threadIdx.x == 0) *nlist = 0;
+    __syncthreads();
+    const int grp = gc + threadIdx.x;
+    if (grp <= g_last) {
+      const unsigned need = unsigned(a.gseg[grp + 1] - a.gseg[grp]);
+      unsigned t;
+      asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(a.gcount + grp) : "memory");
+      if (t + 1 == need) {
+        a.gcount[grp] = 0u;  // re-arm for the next launch (kernel boundary orders it)
+        list[atomicAdd(nlist, 1)] = grp;
+      }
+    }
+    __syncthreads();
+    const int nl = *nlist;
+    for (int i = warp; i < nl; i += blockDim.x >> 5)
+      hb_fold_group<GRAD, true>(a.part, a.gseg, NCW, K, a.betas, a.mu, a.sigma, a.out_f, a.out_g, list[i], lane,
+                                32);
   }
 }
 
@@ -549,32 +680,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) glm_rows_kernel(GlmArgs a, 
 template <bool GRAD>
 __global__ void hb_fold_kernel(const double* part, const int* gseg, int nw, int K, const double* betas,
                                const double* mu, const double* sigma, double* out_f, double* out_g) {
-  const int grp = blockIdx.x;
-  const int s0 = gseg[grp], s1 = gseg[grp + 1];
-  for (int c = threadIdx.x; c <= K; c += blockDim.x) {
-    if (c > 0 && !GRAD) break;
-    double acc = 0.0;
-    for (int s = s0; s < s1; ++s)
-      for (int w = 0; w < nw; ++w) acc += part[(size_t(s) * nw + w) * (K + 1) + c];
-    if (c == 0) {
-      double f = -acc;
-      if (mu) {
-        for (int k = 0; k < K; ++k) {
-          const double z = (betas[size_t(grp) * K + k] - mu[k]) / sigma[k];
-          f += -0.5 * z * z;
-        }
-      }
-      out_f[grp] = f;
-    } else {
-      const int k = c - 1;
-      double gk = acc;
-      if (mu) {
-        const double sg = sigma[k];
-        gk -= (betas[size_t(grp) * K + k] - mu[k]) / (sg * sg);
-      }
-      out_g[size_t(grp) * K + k] = gk;
-    }
-  }
+  hb_fold_group<GRAD, false>(part, gseg, nw, K, betas, mu, sigma, out_f, out_g, blockIdx.x, threadIdx.x, blockDim.x);
 }
 
 }  // namespace pm
