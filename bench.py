@@ -375,7 +375,7 @@ def run_glm(args, cfg):
     dev.set_prior(prior.mu, prior.sigma)  # every rank: the kernel-only timing below adds it
     if dist_mode:
         from paper_1310_1537_b200.dist import DistributedDesign
-        dd = DistributedDesign(data, device=local, x_storage=cfg["x_storage"])
+        dd = DistributedDesign(data, device=local, x_storage=cfg["x_storage"], exchange=args.exchange)
 
         def step_dev(beta):
             return dd.log_posterior_grad_device(beta, prior)
@@ -502,14 +502,22 @@ def run_glm(args, cfg):
                                    f"threads, {geo['stages']} TMA stages, {geo['smem_bytes']} B smem)"},
             "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": 8 * k,
                     "d2h_bytes_per_step": 8 * (k + 1),
-                    "path": ("paper_1310_1537_b200.dist.DistributedDesign.log_posterior_grad (per rank: kernel, "
-                             "NCCL all-gather of the (K+1) partials, ordered fold, (f,g) to host)" if dist_mode else
+                    "path": (("paper_1310_1537_b200.dist.DistributedDesign.log_posterior_grad (per rank: ONE "
+                              "launch -- kernel, peer-memory exchange of the (K+1) partials, ordered fold -- "
+                              "(f,g) to host)" if dd.exchange == "peer" else
+                              "paper_1310_1537_b200.dist.DistributedDesign.log_posterior_grad (per rank: kernel, "
+                              "NCCL all-gather of the (K+1) partials, ordered fold, (f,g) to host)") if dist_mode else
                              "paper_1310_1537_b200.glm.log_posterior_grad (C-ABI pm_glm_launch/wait; beta in "
                              "kernel params, (f,g) written to mapped pinned host memory)")},
-            "gpu_launches": steps * (2 if dist_mode else 1),   # + the fold launch per step (NCCL not counted)
+            # + the fold launch per step on the NCCL path (NCCL's own kernels not counted)
+            "gpu_launches": steps * (2 if dist_mode and dd.exchange == "nccl" else 1),
             "clocks": clk,
         }
-        if dist_mode:
+        if dist_mode and dd.exchange == "peer":
+            line["config"]["collective"] = ("peer-memory exchange inside the evaluation kernel: the finishing CTA "
+                                            "stores the K+1 partial into every rank's mailbox (CUDA IPC, "
+                                            "NVLink/NVSwitch), flag + wait, rank-ordered fold (no NCCL call)")
+        elif dist_mode:
             line["config"]["collective"] = "NCCL all_gather_into_tensor of K+1 doubles + pm_fold_rows per step"
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(cfg, n_full)
@@ -860,6 +868,8 @@ def main():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--config", default="c1", choices=sorted(CONFIGS))
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--exchange", default="auto", choices=["auto", "peer", "nccl"],
+                   help="GLM rank path: peer-memory exchange in the kernel (auto: N>1) or NCCL all-gather")
     p.add_argument("--force-dist", action="store_true",
                    help="GLM configs: use the per-rank NCCL path even at N=1 (a 1-rank group)")
     # internal: CPU baseline subprocess

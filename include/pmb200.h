@@ -103,6 +103,27 @@ PM_API int pm_glm_wait(pm_glm_t h, double* f_out, double* g_out);
  * handle's prior terms in the kernel (exactly one rank does, so the fold holds it once). */
 PM_API int pm_glm_eval_device(pm_glm_t h, const double* beta, int with_prior, int want_grad, double* dev_out,
                        void* stream);
+/* Peer-memory exchange for row-sharded evaluations (one process per GPU, one NVLink/NVSwitch
+ * node).  Replaces dist.py's NCCL all-gather + pm_fold_rows (the reference's ascending-worker
+ * merge of per-worker partials, glm.py:243-250 / _grad_sharded 439-454) by ONE kernel launch:
+ * the finishing CTA of every rank stores its (K+1) partial into all ranks' mailboxes (P2P),
+ * raises its flag there, waits for every rank's flag and folds in ascending rank order, so
+ * dev_out holds the world total with identical bits on every rank.  Setup: each rank creates
+ * its mailbox, exports pm_xchg_ipc_handle (64 bytes), and opens every peer's handle with
+ * pm_xchg_open_peer.  All ranks must call pm_glm_eval_xchg the same number of times (SPMD).
+ * A rank missing for ~10 s ends the wait with NaN results and pm_xchg_status() = 1. */
+typedef struct pm_xchg_s* pm_xchg_t;
+PM_API int pm_xchg_create(int device, int32_t world, int32_t rank, int32_t width, pm_xchg_t* out);
+PM_API int pm_xchg_ipc_handle(pm_xchg_t x, void* handle_out /* 64 bytes */);
+PM_API int pm_xchg_open_peer(pm_xchg_t x, int32_t peer, const void* handle /* 64 bytes */);
+/* Same-process peers (one process driving several GPUs with peer access, or tests): the
+ * local mailbox address, and a peer's mailbox address used directly instead of an IPC map. */
+PM_API int pm_xchg_mailbox(pm_xchg_t x, void** ptr);
+PM_API int pm_xchg_set_peer_ptr(pm_xchg_t x, int32_t peer, void* mailbox);
+PM_API int pm_xchg_status(pm_xchg_t x, int32_t* timed_out);
+PM_API int pm_xchg_destroy(pm_xchg_t x);
+PM_API int pm_glm_eval_xchg(pm_glm_t h, const double* beta, int with_prior, pm_xchg_t x, double* dev_out,
+                            void* stream);
 /* out[c] = in[0][c] + in[1][c] + ... + in[world-1][c] in ascending row order (the reference's
  * ascending-worker merge, glm.py:243-250), c < width; device pointers, one launch on `stream`
  * (NULL = the legacy default stream).  Bitwise identical on every rank given the same input. */

@@ -52,6 +52,14 @@ SIGNATURES = {
     "pm_glm_wait": (c_int, [c_void_p, _dp, _dp]),
     "pm_glm_eval_device": (c_int, [c_void_p, _dp, c_int, c_int, c_void_p, c_void_p]),
     "pm_fold_rows": (c_int, [c_void_p, c_int32, c_int32, c_void_p, c_void_p]),
+    "pm_xchg_create": (c_int, [c_int, c_int32, c_int32, c_int32, POINTER(c_void_p)]),
+    "pm_xchg_ipc_handle": (c_int, [c_void_p, c_void_p]),
+    "pm_xchg_open_peer": (c_int, [c_void_p, c_int32, c_void_p]),
+    "pm_xchg_mailbox": (c_int, [c_void_p, POINTER(c_void_p)]),
+    "pm_xchg_set_peer_ptr": (c_int, [c_void_p, c_int32, c_void_p]),
+    "pm_xchg_status": (c_int, [c_void_p, POINTER(c_int32)]),
+    "pm_xchg_destroy": (c_int, [c_void_p]),
+    "pm_glm_eval_xchg": (c_int, [c_void_p, _dp, c_int, c_void_p, c_void_p, c_void_p]),
     "pm_glm_time_launches": (c_int, [c_void_p, _dp, c_int32, c_int, c_int, POINTER(ctypes.c_float)]),
     "pm_glm_stream": (c_int, [c_void_p, POINTER(c_void_p)]),
     "pm_glm_geometry": (c_int, [c_void_p, _ip, _ip, _ip, POINTER(c_size_t), _ip]),

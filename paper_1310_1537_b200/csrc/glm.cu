@@ -372,6 +372,11 @@ GlmArgs make_args(pm_glm_s* h, bool with_prior, double* out) {
   a.counter = h->counter;
   a.out = out;
   a.beta_dev = h->beta_dev;
+  a.xw = 0;  // no peer exchange (pm_glm_eval_xchg sets these)
+  a.xrank = 0;
+  a.xepoch = 0;
+  for (int p = 0; p < kMaxXchgRanks; ++p) a.xpeer[p] = nullptr;
+  a.xstatus = nullptr;
   return a;
 }
 
@@ -382,8 +387,23 @@ int check_beta(pm_glm_s* h, const double* beta) {
 }
 
 // enqueue one evaluation writing (f, g) to `out` on stream `st` (caller holds the mutex)
-int enqueue_eval(pm_glm_s* h, const double* beta, bool with_prior, bool grad, double* out, cudaStream_t st) {
+struct XchgLaunch {  // peer exchange fields of one evaluation (pm_glm_eval_xchg)
+  int world = 0, rank = 0;
+  unsigned long long epoch = 0;
+  double* peer[kMaxXchgRanks] = {};
+  unsigned* status = nullptr;
+};
+
+int enqueue_eval(pm_glm_s* h, const double* beta, bool with_prior, bool grad, double* out, cudaStream_t st,
+                 const XchgLaunch* xl = nullptr) {
   GlmArgs a = make_args(h, with_prior, out);
+  if (xl) {
+    a.xw = xl->world;
+    a.xrank = xl->rank;
+    a.xepoch = xl->epoch;
+    for (int p = 0; p < kMaxXchgRanks; ++p) a.xpeer[p] = xl->peer[p];
+    a.xstatus = xl->status;
+  }
   cudaError_t e;
   // the fp32-X stream kernel widens X by integer ops to x * 2^-896 and scales beta by 2^896
   // (glm_kernels.cuh ld_x_scaled); a beta that large would overflow, so it takes the wide
@@ -582,6 +602,142 @@ int pm_glm_eval(pm_glm_t h, const double* beta, int with_prior, int want_grad, d
   int rc = pm_glm_launch(h, beta, with_prior, want_grad);
   if (rc) return rc;
   return pm_glm_wait(h, f_out, g_out);
+}
+
+// ---- peer-memory exchange of row-sharded ranks (replaces NCCL all-gather + fold) ----
+struct pm_xchg_s {
+  int device = 0, world = 0, rank = 0, width = 0;
+  char* mailbox = nullptr;          // local, cudaMalloc'd, IPC-exported
+  double* peer[kMaxXchgRanks] = {};  // every rank's mailbox in this process (self = mailbox)
+  bool opened[kMaxXchgRanks] = {};   // IPC mappings to close
+  unsigned* status = nullptr;       // device u32: 1 after a wait timeout
+  unsigned long long epoch = 0;
+  std::mutex mu;
+};
+
+int pm_xchg_create(int device, int32_t world, int32_t rank, int32_t width, pm_xchg_t* out) {
+  if (!out) return fail(PM_EINVAL, "null output");
+  if (world < 1 || world > kMaxXchgRanks) return fail(PM_EINVAL, "world must be in 1..16");
+  if (rank < 0 || rank >= world) return fail(PM_ERANGE, "rank out of range");
+  if (width < 1) return fail(PM_EINVAL, "width must be >= 1");
+  DeviceGuard g(device);
+  pm_xchg_s* x = new pm_xchg_s();
+  x->device = device;
+  x->world = world;
+  x->rank = rank;
+  x->width = width;
+  const size_t bytes = xchg_bytes(world, width);
+  cudaError_t e = cudaMalloc(&x->mailbox, bytes);
+  if (e == cudaSuccess) e = cudaMemset(x->mailbox, 0, bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&x->status, sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemset(x->status, 0, sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    if (x->mailbox) cudaFree(x->mailbox);
+    if (x->status) cudaFree(x->status);
+    delete x;
+    return cuda_fail(e, "pm_xchg_create");
+  }
+  x->peer[rank] = reinterpret_cast<double*>(x->mailbox);
+  *out = x;
+  return PM_OK;
+}
+
+int pm_xchg_ipc_handle(pm_xchg_t x, void* handle_out) {
+  if (!x || !handle_out) return fail(PM_EINVAL, "null argument");
+  DeviceGuard g(x->device);
+  cudaIpcMemHandle_t hd;
+  PM_CUDA(cudaIpcGetMemHandle(&hd, x->mailbox));
+  std::memcpy(handle_out, &hd, sizeof(hd));
+  return PM_OK;
+}
+
+int pm_xchg_open_peer(pm_xchg_t x, int32_t peer, const void* handle) {
+  if (!x || !handle) return fail(PM_EINVAL, "null argument");
+  if (peer < 0 || peer >= x->world) return fail(PM_ERANGE, "peer out of range");
+  if (peer == x->rank) return PM_OK;
+  std::lock_guard<std::mutex> lk(x->mu);
+  if (x->opened[peer]) return fail(PM_ESTATE, "peer already opened");
+  DeviceGuard g(x->device);
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle, sizeof(hd));
+  void* p = nullptr;
+  PM_CUDA(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
+  x->peer[peer] = static_cast<double*>(p);
+  x->opened[peer] = true;
+  return PM_OK;
+}
+
+int pm_xchg_mailbox(pm_xchg_t x, void** ptr) {
+  if (!x || !ptr) return fail(PM_EINVAL, "null argument");
+  *ptr = x->mailbox;
+  return PM_OK;
+}
+
+int pm_xchg_set_peer_ptr(pm_xchg_t x, int32_t peer, void* mailbox) {
+  if (!x || !mailbox) return fail(PM_EINVAL, "null argument");
+  if (peer < 0 || peer >= x->world) return fail(PM_ERANGE, "peer out of range");
+  std::lock_guard<std::mutex> lk(x->mu);
+  if (x->opened[peer]) return fail(PM_ESTATE, "peer was opened through IPC");
+  x->peer[peer] = static_cast<double*>(mailbox);
+  return PM_OK;
+}
+
+int pm_xchg_status(pm_xchg_t x, int32_t* timed_out) {
+  if (!x || !timed_out) return fail(PM_EINVAL, "null argument");
+  DeviceGuard g(x->device);
+  unsigned v = 0;
+  PM_CUDA(cudaMemcpy(&v, x->status, sizeof(v), cudaMemcpyDeviceToHost));
+  *timed_out = int(v);
+  return PM_OK;
+}
+
+int pm_xchg_destroy(pm_xchg_t x) {
+  if (!x) return PM_OK;
+  {
+    DeviceGuard g(x->device);
+    cudaDeviceSynchronize();
+    for (int p = 0; p < x->world; ++p)
+      if (x->opened[p]) cudaIpcCloseMemHandle(x->peer[p]);
+    if (x->mailbox) cudaFree(x->mailbox);
+    if (x->status) cudaFree(x->status);
+  }
+  delete x;
+  return PM_OK;
+}
+
+int pm_glm_eval_xchg(pm_glm_t h, const double* beta, int with_prior, pm_xchg_t x, double* dev_out, void* stream) {
+  if (!h || !x) return fail(PM_EINVAL, "null handle");
+  if (!dev_out) return fail(PM_EINVAL, "dev_out is null");
+  std::lock_guard<std::mutex> lk(h->mu);
+  std::lock_guard<std::mutex> lx(x->mu);
+  if (h->K == 0) return fail(PM_ESTATE, "no data uploaded");
+  if (x->width != h->K + 1) return fail(PM_EINVAL, "exchange width must be n_cols + 1");
+  if (x->device != h->device) return fail(PM_EINVAL, "exchange and design on different devices");
+  for (int p = 0; p < x->world; ++p)
+    if (!x->peer[p]) return fail(PM_ESTATE, "peer mailbox not opened (pm_xchg_open_peer)");
+  int rc = check_beta(h, beta);
+  if (rc) return rc;
+  if (with_prior && !h->has_prior) return fail(PM_ESTATE, "no prior set (pm_glm_set_prior)");
+  DeviceGuard g(h->device);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+  if (st != h->stream) {
+    PM_CUDA(cudaEventRecord(h->ev_a, h->stream));
+    PM_CUDA(cudaStreamWaitEvent(st, h->ev_a, 0));
+  }
+  XchgLaunch xl;
+  xl.world = x->world;
+  xl.rank = x->rank;
+  xl.epoch = ++x->epoch;
+  for (int p = 0; p < x->world; ++p) xl.peer[p] = x->peer[p];
+  xl.status = x->status;
+  rc = enqueue_eval(h, beta, with_prior != 0, true, dev_out, st, &xl);
+  if (rc) return rc;
+  if (st != h->stream) {
+    PM_CUDA(cudaEventRecord(h->ev_b, st));
+    PM_CUDA(cudaStreamWaitEvent(h->stream, h->ev_b, 0));
+  }
+  return PM_OK;
 }
 
 int pm_glm_eval_device(pm_glm_t h, const double* beta, int with_prior, int want_grad, double* dev_out,

@@ -545,6 +545,19 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
   }
 }
 
+constexpr int kMaxXchgRanks = 16;
+
+// Mailbox of the peer exchange (one per rank, device memory, IPC-shared):
+//   data  [2][world][width] doubles (double-buffered by epoch parity: a rank can be at most one
+//         evaluation ahead of the slowest reader, see pm_glm_eval_xchg)
+//   flags [world] u64 = latest epoch rank r deposited here
+__host__ __device__ inline size_t xchg_flags_offset(int world, int width) {
+  return (size_t(2) * world * width * sizeof(double) + 127) / 128 * 128;
+}
+__host__ __device__ inline size_t xchg_bytes(int world, int width) {
+  return xchg_flags_offset(world, width) + size_t(world) * sizeof(unsigned long long);
+}
+
 struct GlmArgs {
   const void* X;
   const double* y;
@@ -560,7 +573,66 @@ struct GlmArgs {
   unsigned int* counter;      // zero between launches
   double* out;                // [K+1]  (f, g)
   const double* beta_dev;     // wide kernel only
+  // peer-memory exchange of row-sharded ranks (xw > 0; pm_glm_eval_xchg): the finishing CTA
+  // deposits this rank's (K+1) partial into every rank's mailbox over NVLink, raises its flag
+  // there, waits for all ranks' flags in its own mailbox and folds in ascending rank order
+  int xw, xrank;
+  unsigned long long xepoch;  // >= 1, +1 per evaluation, identical on every rank
+  double* xpeer[kMaxXchgRanks];  // mailbox base of every rank, mapped into this process
+  unsigned* xstatus;          // local: set to 1 on a wait timeout
 };
+
+// Peer exchange, second half (the finishing CTA only): publish this rank's deposits, wait for
+// every rank's, fold them in ascending rank order (dist.ordered_sum / pm_fold_rows: identical
+// bits on every rank).  Thread 0: one system-scope fence after the CTA barrier covers every
+// thread's P2P stores (PTX fences are cumulative over writes ordered before them by
+// bar.sync), then a release store of the epoch into each rank's flag slot; the acquire loads
+// of the local flags order the peers' deposits before the fold's reads.  A rank that never
+// arrives (dead peer) ends the wait after ~10 s with *xstatus = 1 and NaN results, instead of
+// hanging the GPU.
+// `flag`: a free shared int (the finisher's last-CTA flag; the kernels reserve all dynamic
+// shared memory, so no static __shared__ here)
+__device__ inline void xchg_finish(const GlmArgs& a, int ncols, int* flag) {
+  const int width = a.K + 1;
+  volatile int& timed_out = *flag;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    timed_out = 0;
+    asm volatile("fence.sc.sys;" ::: "memory");
+    const size_t fo = xchg_flags_offset(a.xw, width);
+    for (int p = 0; p < a.xw; ++p) {
+      unsigned long long* f = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(a.xpeer[p]) + fo) + a.xrank;
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(a.xepoch) : "memory");
+    }
+    const unsigned long long* mine =
+        reinterpret_cast<const unsigned long long*>(reinterpret_cast<const char*>(a.xpeer[a.xrank]) + fo);
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int r = 0; r < a.xw; ++r) {
+      while (true) {
+        unsigned long long e;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(e) : "l"(mine + r) : "memory");
+        if (e >= a.xepoch) break;
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > 10000000000ull) {
+          timed_out = 1;
+          *a.xstatus = 1u;
+          break;
+        }
+        __nanosleep(64);
+      }
+      if (timed_out) break;
+    }
+  }
+  __syncthreads();
+  const double* data = a.xpeer[a.xrank] + size_t(a.xepoch & 1) * a.xw * width;
+  for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
+    double acc = __ldcv(data + c);
+    for (int r = 1; r < a.xw; ++r) acc += __ldcv(data + size_t(r) * width + c);
+    a.out[c] = timed_out ? __longlong_as_double(0x7ff8000000000000ll) : acc;
+  }
+}
 
 // Deterministic cross-CTA finish: CTA partial -> partials[blockIdx]; the last CTA to
 // arrive sums all partials in ascending CTA order (the reference's ascending-worker merge,
@@ -626,24 +698,30 @@ __device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& s
       if (c >= ncols) break;
       const double tot = warp_sum(part[u]);
       if (lane != 0) continue;
+      double v;
       if (c == 0) {
-        double f = tot;  // partials already hold -sum(nll) = L
+        v = tot;  // partials already hold -sum(nll) = L
         if (a.with_prior) {
-          for (int k = 0; k < K; ++k) f += sm.wg[k];  // prior terms, ascending k
+          for (int k = 0; k < K; ++k) v += sm.wg[k];  // prior terms, ascending k
         }
-        a.out[0] = f;
       } else {
         const int k = c - 1;
-        double gk = tot;
+        v = tot;
         if (a.with_prior) {
           const double sg = a.prior_sigma[k];
-          gk -= (sm.sbeta[k] - a.prior_mu[k]) / (sg * sg);
+          v -= (sm.sbeta[k] - a.prior_mu[k]) / (sg * sg);
         }
-        a.out[c] = gk;
+      }
+      if (a.xw == 0) {
+        a.out[c] = v;
+      } else {  // deposit into slot [parity][xrank] of every rank's mailbox (P2P stores)
+        const size_t o = (size_t(a.xepoch & 1) * a.xw + a.xrank) * size_t(K + 1) + c;
+        for (int p = 0; p < a.xw; ++p) a.xpeer[p][o] = v;
       }
     }
   }
   if (tid == 0) *a.counter = 0u;  // re-arm for the next launch (kernel boundary orders it)
+  if (a.xw > 0) xchg_finish(a, ncols, sm.flag);
 }
 
 // K1 + K2: persistent fused single-pass kernel, one CTA per SM.

@@ -23,7 +23,7 @@ import numpy as np
 from .glm import DesignMatrix, GradResult, _check_beta
 from .parallel import partition
 
-__all__ = ["shard_bounds", "ordered_sum", "gather_partials", "DistributedDesign",
+__all__ = ["shard_bounds", "ordered_sum", "gather_partials", "PeerExchange", "DistributedDesign",
            "strip_bounds", "exchange_halos", "LatticeStrip", "strip_sweeps"]
 
 
@@ -70,12 +70,91 @@ def gather_partials(part, group=None):
     return ordered_sum(torch.stack(parts))
 
 
+class PeerExchange:
+    """Mailboxes of the peer-memory exchange (pm_xchg_*): every rank's (K+1) partial goes
+    straight into all ranks' device memory from the finishing CTA of its own evaluation
+    kernel (P2P stores over NVLink/NVSwitch, CUDA IPC mappings), so one evaluation is ONE
+    launch with no NCCL call and no fold launch.  Built collectively; `ok` is False on every
+    rank if any rank could not map a peer (then the NCCL path is used)."""
+
+    def __init__(self, device: int, width: int, group=None):
+        import torch.distributed as dist
+
+        from . import _lib
+        _lib = _lib_override or _lib  # tests stand in for the library on CPU
+        self._lib = _lib
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self._h = None
+        err = ""
+        try:
+            h = ctypes.c_void_p()
+            _lib.check(_lib.load().pm_xchg_create(device, self.world, self.rank, width, ctypes.byref(h)),
+                       "pm_xchg_create")
+            self._h = h
+            buf = ctypes.create_string_buffer(64)
+            _lib.call("pm_xchg_ipc_handle", h, ctypes.cast(buf, ctypes.c_void_p))
+            mine = bytes(buf.raw)
+        except Exception as e:  # noqa: BLE001 - any failure means: use NCCL on every rank
+            mine, err = b"", str(e)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, (mine, _hostname()), group=group)
+        ok = all(hd[0] for hd in handles) and len({hd[1] for hd in handles}) == 1
+        if ok:
+            try:
+                for p, (hd, _) in enumerate(handles):
+                    if p != self.rank:
+                        _lib.call("pm_xchg_open_peer", self._h, p, ctypes.cast(ctypes.c_char_p(hd), ctypes.c_void_p))
+            except Exception as e:  # noqa: BLE001
+                ok, err = False, str(e)
+        flags = [None] * self.world
+        dist.all_gather_object(flags, ok, group=group)
+        self.ok = all(flags)
+        self.error = err
+        if not self.ok:
+            self.close()
+
+    def eval(self, dev, beta, with_prior: bool, out_ptr: int, stream: int) -> None:
+        self._lib.call("pm_glm_eval_xchg", dev.handle, self._lib.dptr(beta), int(with_prior), self._h,
+                       ctypes.c_void_p(out_ptr), ctypes.c_void_p(stream))
+
+    def timed_out(self) -> bool:
+        v = ctypes.c_int32()
+        self._lib.call("pm_xchg_status", self._h, ctypes.byref(v))
+        return bool(v.value)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._lib.load().pm_xchg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_lib_override = None
+
+
+def _hostname() -> str:
+    import socket
+    return socket.gethostname()
+
+
 class DistributedDesign:
-    """This rank's row shard on its GPU: one kernel, one NCCL all-gather and one fold launch
-    per evaluation.  Rank 0's kernel adds the prior terms (the same device finaliser as the
+    """This rank's row shard on its GPU.  One evaluation is one kernel launch whose finishing
+    CTA exchanges the (K+1) partials with the other ranks through peer memory and folds them
+    in ascending rank order (PeerExchange, NCCL backend, world > 1); otherwise (gloo, world 1,
+    PM_DIST_XCHG=0, or a node without peer mappings) one kernel, one NCCL all-gather and one
+    fold launch.  Rank 0's kernel adds the prior terms (the same device finaliser as the
     single-GPU path), so the rank-ordered fold holds them exactly once."""
 
-    def __init__(self, local: DesignMatrix, device: int, x_storage: str = "f64", group=None):
+    def __init__(self, local: DesignMatrix, device: int, x_storage: str = "f64", group=None,
+                 exchange: str = "auto"):
+        import os
+
         import torch
         import torch.distributed as dist
         self.local = local
@@ -85,6 +164,20 @@ class DistributedDesign:
         self.dev = local.on_device(device, x_storage)
         self.k = local.n_cols
         self._buf = torch.empty(self.k + 1, dtype=torch.float64, device=f"cuda:{device}")
+        self._out = torch.empty(self.k + 1, dtype=torch.float64, device=f"cuda:{device}")
+        self.xchg = None
+        # "auto": peer exchange for NCCL groups of > 1 rank; "peer": also for a 1-rank group
+        # (exercises the exchange kernel on one GPU); "nccl" / PM_DIST_XCHG=0: NCCL all-gather
+        want = exchange if exchange != "auto" else os.environ.get("PM_DIST_XCHG", "auto")
+        want = {"1": "auto", "0": "nccl"}.get(want, want)
+        if (want in ("auto", "peer") and dist.is_initialized() and dist.get_backend(group) == "nccl"
+                and (dist.get_world_size(group) > 1 or want == "peer")):
+            x = PeerExchange(device, self.k + 1, group)
+            self.xchg = x if x.ok else None
+
+    @property
+    def exchange(self) -> str:
+        return "peer" if self.xchg is not None else "nccl"
 
     def _partial(self, beta: np.ndarray, prior=None):
         stream = torch_stream_handle(self.device)
@@ -97,10 +190,18 @@ class DistributedDesign:
     def log_posterior_grad_device(self, beta, prior=None):
         """(f, g) as a device tensor of K+1 doubles, identical on every rank."""
         beta = _check_beta(beta, self.k)
+        if self.xchg is not None:
+            with_prior = prior is not None and self.rank == 0
+            if with_prior:
+                self.dev.set_prior(prior.mu, prior.sigma)
+            self.xchg.eval(self.dev, beta, with_prior, self._out.data_ptr(), torch_stream_handle(self.device))
+            return self._out
         return gather_partials(self._partial(beta, prior), self.group)
 
     def log_posterior_grad(self, beta, prior=None) -> GradResult:
         out = self.log_posterior_grad_device(beta, prior).cpu().numpy()
+        if self.xchg is not None and self.xchg.timed_out():
+            raise RuntimeError("peer exchange timed out: a rank did not take part in the evaluation")
         return GradResult(float(out[0]), out[1:].copy())
 
 

@@ -143,3 +143,73 @@ def test_strip_halo_exchange_matches_full_lattice(world):
     got = np.concatenate([r[2] for r in res], axis=0)
     ref = go.ising_sweeps(ising_spins(*shape, seed=4), None, 0.8814, True, sweeps, go.RNG_PHILOX4X32, seed, 0, 0)
     np.testing.assert_array_equal(got, ref)
+
+
+def _xchg_worker(rank, world, port, q, fail_rank):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1310_1537_b200 import dist as pdist
+
+        class FakeLib:
+            """Stands in for libpmb200's pm_xchg_* on CPU: handles are 64 bytes naming the
+            rank; rank `fail_rank` fails to map its peers."""
+
+            def __init__(self):
+                self.opened, self.destroyed = [], 0
+
+            def load(self):
+                return self
+
+            def check(self, rc, what=""):
+                if rc:
+                    raise RuntimeError(what)
+
+            def pm_xchg_create(self, device, world_, rank_, width, out):
+                out._obj.value = 1000 + rank_
+                return 0
+
+            def pm_xchg_destroy(self, h):
+                self.destroyed += 1
+                return 0
+
+            def call(self, name, *args):
+                if name == "pm_xchg_ipc_handle":
+                    import ctypes
+                    ctypes.memmove(args[1], f"rank{rank}".encode().ljust(64, b"\0"), 64)
+                elif name == "pm_xchg_open_peer":
+                    import ctypes
+                    if rank == fail_rank:
+                        raise RuntimeError("cudaIpcOpenMemHandle: peer access unsupported")
+                    self.opened.append((args[1], ctypes.string_at(args[2], 5)))
+
+        fake = FakeLib()
+        pdist._lib_override = fake
+        x = pdist.PeerExchange(0, 5)
+        q.put((rank, x.ok, sorted(fake.opened), fake.destroyed))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank", [-1, 1])
+def test_peer_exchange_setup_agrees_across_ranks(fail_rank):
+    """PeerExchange's collective setup (gloo, world 3, libpmb200 stood in for on CPU): every
+    rank opens every other rank's handle; if any rank cannot map a peer, ALL ranks report
+    ok = False and release their mailbox (so every rank falls back to the NCCL path)."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_xchg_worker, args=(r, world, port, q, fail_rank)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok, opened, destroyed in res:
+        assert ok == (fail_rank < 0)
+        if rank != fail_rank:
+            assert opened == [(p, f"rank{p}".encode()) for p in range(world) if p != rank]
+        assert destroyed == (0 if ok else 1)

@@ -103,3 +103,114 @@ def test_nccl_single_rank_back_to_back_and_strip(gpu):
         strip.close()
     finally:
         dist.destroy_process_group()
+
+
+def _xchg(device, world, rank, width):
+    import ctypes
+
+    from paper_1310_1537_b200 import _lib
+    h = ctypes.c_void_p()
+    _lib.check(_lib.load().pm_xchg_create(device, world, rank, width, ctypes.byref(h)), "pm_xchg_create")
+    return h
+
+
+def _mailbox(h):
+    import ctypes
+
+    from paper_1310_1537_b200 import _lib
+    p = ctypes.c_void_p()
+    _lib.call("pm_xchg_mailbox", h, ctypes.byref(p))
+    return p.value
+
+
+def test_peer_exchange_single_rank_matches_single_gpu_path(gpu):
+    """pm_glm_eval_xchg with world 1: the finishing CTA deposits into its own mailbox, raises
+    its flag, waits and folds -- bit-identical to the plain evaluation, over many epochs
+    (both mailbox parities), with and without the prior."""
+    import ctypes
+
+    import torch
+    from paper_1310_1537_b200 import _lib
+    gen = np.random.default_rng(8)
+    n, k = 70_001, 100
+    x = gen.standard_normal((n, k))
+    y = (gen.random(n) < 0.5).astype(float)
+    d = DesignMatrix(x, y)
+    dev = d.on_device(0)
+    prior = GaussianPrior(gen.normal(0, 0.5, k), np.full(k, 2.0))
+    dev.set_prior(prior.mu, prior.sigma)
+    xh = _xchg(0, 1, 0, k + 1)
+    out = torch.empty(k + 1, dtype=torch.float64, device="cuda:0")
+    try:
+        for i in range(7):
+            beta = gen.normal(0, 0.2, k)
+            wp = i % 2 == 0
+            if wp:  # the reference evaluations below reset the shared handle's prior
+                dev.set_prior(prior.mu, prior.sigma)
+            _lib.call("pm_glm_eval_xchg", dev.handle, _lib.dptr(beta), int(wp), xh,
+                      ctypes.c_void_p(out.data_ptr()), None)  # the handle's own stream
+            torch.cuda.synchronize()
+            got = out.cpu().numpy()
+            ref = glm.log_posterior_grad(d, beta, prior) if wp else glm.loglike_grad(d, beta)
+            assert got[0] == ref.f and np.array_equal(got[1:], ref.g), i
+        st = ctypes.c_int32()
+        _lib.call("pm_xchg_status", xh, ctypes.byref(st))
+        assert st.value == 0
+    finally:
+        _lib.load().pm_xchg_destroy(xh)
+
+
+def test_peer_exchange_two_ranks_one_process(gpu):
+    """Two row shards on one GPU, each with its own design handle and mailbox, exchanging
+    through peer memory (same-process mailbox pointers): the two kernels run on separate
+    streams and only their finishing CTAs wait on each other (one SM each), bounded by the
+    kernel's 10 s timeout.  Both ranks must hold the ascending-rank fold of the two partials,
+    bit-identical to the NCCL path's pm_fold_rows and within 1e-10 of the oracle."""
+    import ctypes
+
+    import torch
+    from paper_1310_1537_b200 import _lib
+    from paper_1310_1537_b200.parallel import partition
+    gen = np.random.default_rng(9)
+    n, k = 300_007, 100
+    x = gen.standard_normal((n, k))
+    y = (gen.random(n) < 0.5).astype(float)
+    prior = GaussianPrior(gen.normal(0, 0.5, k), np.full(k, 2.0))
+    shards = [DesignMatrix(x[a:b], y[a:b]) for a, b in partition(n, 2)]
+    devs = [s.on_device(0) for s in shards]
+    devs[0].set_prior(prior.mu, prior.sigma)
+    xs = [_xchg(0, 2, r, k + 1) for r in range(2)]
+    boxes = [_mailbox(h) for h in xs]
+    for r in range(2):
+        _lib.call("pm_xchg_set_peer_ptr", xs[r], 1 - r, ctypes.c_void_p(boxes[1 - r]))
+    streams = [torch.cuda.Stream(device=0) for _ in range(2)]
+    outs = [torch.empty(k + 1, dtype=torch.float64, device="cuda:0") for _ in range(2)]
+    part = [torch.empty(k + 1, dtype=torch.float64, device="cuda:0") for _ in range(2)]
+    try:
+        for i in range(4):
+            beta = gen.normal(0, 0.2, k)
+            for r in range(2):
+                _lib.call("pm_glm_eval_xchg", devs[r].handle, _lib.dptr(beta), int(r == 0), xs[r],
+                          ctypes.c_void_p(outs[r].data_ptr()), ctypes.c_void_p(streams[r].cuda_stream))
+            torch.cuda.synchronize()
+            a, b = outs[0].cpu().numpy(), outs[1].cpu().numpy()
+            assert np.array_equal(a, b), i
+            # the NCCL path's fold of the same partials
+            for r in range(2):
+                devs[r].eval_device(beta, True, part[r].data_ptr(), 0, with_prior=(r == 0))
+            torch.cuda.synchronize()
+            blk = torch.stack(part)
+            fold = torch.empty(k + 1, dtype=torch.float64, device="cuda:0")
+            _lib.call("pm_fold_rows", blk.data_ptr(), 2, k + 1, fold.data_ptr(), None)
+            torch.cuda.synchronize()
+            assert np.array_equal(a, fold.cpu().numpy()), i
+            f_ref, g_ref = gl.log_posterior_grad(x, y, beta, prior.mu, prior.sigma)
+            assert abs(a[0] - f_ref) / max(abs(f_ref), 1) < 1e-10
+            assert np.max(np.abs(a[1:] - g_ref) / np.maximum(np.abs(g_ref), 1)) < 1e-10
+        for h in xs:
+            st = ctypes.c_int32()
+            _lib.call("pm_xchg_status", h, ctypes.byref(st))
+            assert st.value == 0
+    finally:
+        for h in xs:
+            _lib.load().pm_xchg_destroy(h)
