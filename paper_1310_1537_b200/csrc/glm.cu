@@ -1085,7 +1085,7 @@ struct pm_hb_s {
   // small-K row-per-lane path (even K <= 32): balanced tile ranges + segment fold
   bool rows = false;
   int rows_grid = 0, rows_stages = 0, rows_ncw = 7, rows_tps = 1;
-  int rows_contig = 1, rows_fused = 1;  // PM_HB_CONTIG / PM_HB_FUSED = 0 for A/B
+  int rows_contig = 1, rows_fused = 0, rows_pdl = 1;  // PM_HB_CONTIG / _FUSED / PM_PDL = 0 for A/B
   int* cta_g0 = nullptr;        // [rows_grid] first group of each CTA
   unsigned* gcount = nullptr;   // [G] fused-fold tickets
   size_t rows_smem = 0;
@@ -1155,11 +1155,10 @@ cudaError_t launch_hb_rows_n(const pm_hb_s* h, const HbArgs& a, cudaStream_t st)
   r.sigma = a.sigma;
   r.out_f = a.out_f;
   r.out_g = a.out_g;
-  kern<<<h->rows_grid, (NCW + 1) * 32, h->rows_smem, st>>>(r);
-  e = cudaGetLastError();
+  e = launch_pdl(h->rows_pdl != 0, kern, dim3(h->rows_grid), dim3((NCW + 1) * 32), h->rows_smem, st, r);
   if (e != cudaSuccess || h->rows_fused) return e;
-  hb_fold_kernel<GRAD><<<h->G, 64, 0, st>>>(h->part, h->gseg, NCW, h->K, a.betas, a.mu, a.sigma, a.out_f, a.out_g);
-  return cudaGetLastError();
+  return launch_pdl(h->rows_pdl != 0, hb_fold_kernel<GRAD>, dim3(h->G), dim3(64), 0, st, (const double*)h->part,
+                    (const int*)h->gseg, int(NCW), h->K, a.betas, a.mu, a.sigma, a.out_f, a.out_g);
 }
 
 template <int KMAX, bool GRAD>
@@ -1358,7 +1357,11 @@ int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64_t* off
     const char* e_contig = std::getenv("PM_HB_CONTIG");
     const char* e_fused = std::getenv("PM_HB_FUSED");
     h->rows_contig = (e_contig && e_contig[0] == '0') ? 0 : 1;
-    h->rows_fused = (e_fused && e_fused[0] == '0') ? 0 : 1;
+    // measured (profiles/r01_ab_hb_pdl.txt): with PDL a separate fold launch overlapped with
+    // the next rows kernel beats the fused per-group-ticket fold (68.3 vs 71.2 us)
+    h->rows_fused = (e_fused && e_fused[0] == '1') ? 1 : 0;
+    const char* e_pdl = std::getenv("PM_PDL");
+    h->rows_pdl = (e_pdl && e_pdl[0] == '0') ? 0 : 1;
     h->rows = true;
     h->rows_grid = C;
     h->rows_ncw = ncw;

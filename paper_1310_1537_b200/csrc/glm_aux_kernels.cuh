@@ -479,6 +479,10 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a
       }
     }
   }
+  // PDL: the copies above only read X and y (never written by a kernel); the consumers and
+  // the fold below read beta and write the partials / tickets the previous launch uses
+  if (threadIdx.x == 0) pdl_trigger();
+  if (warp > 0) pdl_wait();
   // the CTA's groups and segments (host-computed; loaded after the producer started)
   const int g_first = a.cta_g0[c];
   const int seg0 = a.seg_base[c];
@@ -555,6 +559,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a
     }
   }
   if (!a.fused) return;
+  pdl_wait();  // (the producer thread: its ticket writes below follow the previous launch)
   // Fused fold: one acq_rel ticket per group this CTA touched (thread i takes groups
   // g_first + i, ...; the CTA barrier before it orders every warp's partial stores, PTX
   // fences being cumulative); the CTA that completes a group (count = its segments, one per
@@ -680,6 +685,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) glm_rows_kernel(GlmArgs a, 
 template <bool GRAD>
 __global__ void hb_fold_kernel(const double* part, const int* gseg, int nw, int K, const double* betas,
                                const double* mu, const double* sigma, double* out_f, double* out_g) {
+  pdl_trigger();  // the next evaluation's rows kernel may start streaming X meanwhile
+  pdl_wait();     // the rows kernel's partials are complete
   hb_fold_group<GRAD, false>(part, gseg, nw, K, betas, mu, sigma, out_f, out_g, blockIdx.x, threadIdx.x, blockDim.x);
 }
 

@@ -15,6 +15,7 @@
 //   W odd  : plain int8 grid [H][W] (colours are the parity of the flat index).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -27,6 +28,11 @@
 using namespace pm;
 
 namespace {
+
+bool pdl_default() {
+  const char* e = std::getenv("PM_PDL");
+  return !(e && e[0] == '0');
+}
 
 constexpr int kPottsIdx = 625;  // n0 + 5 n1 + 25 n2 + 125 n3, n_a in 0..4
 
@@ -205,6 +211,10 @@ __global__ void __launch_bounds__(256, NG == 1 ? 6 : 4)
     for (int t = tid; t < kPottsIdx * 3; t += blockDim.x * blockDim.y) dst[t] = pthr[t];
   }
   __syncthreads();
+  // PDL: the tables above are host-built (memcpy); the lattice is written by the previous
+  // half-sweep, so wait for it here -- the launch and block scheduling overlap its tail
+  pdl_trigger();
+  pdl_wait();
   // 2-D grid of 2-D blocks: x = (16*NG)-site column groups of a row, y = rows
   const int per_row = a.W2 / (16 * NG);
   const int cgrp = blockIdx.x * blockDim.x + threadIdx.x;
@@ -371,6 +381,7 @@ struct pm_lat_s {
   double* cdf = nullptr;
   unsigned long long* pthr = nullptr;
   uint4* pthr32 = nullptr;    // Potts thresholds as (t0, t1, t2, 0) when all < 2^32
+  bool pdl = pdl_default();   // packed half-sweeps launched with PDL (PM_PDL=0 disables)
   bool t32 = false;           // every threshold of the active model fits 32 bits
   // uniforms staging
   double* uni = nullptr;
@@ -623,7 +634,10 @@ static void launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t seed, cud
   const dim3 block(bx, by);
   const dim3 grid((per_row + bx - 1) / bx, std::min((h->H + by - 1) / by, 65535));
   const bool ising = h->model == PM_MODEL_ISING;
-#define PM_LAUNCH_PACKED(M, T, N) gibbs_packed_kernel<M, T, N><<<grid, block, 0, st>>>(pa, h->pthr, h->pthr32)
+  cudaError_t e = cudaSuccess;  // a failed launch is also the thread's last error (callers check it)
+#define PM_LAUNCH_PACKED(M, T, N)                                                                      \
+  e = launch_pdl(h->pdl, gibbs_packed_kernel<M, T, N>, grid, block, 0, st, pa,                        \
+                 (const unsigned long long*)h->pthr, (const uint4*)h->pthr32)
 #define PM_LAUNCH_NG(M, T)            \
   do {                                \
     if (ng == 4)                      \
@@ -639,6 +653,7 @@ static void launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t seed, cud
   else PM_LAUNCH_NG(PM_MODEL_POTTS4, false);
 #undef PM_LAUNCH_NG
 #undef PM_LAUNCH_PACKED
+  (void)e;
 }
 
 int pm_lat_create_strip(int device, int32_t height, int32_t width, int32_t row0, int32_t rows, int model,

@@ -7,6 +7,7 @@
 #include <atomic>
 #include <mutex>
 #include <string>
+#include <utility>
 
 #include "../../include/pmb200.h"
 
@@ -65,6 +66,23 @@ namespace pm {
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device); `mask` is a
 // per-kernel static bitmask of devices already configured.
 cudaError_t ensure_smem_attr(const void* kernel, std::atomic<uint64_t>& mask);
+
+// <<<grid, block, smem, stream>>> with the PDL attribute when `pdl` (see pdl_wait).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------- device PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -160,6 +178,14 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+
+// Programmatic dependent launch (PDL): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while the previous kernel in
+// its stream drains; pdl_wait() blocks until that kernel has completed and its writes are
+// visible (everything before it may only touch data no earlier kernel writes), pdl_trigger()
+// lets the next such kernel be scheduled as this one's CTAs exit.  No-ops without PDL.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ double shfl_d(double v, int src) {
   return __shfl_sync(0xffffffffu, v, src);
