@@ -145,6 +145,17 @@ StreamLaunch pick_stream(int kc) {
 }
 
 template <bool GRAD>
+StreamLaunch pick_stream_pairs_f64(int kc) {  // fp64 X, pairs layout (even kc)
+  switch (kc) {
+    case 2: return launch_stream<double, 2, GRAD, 1>;
+    case 4: return launch_stream<double, 4, GRAD, 1>;
+    case 6: return launch_stream<double, 6, GRAD, 1>;
+    case 8: return launch_stream<double, 8, GRAD, 1>;
+  }
+  return nullptr;
+}
+
+template <bool GRAD>
 StreamLaunch pick_stream_pairs(int kc, int pairs) {  // fp32-X, pairs layouts (even kc)
   if (pairs == 2) {
     if (kc == 2) return launch_stream<float, 2, GRAD, 2>;
@@ -161,6 +172,7 @@ StreamLaunch pick_stream_pairs(int kc, int pairs) {  // fp32-X, pairs layouts (e
 }
 
 StreamLaunch pick_stream_any(int xtype, int kc, bool grad, int pairs) {
+  if (xtype == PM_X_F64 && pairs) return grad ? pick_stream_pairs_f64<true>(kc) : pick_stream_pairs_f64<false>(kc);
   if (xtype == PM_X_F64) return grad ? pick_stream<double, true>(kc) : pick_stream<double, false>(kc);
   if (pairs) return grad ? pick_stream_pairs<true>(kc, pairs) : pick_stream_pairs<false>(kc, pairs);
   return grad ? pick_stream<float, true>(kc) : pick_stream<float, false>(kc);
@@ -324,6 +336,10 @@ int choose_geometry(pm_glm_s* h) {
     h->pairs = 0;
     if (h->kind == KIND_STREAM && h->xtype == PM_X_F32 && h->K % 2 == 0 && kc % 2 == 0 && pmode > 0)
       h->pairs = (pmode == 2 && kc <= 4) ? 2 : 1;
+    // fp64 X: the same pairs layout with 16-byte loads (PM_F64_PAIRS=0 disables for A/B)
+    const char* e64 = std::getenv("PM_F64_PAIRS");
+    if (h->kind == KIND_STREAM && h->xtype == PM_X_F64 && h->K % 2 == 0 && kc % 2 == 0 && !(e64 && e64[0] == '0'))
+      h->pairs = 1;
     // fp32-X, K <= 128: 15 consumer warps, one 32-row stage each (PM_STREAM_NCW=7 disables;
     // measured: 16-row stages, 2 per warp, are 26 % slower -- per-stage overheads dominate)
     const char* e15 = std::getenv("PM_STREAM_NCW");

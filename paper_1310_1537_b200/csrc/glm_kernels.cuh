@@ -14,6 +14,8 @@
 // X is read from HBM exactly once per evaluation.
 #pragma once
 
+#include <type_traits>
+
 #include "pm_internal.cuh"
 #include "pm_math.cuh"
 
@@ -187,8 +189,9 @@ __device__ __forceinline__ void consume_tile(const XT* xs, const double* ys, int
 // the same rows.  Lane l ends with the dot product of row l & (R-1); the residual of the row
 // in slot r lives in lane l ^ r.  Bitwise deterministic for a fixed geometry; the per-row
 // arithmetic (product + sum orders) differs from consume_tile only in the lane summation tree.
-template <int KC, bool GRAD, int R, int TR>
-__device__ __forceinline__ void consume_tile_pairs(const float* xs, const double* ys, int K, int lane, int64_t row0,
+// (fp64 X: the same layout with 16-byte loads of two doubles, no widening.)
+template <typename XT, int KC, bool GRAD, int R, int TR>
+__device__ __forceinline__ void consume_tile_pairs(const XT* xs, const double* ys, int K, int lane, int64_t row0,
                                                    int64_t row_limit, const double (&breg)[KC], double (&g)[KC],
                                                    double& nll_acc, uint64_t* empty, const uint32_t (&roff)[R]) {
   static_assert(KC % 2 == 0, "pairs layout needs an even register count");
@@ -196,13 +199,27 @@ __device__ __forceinline__ void consume_tile_pairs(const float* xs, const double
   const bool last_ok = 64 * (KP - 1) + 2 * lane < K;
 #pragma unroll 1
   for (int sub = 0; sub < TR / R; ++sub) {
-    const char* xb = reinterpret_cast<const char*>(xs) + size_t(sub) * R * K * sizeof(float);
+    const char* xb = reinterpret_cast<const char*>(xs) + size_t(sub) * R * K * sizeof(XT);
     double x[R][KC];
     double v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const uint2* pr = reinterpret_cast<const uint2*>(xb + roff[r]);
       double acc = 0.0;
+      if constexpr (std::is_same<XT, double>::value) {
+        const double2* pr = reinterpret_cast<const double2*>(xb + roff[r]);
+#pragma unroll
+        for (int c = 0; c < KP; ++c) {
+          double2 u = make_double2(0.0, 0.0);
+          if (c < KP - 1 || last_ok) u = pr[32 * c];
+          x[r][2 * c] = u.x;
+          x[r][2 * c + 1] = u.y;
+          acc = fma(x[r][2 * c], breg[2 * c], acc);
+          acc = fma(x[r][2 * c + 1], breg[2 * c + 1], acc);
+        }
+        v[r] = acc;
+        continue;
+      }
+      const uint2* pr = reinterpret_cast<const uint2*>(xb + roff[r]);
 #pragma unroll
       for (int c = 0; c < KP; ++c) {
         uint2 u = make_uint2(0u, 0u);
@@ -210,9 +227,6 @@ __device__ __forceinline__ void consume_tile_pairs(const float* xs, const double
 #if defined(PM_F32_F2F)
         x[r][2 * c] = double(__uint_as_float(u.x));
         x[r][2 * c + 1] = double(__uint_as_float(u.y));
-#elif defined(PM_F32_MIX)  // A/B: one F2F (XU pipe, unscaled) + one integer widening per pair
-        x[r][2 * c] = double(__uint_as_float(u.x));
-        x[r][2 * c + 1] = ld_x_scaled(reinterpret_cast<const float*>(&u.y));
 #else
         x[r][2 * c] = ld_x_scaled(reinterpret_cast<const float*>(&u.x));
         x[r][2 * c + 1] = ld_x_scaled(reinterpret_cast<const float*>(&u.y));
@@ -228,7 +242,7 @@ __device__ __forceinline__ void consume_tile_pairs(const float* xs, const double
       double dep = yv;
 #pragma unroll
       for (int r = 0; r < R; ++r) dep += v[r];
-      mbar_arrive_after(empty, dep, lane, const_cast<float*>(xs));
+      mbar_arrive_after(empty, dep, lane, const_cast<XT*>(xs));
     }
 #pragma unroll
     for (int st = R / 2; st >= 1; st >>= 1) {
@@ -244,9 +258,7 @@ __device__ __forceinline__ void consume_tile_pairs(const float* xs, const double
     nll_acc += (valid && lane < R) ? nll : 0.0;
     if (GRAD) {
       w = valid ? w : 0.0;
-#ifndef PM_F32_MIX
-      w *= XScale<float>::value;  // exact (power of two)
-#endif
+      w *= XScale<XT>::value;  // exact (power of two)
       constexpr int NS = KC >= 8 ? 1 : ((8 / KC) < R ? (8 / KC) : R);
       double ga[NS > 1 ? NS - 1 : 1][KC];
 #pragma unroll
@@ -255,19 +267,13 @@ __device__ __forceinline__ void consume_tile_pairs(const float* xs, const double
         for (int j = 0; j < KC; ++j) ga[s2][j] = 0.0;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const double wr0 = r == 0 ? w : shfl_xor_d(w, r);
-#ifdef PM_F32_MIX
-        const double wr1 = wr0 * XScale<float>::value;  // odd registers hold x * 2^-896
-#else
-        const double wr1 = wr0;
-#endif
+        const double wr = r == 0 ? w : shfl_xor_d(w, r);
         if (r % NS == 0) {
 #pragma unroll
-          for (int j = 0; j < KC; ++j) g[j] = fma((j & 1) ? wr1 : wr0, x[r][j], g[j]);
+          for (int j = 0; j < KC; ++j) g[j] = fma(wr, x[r][j], g[j]);
         } else {
 #pragma unroll
-          for (int j = 0; j < KC; ++j)
-            ga[r % NS - 1][j] = fma((j & 1) ? wr1 : wr0, x[r][j], ga[r % NS - 1][j]);
+          for (int j = 0; j < KC; ++j) ga[r % NS - 1][j] = fma(wr, x[r][j], ga[r % NS - 1][j]);
         }
       }
 #pragma unroll
@@ -524,12 +530,25 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
   for (int64_t i = cw; i < n_mine; i += nact) {
     mbar_wait(&sm.full[s], n & 1);
     const int64_t tile = tile_begin + i * stride;
+#ifdef PM_AB_NO_COMPUTE  // A/B timing experiment only: the TMA pipeline without the consumers' math
+    {
+      const double dep = sm.ys[size_t(s) * TR + lane];
+      nll_acc += dep;
+      mbar_arrive_after(&sm.empty[s], dep, lane, sm.xs + size_t(s) * tile_pitch);
+      s += nact;
+      if (s >= Se) {
+        s = cw;
+        ++n;
+      }
+      continue;
+    }
+#endif
     if constexpr (PAIRS == 2) {
       consume_tile_f32full<KC, GRAD>(reinterpret_cast<const float*>(sm.xs + size_t(s) * tile_pitch),
                                      sm.ys + size_t(s) * TR, K, lane, tile * TR, row_limit, breg, g, nll_acc,
                                      &sm.empty[s], roff);
     } else if constexpr (PAIRS == 1) {
-      consume_tile_pairs<KC, GRAD, R, TR>(reinterpret_cast<const float*>(sm.xs + size_t(s) * tile_pitch),
+      consume_tile_pairs<XT, KC, GRAD, R, TR>(reinterpret_cast<const XT*>(sm.xs + size_t(s) * tile_pitch),
                                           sm.ys + size_t(s) * TR, K, lane, tile * TR, row_limit, breg, g,
                                           nll_acc, &sm.empty[s], roff);
     } else {
@@ -752,12 +771,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
 #pragma unroll
   for (int j = 0; j < KC; ++j) {
     const int c = lane_col<PAIRS != 0>(lane, j);
-#ifdef PM_F32_MIX
-    const double sc = (PAIRS && (j & 1) == 0) ? 1.0 : XScale<XT>::value;
-#else
-    const double sc = XScale<XT>::value;
-#endif
-    breg[j] = (c < K) ? beta.v[c] * sc : 0.0;  // exact (power of two)
+    breg[j] = (c < K) ? beta.v[c] * XScale<XT>::value : 0.0;  // exact (power of two)
     g[j] = 0.0;
   }
   double nll = 0.0;

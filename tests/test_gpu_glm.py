@@ -270,3 +270,25 @@ def test_fp32_widening_edge_values(gpu):
         f, g = gl.loglike_grad(x64, y, beta)
         r = glm.loglike_grad(d, beta, plan)
         assert rel(r.f, f) < TOL and grel(r.g, g) < TOL
+
+
+@pytest.mark.parametrize("pairs", ["1", "0"])
+def test_fp64_stream_layouts(gpu, monkeypatch, pairs):
+    """fp64 X through the stream kernel's two consumer layouts (column pairs with 16-byte
+    loads and XOR-permuted rows, or column per lane), f only and f + g, odd and even N,
+    against the oracle (1e-10)."""
+    monkeypatch.setenv("PM_F64_PAIRS", pairs)
+    monkeypatch.setenv("PM_GLM_ROWS", "0")
+    gen = np.random.default_rng(78)
+    for k in (2, 40, 64, 66, 100, 128, 192, 256):
+        n = 2999 + 41 * k
+        x = gen.standard_normal((n, k))
+        x[:, 0] = 1.0
+        y = (gen.random(n) < 0.6).astype(np.float64)
+        beta = gen.normal(0, 0.3, k)
+        d = DesignMatrix(x, y)
+        f, g = gl.loglike_grad(x, y, beta)
+        r = glm.loglike_grad(d, beta)
+        assert rel(r.f, f) < TOL and grel(r.g, g) < TOL, k
+        assert rel(glm.loglike(d, beta), f) < TOL, k
+        d.release_device()
