@@ -616,10 +616,12 @@ def run_hb(args, cfg):
 
 # ---------------------------------------------------------------------------- B200 arm: Gibbs
 def run_gibbs_strips(args, cfg):
-    """N>1: horizontal strips, one per rank, halo rows exchanged over NCCL per half-sweep."""
+    """N>1: horizontal strips, one per rank; halo rows exchanged by the half-sweep kernels
+    through peer memory (start_peer_halos), or over NCCL per half-sweep (--exchange nccl, or
+    if a peer mapping fails on any rank)."""
     import torch
     import torch.distributed as dist
-    from paper_1310_1537_b200.dist import LatticeStrip, strip_bounds, strip_sweeps
+    from paper_1310_1537_b200.dist import LatticeStrip, start_peer_halos, strip_bounds, strip_sweeps
     from paper_1310_1537_b200.synthetic import ising_spins, potts_states
     ws, rank, local = dist_env()
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -629,6 +631,7 @@ def run_gibbs_strips(args, cfg):
     strip = LatticeStrip(h, w, a, b - a, local, model=cfg["model"], w=2 * 0.4407, coupling=0.4407)
     strip.set_spins(full[a:b])
     del full
+    peer = args.exchange != "nccl" and start_peer_halos(strip, rank, ws)
     seed = 2024
     strip_sweeps(strip, args.warmup, seed, 0, rank, ws)
     torch.cuda.synchronize()
@@ -653,7 +656,9 @@ def run_gibbs_strips(args, cfg):
             "scaling": "strong", "vs_baseline": None, "dtype": "int8 spins, u32 Philox",
             "data": "synthetic iid uniform initial state",
             "config": {"workload": cfg["desc"], "H": h, "W": w, "beta_J": 0.4407,
-                       "parallelism": f"row strips x{ws}, NCCL halo exchange per half-sweep"},
+                       "parallelism": f"row strips x{ws}, " + (
+                           "halo rows stored into the neighbours' mailboxes by the half-sweep kernels "
+                           "(P2P, flags; no NCCL call)" if peer else "NCCL halo exchange per half-sweep")},
             "msite_per_s": h * w / (ms * 1e-3) / 1e6,
             "roofline": {"bound": "issue (Philox4x32) + halo latency", "achieved": 2 * h * w / (ms * 1e-3) / 1e9,
                          "peak": peak * ws, "unit": "GB/s", "frac": 2 * h * w / (ms * 1e-3) / 1e9 / (peak * ws),

@@ -296,6 +296,21 @@ PM_API int pm_lat_strip_half_sweep(pm_lat_t h, int colour, uint64_t seed, uint64
 /* Device pointer of packed row `array_row` of colour `colour` (W/2 bytes): 0 = top halo,
  * 1..rows = own rows, rows+1 = bottom halo. */
 PM_API int pm_lat_strip_row(pm_lat_t h, int colour, int32_t array_row, void** dev_ptr);
+/* Peer-memory halo exchange (replaces the caller's per-half-sweep exchange, e.g. NCCL
+ * send/recv): each strip owns a mailbox of double-buffered halo rows + flags; the
+ * half-sweep kernel stores its first / last own rows straight into the up neighbour's
+ * "row below" / the down neighbour's "row above" (P2P over NVLink/NVSwitch), its last CTA
+ * raises their flags, and the rows that need a halo wait for it (acquire, ~10 s timeout ->
+ * pm_lat_strip_xchg_status = 1).  Setup: pm_lat_strip_xchg_create (returns the mailbox
+ * address), pm_lat_strip_xchg_ipc_handle (64 bytes, for other processes), set_peers with a
+ * same-process mailbox pointer or an IPC handle per neighbour (up = the strip above, rows
+ * row0-1..., periodic), then pm_lat_strip_xchg_start after pm_lat_set_spins.  Every strip
+ * must then run the same half-sweep sequence (SPMD). */
+PM_API int pm_lat_strip_xchg_create(pm_lat_t h, void** mailbox);
+PM_API int pm_lat_strip_xchg_ipc_handle(pm_lat_t h, void* handle_out /* 64 bytes */);
+PM_API int pm_lat_strip_xchg_set_peers(pm_lat_t h, void* up, const void* up_ipc, void* down, const void* down_ipc);
+PM_API int pm_lat_strip_xchg_start(pm_lat_t h, void* stream);
+PM_API int pm_lat_strip_xchg_status(pm_lat_t h, int32_t* timed_out);
 
 /* ---------------------------------------------------------------- batch RNG
  * Device generation of the reference's deviate streams (rng.py:42-138) and its Gamma /

@@ -102,6 +102,11 @@ SIGNATURES = {
     "pm_lat_create_strip": (c_int, [c_int, c_int32, c_int32, c_int32, c_int32, c_int, POINTER(c_void_p)]),
     "pm_lat_strip_half_sweep": (c_int, [c_void_p, c_int, c_uint64, c_uint64, c_void_p]),
     "pm_lat_strip_row": (c_int, [c_void_p, c_int, c_int32, POINTER(c_void_p)]),
+    "pm_lat_strip_xchg_create": (c_int, [c_void_p, POINTER(c_void_p)]),
+    "pm_lat_strip_xchg_ipc_handle": (c_int, [c_void_p, c_void_p]),
+    "pm_lat_strip_xchg_set_peers": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pm_lat_strip_xchg_start": (c_int, [c_void_p, c_void_p]),
+    "pm_lat_strip_xchg_status": (c_int, [c_void_p, POINTER(c_int32)]),
     "pm_rng_fill": (c_int, [c_int, c_int, c_uint64, c_uint64, c_uint64, c_int64, c_void_p, c_int, _fp]),
     "pm_rng_gamma": (c_int, [c_int, c_double, c_double, c_int64, _u64p, _u64p, _u64p, _u64p, _dp, _fp]),
     "pm_rng_dirichlet": (c_int, [c_int, _dp, c_int32, c_int64, _u64p, _u64p, _u64p, _u64p, _dp, _fp]),

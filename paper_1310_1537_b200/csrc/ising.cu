@@ -157,7 +157,45 @@ struct PackedArgs {
   // halo .. halo+rows-1; with halo = 1 the arrays carry one halo row above and below
   // (filled by the caller's exchange) and there is no vertical wrap inside the strip.
   int row0, rows, halo;
+  // peer-memory halo exchange (xmb != null; pm_lat_strip_xchg_*): this strip's mailbox and
+  // its up / down neighbours' mailboxes (CUDA IPC or same-process pointers).  The halo rows
+  // of the colour read here come from xmb (parity rpar), waiting for flag >= kread; the own
+  // first / last rows computed here are also stored into the up neighbour's DOWN halo / the
+  // down neighbour's UP halo (parity wpar), and the last CTA raises their flags to kwrite.
+  int8_t* xmb;
+  int8_t* xup;
+  int8_t* xdown;
+  int rpar, wpar;
+  unsigned long long kread, kwrite;
+  unsigned* ticket;
+  unsigned* status;
 };
+
+// Strip mailbox: halos [parity 2][colour 2][side 2: 0 = row above the strip, 1 = row below]
+// [W2] bytes, then flags [colour 2][side 2] u64 = latest deposit number in that halo.
+__host__ __device__ inline size_t lat_xchg_halo(int par, int colour, int side, int W2) {
+  return (size_t(par) * 4 + colour * 2 + side) * W2;
+}
+__host__ __device__ inline size_t lat_xchg_flags(int W2) { return (size_t(8) * W2 + 127) / 128 * 128; }
+__host__ __device__ inline size_t lat_xchg_bytes(int W2) { return lat_xchg_flags(W2) + 4 * sizeof(unsigned long long); }
+
+// wait (acquire, system scope) until *flag >= k; ~10 s then *status = 1
+__device__ inline void lat_wait_flag(const unsigned long long* flag, unsigned long long k, unsigned* status) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (true) {
+    unsigned long long e;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(e) : "l"(flag) : "memory");
+    if (e >= k) return;
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > 10000000000ull) {
+      *status = 1u;
+      return;
+    }
+    __nanosleep(100);
+  }
+}
 
 __device__ __forceinline__ uint4 ld16(const int8_t* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
 
@@ -188,11 +226,14 @@ struct GibbsTables {
 };
 
 // Thread = NG consecutive 16-site groups of one packed row (setup amortised over 16*NG sites).
-template <int MODEL, bool T32, int NG>
+template <int MODEL, bool T32, int NG, bool XCHG>
 __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const GibbsTables<MODEL, T32>& tb, int r,
                                                  int q0);
 
-template <int MODEL, bool T32, int NG>
+__device__ inline void lat_xchg_publish(const PackedArgs& a);
+
+// XCHG: the strip peer-memory halo exchange (PackedArgs xmb ...) is compiled in
+template <int MODEL, bool T32, int NG, bool XCHG>
 __global__ void __launch_bounds__(256, NG == 1 ? 6 : 4)
     gibbs_packed_kernel(PackedArgs a, const unsigned long long* __restrict__ pthr, const uint4* __restrict__ pthr32) {
   __shared__ GibbsTables<MODEL, T32> tb;
@@ -218,13 +259,15 @@ __global__ void __launch_bounds__(256, NG == 1 ? 6 : 4)
   // 2-D grid of 2-D blocks: x = (16*NG)-site column groups of a row, y = rows
   const int per_row = a.W2 / (16 * NG);
   const int cgrp = blockIdx.x * blockDim.x + threadIdx.x;
-  if (cgrp >= per_row) return;
-  for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < a.rows; r += gridDim.y * blockDim.y) {
-    gibbs_packed_row<MODEL, T32, NG>(a, tb, r, cgrp * 16 * NG);
+  if (cgrp < per_row) {
+    for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < a.rows; r += gridDim.y * blockDim.y) {
+      gibbs_packed_row<MODEL, T32, NG, XCHG>(a, tb, r, cgrp * 16 * NG);
+    }
   }
+  if constexpr (XCHG) lat_xchg_publish(a);
 }
 
-template <int MODEL, bool T32, int NG>
+template <int MODEL, bool T32, int NG, bool XCHG>
 __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const GibbsTables<MODEL, T32>& tb, int r,
                                                  int q0) {
   constexpr int NW = 4 * NG;   // 32-bit words (4 sites each) handled by this thread
@@ -235,6 +278,18 @@ __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const Gibb
   const int8_t* orow = a.other + int64_t(li) * a.W2;
   const int8_t* urow = a.other + int64_t(iu) * a.W2;
   const int8_t* drow = a.other + int64_t(id) * a.W2;
+  if constexpr (XCHG) {  // halo rows of the other colour from the mailbox, once the neighbours delivered
+    const int oc = a.colour ^ 1;
+    const unsigned long long* fl = reinterpret_cast<const unsigned long long*>(a.xmb + lat_xchg_flags(a.W2));
+    if (r == 0) {
+      lat_wait_flag(fl + oc * 2 + 0, a.kread, a.status);
+      urow = a.xmb + lat_xchg_halo(a.rpar, oc, 0, a.W2);
+    }
+    if (r == a.rows - 1) {
+      lat_wait_flag(fl + oc * 2 + 1, a.kread, a.status);
+      drow = a.xmb + lat_xchg_halo(a.rpar, oc, 1, a.W2);
+    }
+  }
   uint32_t U[NW], D[NW], M[NW];
 #pragma unroll
   for (int g = 0; g < NG; ++g) {
@@ -295,6 +350,42 @@ __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const Gibb
   for (int g = 0; g < NG; ++g)
     *reinterpret_cast<uint4*>(a.mine + int64_t(li) * a.W2 + q0 + 16 * g) =
         make_uint4(res[4 * g], res[4 * g + 1], res[4 * g + 2], res[4 * g + 3]);
+  if constexpr (XCHG) {  // own boundary rows into the neighbours' halos (P2P stores over NVLink)
+    if (r == 0) {
+#pragma unroll
+      for (int g = 0; g < NG; ++g)
+        *reinterpret_cast<uint4*>(a.xup + lat_xchg_halo(a.wpar, a.colour, 1, a.W2) + q0 + 16 * g) =
+            make_uint4(res[4 * g], res[4 * g + 1], res[4 * g + 2], res[4 * g + 3]);
+    }
+    if (r == a.rows - 1) {
+#pragma unroll
+      for (int g = 0; g < NG; ++g)
+        *reinterpret_cast<uint4*>(a.xdown + lat_xchg_halo(a.wpar, a.colour, 0, a.W2) + q0 + 16 * g) =
+            make_uint4(res[4 * g], res[4 * g + 1], res[4 * g + 2], res[4 * g + 3]);
+    }
+  }
+}
+
+// Completion of a peer-exchanging half-sweep: the last CTA (acq_rel ticket after a CTA
+// barrier and a system-scope fence covering the CTA's P2P stores) raises the neighbours'
+// flags for this colour: up neighbour's "row below" flag, down neighbour's "row above" flag.
+__device__ inline void lat_xchg_publish(const PackedArgs& a) {
+  __shared__ int last;
+  __syncthreads();
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    asm volatile("fence.sc.sys;" ::: "memory");
+    unsigned t;
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(a.ticket) : "memory");
+    last = (t == gridDim.x * gridDim.y - 1) ? 1 : 0;
+    if (last) {
+      *a.ticket = 0u;  // re-arm (kernel boundary orders it)
+      asm volatile("fence.sc.sys;" ::: "memory");
+      unsigned long long* fu = reinterpret_cast<unsigned long long*>(a.xup + lat_xchg_flags(a.W2)) + a.colour * 2 + 1;
+      unsigned long long* fd = reinterpret_cast<unsigned long long*>(a.xdown + lat_xchg_flags(a.W2)) + a.colour * 2 + 0;
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(fu), "l"(a.kwrite) : "memory");
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(fd), "l"(a.kwrite) : "memory");
+    }
+  }
 }
 
 // ---------------------------------------------------------------- layout conversion
@@ -386,14 +477,29 @@ struct pm_lat_s {
   // uniforms staging
   double* uni = nullptr;
   size_t uni_cap = 0;
+  // strip peer-memory halo exchange (pm_lat_strip_xchg_*)
+  int8_t* xmb = nullptr;                   // own mailbox (IPC-exported)
+  int8_t* xup = nullptr;                   // up / down neighbours' mailboxes in this process
+  int8_t* xdown = nullptr;
+  bool xup_ipc = false, xdown_ipc = false;  // mappings to close
+  unsigned* xticket = nullptr;             // [0] ticket, [1] status
+  unsigned long long xcount[2] = {0, 0};   // deposits made per colour (identical on every rank)
+  bool xready = false;                     // initial deposit done: half-sweeps use the mailbox
 };
 
 namespace {
 
 void free_lat(pm_lat_s* h) {
+  if (h->xup_ipc && h->xup) cudaIpcCloseMemHandle(h->xup);
+  if (h->xdown_ipc && h->xdown && !(h->xup_ipc && h->xdown == h->xup)) cudaIpcCloseMemHandle(h->xdown);
+  h->xup = h->xdown = nullptr;
+  h->xup_ipc = h->xdown_ipc = false;
   for (void* p : {(void*)h->pk0, (void*)h->pk1, (void*)h->scratch, (void*)h->cls, (void*)h->ptab, (void*)h->cdf,
-                  (void*)h->pthr, (void*)h->pthr32, (void*)h->uni})
+                  (void*)h->pthr, (void*)h->pthr32, (void*)h->uni, (void*)h->xmb, (void*)h->xticket})
     if (p) cudaFree(p);
+  h->xmb = nullptr;
+  h->xticket = nullptr;
+  h->xready = false;
   h->pthr32 = nullptr;
   h->pk0 = h->pk1 = h->scratch = nullptr;
   h->cls = nullptr;
@@ -626,6 +732,23 @@ static void launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t seed, cud
   pa.row0 = h->row0;
   pa.rows = h->H;
   pa.halo = h->strip;
+  pa.xmb = pa.xup = pa.xdown = nullptr;
+  pa.rpar = pa.wpar = 0;
+  pa.kread = pa.kwrite = 0;
+  pa.ticket = pa.status = nullptr;
+  if (h->strip && h->xready) {
+    // read the other colour's latest deposit, write this colour's next one
+    const unsigned long long kr = h->xcount[c ^ 1], kw = ++h->xcount[c];
+    pa.xmb = h->xmb;
+    pa.xup = h->xup;
+    pa.xdown = h->xdown;
+    pa.rpar = int(kr & 1);
+    pa.wpar = int(kw & 1);
+    pa.kread = kr;
+    pa.kwrite = kw;
+    pa.ticket = h->xticket;
+    pa.status = h->xticket + 1;
+  }
   const int W2 = h->W / 2;
   const int ng = (W2 % 64 == 0) ? 4 : (W2 % 32 == 0) ? 2 : 1;   // 16-site groups per thread
   const int per_row = W2 / (16 * ng);
@@ -636,8 +759,10 @@ static void launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t seed, cud
   const bool ising = h->model == PM_MODEL_ISING;
   cudaError_t e = cudaSuccess;  // a failed launch is also the thread's last error (callers check it)
 #define PM_LAUNCH_PACKED(M, T, N)                                                                      \
-  e = launch_pdl(h->pdl, gibbs_packed_kernel<M, T, N>, grid, block, 0, st, pa,                        \
-                 (const unsigned long long*)h->pthr, (const uint4*)h->pthr32)
+  e = pa.xmb ? launch_pdl(h->pdl, gibbs_packed_kernel<M, T, N, true>, grid, block, 0, st, pa,          \
+                          (const unsigned long long*)h->pthr, (const uint4*)h->pthr32)                 \
+             : launch_pdl(h->pdl, gibbs_packed_kernel<M, T, N, false>, grid, block, 0, st, pa,         \
+                          (const unsigned long long*)h->pthr, (const uint4*)h->pthr32)
 #define PM_LAUNCH_NG(M, T)            \
   do {                                \
     if (ng == 4)                      \
@@ -717,6 +842,122 @@ int pm_lat_strip_row(pm_lat_t h, int colour, int32_t array_row, void** dev_ptr) 
   if (colour != 0 && colour != 1) return fail(PM_EINVAL, "colour must be 0 or 1");
   if (array_row < 0 || array_row > h->H + 1) return fail(PM_ERANGE, "array row out of range");
   *dev_ptr = (colour ? h->pk1 : h->pk0) + size_t(array_row) * (h->W / 2);
+  return PM_OK;
+}
+
+int pm_lat_strip_xchg_create(pm_lat_t h, void** mailbox) {
+  if (!h || !mailbox) return fail(PM_EINVAL, "null argument");
+  if (!h->strip) return fail(PM_ESTATE, "not a strip handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  if (!h->xmb) {
+    const size_t bytes = lat_xchg_bytes(h->W / 2);
+    PM_CUDA(cudaMalloc(&h->xmb, bytes));
+    PM_CUDA(cudaMemset(h->xmb, 0, bytes));
+    PM_CUDA(cudaMalloc(&h->xticket, 2 * sizeof(unsigned)));
+    PM_CUDA(cudaMemset(h->xticket, 0, 2 * sizeof(unsigned)));
+    PM_CUDA(cudaDeviceSynchronize());
+  }
+  *mailbox = h->xmb;
+  return PM_OK;
+}
+
+int pm_lat_strip_xchg_ipc_handle(pm_lat_t h, void* handle_out) {
+  if (!h || !handle_out) return fail(PM_EINVAL, "null argument");
+  if (!h->xmb) return fail(PM_ESTATE, "call pm_lat_strip_xchg_create first");
+  DeviceGuard g(h->device);
+  cudaIpcMemHandle_t hd;
+  PM_CUDA(cudaIpcGetMemHandle(&hd, h->xmb));
+  std::memcpy(handle_out, &hd, sizeof(hd));
+  return PM_OK;
+}
+
+int pm_lat_strip_xchg_set_peers(pm_lat_t h, void* up, const void* up_ipc, void* down, const void* down_ipc) {
+  if (!h) return fail(PM_EINVAL, "null handle");
+  if (!h->xmb) return fail(PM_ESTATE, "call pm_lat_strip_xchg_create first");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->xup || h->xdown) return fail(PM_ESTATE, "peers already set");
+  DeviceGuard g(h->device);
+  auto map = [&](void* ptr, const void* ipc, int8_t** out, bool* opened) -> int {
+    if (ptr) {
+      *out = static_cast<int8_t*>(ptr);
+      return PM_OK;
+    }
+    if (!ipc) return fail(PM_EINVAL, "need a pointer or an IPC handle for each neighbour");
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, ipc, sizeof(hd));
+    void* p = nullptr;
+    PM_CUDA(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
+    *out = static_cast<int8_t*>(p);
+    *opened = true;
+    return PM_OK;
+  };
+  int rc = map(up, up_ipc, &h->xup, &h->xup_ipc);
+  if (rc) return rc;
+  // world 2: both neighbours are the same rank (map it once)
+  if (!down && down_ipc && up_ipc && std::memcmp(up_ipc, down_ipc, sizeof(cudaIpcMemHandle_t)) == 0) {
+    h->xdown = h->xup;
+    return PM_OK;
+  }
+  rc = map(down, down_ipc, &h->xdown, &h->xdown_ipc);
+  if (rc) {
+    if (h->xup_ipc) cudaIpcCloseMemHandle(h->xup);
+    h->xup = nullptr;
+    h->xup_ipc = false;
+  }
+  return rc;
+}
+
+int pm_lat_strip_xchg_status(pm_lat_t h, int32_t* timed_out) {
+  if (!h || !timed_out) return fail(PM_EINVAL, "null argument");
+  if (!h->xticket) return fail(PM_ESTATE, "no exchange");
+  DeviceGuard g(h->device);
+  unsigned v[2] = {0, 0};
+  PM_CUDA(cudaMemcpy(v, h->xticket, sizeof(v), cudaMemcpyDeviceToHost));
+  *timed_out = int(v[1]);
+  return PM_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// Initial deposit: this strip's first / last rows of both colours into the neighbours' halos
+// (deposit number 1 of each colour, parity 1), then their flags.
+__global__ void lat_xchg_init_kernel(const int8_t* pk0, const int8_t* pk1, int rows, int W2, int8_t* up,
+                                     int8_t* down) {
+  for (int c = 0; c < 2; ++c) {
+    const int8_t* pk = c ? pk1 : pk0;
+    for (int q = threadIdx.x; q < W2; q += blockDim.x) {
+      up[lat_xchg_halo(1, c, 1, W2) + q] = pk[size_t(1) * W2 + q];       // my first row: below `up`
+      down[lat_xchg_halo(1, c, 0, W2) + q] = pk[size_t(rows) * W2 + q];  // my last row: above `down`
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("fence.sc.sys;" ::: "memory");
+    for (int c = 0; c < 2; ++c) {
+      unsigned long long* fu = reinterpret_cast<unsigned long long*>(up + lat_xchg_flags(W2)) + c * 2 + 1;
+      unsigned long long* fd = reinterpret_cast<unsigned long long*>(down + lat_xchg_flags(W2)) + c * 2 + 0;
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(fu), "l"(1ull) : "memory");
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(fd), "l"(1ull) : "memory");
+    }
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int pm_lat_strip_xchg_start(pm_lat_t h, void* stream) {
+  if (!h) return fail(PM_EINVAL, "null handle");
+  if (!h->xmb || !h->xup || !h->xdown) return fail(PM_ESTATE, "exchange peers not set");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  if (h->xcount[0] || h->xcount[1]) return fail(PM_ESTATE, "exchange already started");
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+  lat_xchg_init_kernel<<<1, 256, 0, st>>>(h->pk0, h->pk1, h->H, h->W / 2, h->xup, h->xdown);
+  PM_CUDA(cudaGetLastError());
+  h->xcount[0] = h->xcount[1] = 1;
+  h->xready = true;
   return PM_OK;
 }
 

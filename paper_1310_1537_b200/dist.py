@@ -24,7 +24,7 @@ from .glm import DesignMatrix, GradResult, _check_beta
 from .parallel import partition
 
 __all__ = ["shard_bounds", "ordered_sum", "gather_partials", "PeerExchange", "DistributedDesign",
-           "strip_bounds", "exchange_halos", "LatticeStrip", "strip_sweeps"]
+           "strip_bounds", "exchange_halos", "LatticeStrip", "start_peer_halos", "strip_sweeps"]
 
 
 def shard_bounds(n_rows: int, world: int, rank: int) -> tuple[int, int]:
@@ -268,6 +268,7 @@ class LatticeStrip:
         else:
             _lib.call("pm_lat_set_potts", h, float(coupling))
         self._views = {}
+        self.peer_exchange = False  # True after xchg_start: half-sweeps exchange halos themselves
 
     def set_spins(self, own_rows: np.ndarray) -> None:
         s = np.ascontiguousarray(own_rows, dtype=np.int8)
@@ -295,6 +296,40 @@ class LatticeStrip:
             self._views[key] = t
         return t
 
+    # ---- peer-memory halo exchange (pm_lat_strip_xchg_*) ----
+    def xchg_mailbox(self) -> int:
+        import ctypes
+        p = ctypes.c_void_p()
+        self._lib.call("pm_lat_strip_xchg_create", self._h, ctypes.byref(p))
+        return p.value
+
+    def xchg_ipc_handle(self) -> bytes:
+        import ctypes
+        self.xchg_mailbox()
+        buf = ctypes.create_string_buffer(64)
+        self._lib.call("pm_lat_strip_xchg_ipc_handle", self._h, ctypes.cast(buf, ctypes.c_void_p))
+        return bytes(buf.raw)
+
+    def xchg_set_peers(self, up=None, down=None, up_ipc: bytes = None, down_ipc: bytes = None) -> None:
+        """Neighbour mailboxes: same-process device pointers (up/down) or IPC handles."""
+        import ctypes
+
+        def h(b):
+            return None if b is None else ctypes.cast(ctypes.c_char_p(b), ctypes.c_void_p)
+        self._lib.call("pm_lat_strip_xchg_set_peers", self._h, ctypes.c_void_p(up), h(up_ipc),
+                       ctypes.c_void_p(down), h(down_ipc))
+
+    def xchg_start(self) -> None:
+        import ctypes
+        self._lib.call("pm_lat_strip_xchg_start", self._h, ctypes.c_void_p(torch_stream_handle(self.device)))
+        self.peer_exchange = True
+
+    def xchg_timed_out(self) -> bool:
+        import ctypes
+        v = ctypes.c_int32()
+        self._lib.call("pm_lat_strip_xchg_status", self._h, ctypes.byref(v))
+        return bool(v.value)
+
     def half_sweep(self, colour: int, seed: int, sweep: int) -> None:
         import ctypes
 
@@ -315,9 +350,47 @@ class LatticeStrip:
             pass
 
 
+def start_peer_halos(strip, rank: int, world: int, group=None) -> bool:
+    """Set up the peer-memory halo exchange for a strip (collective over the group): mailbox
+    IPC handles all-gathered, neighbours (rank-1, rank+1, periodic) mapped; every rank agrees
+    on the outcome, so on failure all ranks keep the NCCL path.  Call after set_spins."""
+    import torch.distributed as dist
+    ok, err, mine = True, "", b""
+    try:
+        mine = strip.xchg_ipc_handle()
+    except Exception as e:  # noqa: BLE001
+        ok, err = False, str(e)
+    handles = [None] * world
+    dist.all_gather_object(handles, (mine, ok), group=group)
+    ok = all(o for _, o in handles)
+    if ok:
+        up, down = (rank - 1) % world, (rank + 1) % world
+        try:
+            if world == 1:
+                mb = strip.xchg_mailbox()
+                strip.xchg_set_peers(up=mb, down=mb)
+            else:
+                strip.xchg_set_peers(up_ipc=handles[up][0], down_ipc=handles[down][0])
+        except Exception as e:  # noqa: BLE001
+            ok, err = False, str(e)
+    flags = [None] * world
+    dist.all_gather_object(flags, ok, group=group)
+    if not all(flags):
+        return False
+    strip.xchg_start()
+    return True
+
+
 def strip_sweeps(strip, n_sweeps: int, seed: int, sweep0: int, rank: int, world: int, group=None) -> None:
     """n_sweeps full sweeps of a strip-decomposed lattice: per colour, the device half-sweep
-    then one halo exchange of that colour (bit-identical to the single-GPU sweep)."""
+    then one halo exchange of that colour (bit-identical to the single-GPU sweep).  After
+    start_peer_halos the half-sweep kernels exchange the halo rows themselves (P2P stores +
+    flags), so this is just the sequence of half-sweep launches."""
+    if getattr(strip, "peer_exchange", False):
+        for t in range(n_sweeps):
+            for c in (0, 1):
+                strip.half_sweep(c, seed, sweep0 + t)
+        return
     r = strip.rows
     for c in (0, 1):  # halos of both colours must be current before the first half-sweep
         exchange_halos(strip.row(c, 1), strip.row(c, r), strip.row(c, 0), strip.row(c, r + 1), rank, world, group)
