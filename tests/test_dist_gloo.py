@@ -213,3 +213,60 @@ def test_peer_exchange_setup_agrees_across_ranks(fail_rank):
         if rank != fail_rank:
             assert opened == [(p, f"rank{p}".encode()) for p in range(world) if p != rank]
         assert destroyed == (0 if ok else 1)
+
+
+def _halo_worker(rank, world, port, q, fail_rank):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1310_1537_b200.dist import start_peer_halos
+
+        class FakeStrip:
+            """The strip's pm_lat_strip_xchg_* calls stood in for on CPU."""
+
+            def __init__(self):
+                self.peers, self.started = None, False
+
+            def xchg_ipc_handle(self):
+                return f"mb{rank}".encode().ljust(64, b"\0")
+
+            def xchg_mailbox(self):
+                return 4096 + rank
+
+            def xchg_set_peers(self, up=None, down=None, up_ipc=None, down_ipc=None):
+                if rank == fail_rank:
+                    raise RuntimeError("cudaIpcOpenMemHandle failed")
+                self.peers = (up, down, up_ipc[:3] if up_ipc else None, down_ipc[:3] if down_ipc else None)
+
+            def xchg_start(self):
+                self.started = True
+
+        s = FakeStrip()
+        ok = start_peer_halos(s, rank, world)
+        q.put((rank, ok, s.started, s.peers))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,fail_rank", [(3, -1), (3, 2), (1, -1)])
+def test_peer_halo_setup_neighbours_and_agreement(world, fail_rank):
+    """start_peer_halos (gloo, CPU stand-in strips): rank r maps rank r-1 as the strip above
+    and r+1 below (periodic; world 1 maps itself by pointer); a failure on any rank leaves
+    every rank on the NCCL path (nobody starts the peer exchange)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, q, fail_rank)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok, started, peers in res:
+        assert ok == (fail_rank < 0) and started == ok
+        if ok and world == 1:
+            assert peers == (4096, 4096, None, None)
+        elif ok:
+            assert peers == (None, None, f"mb{(rank - 1) % world}".encode(), f"mb{(rank + 1) % world}".encode())
