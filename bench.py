@@ -96,6 +96,19 @@ def load_traffic(key: str):
         return None
 
 
+def issue_roofline(config: str, ms_per_sweep: float, clk: dict):
+    """The Gibbs sweep's real bound: warp instructions issued per second (ncu count of one
+    Ising half-sweep launch, profiles/traffic.json) against 148 SMs x 4 schedulers x the
+    median SM clock sampled during the timed region."""
+    n = load_traffic("c4_warp_inst_per_half_sweep") if config == "c4" else None
+    if not n or not clk or not clk.get("sm_mhz"):
+        return None
+    achieved = 2 * n / (ms_per_sweep * 1e-3)
+    peak = 148 * 4 * clk["sm_mhz"] * 1e6
+    return {"achieved": achieved, "peak": peak, "unit": "warp instructions/s", "frac": achieved / peak,
+            "source": "ncu smsp__inst_executed.sum per half-sweep (profiles/r01_ncu_gibbs_packed_raw.csv)"}
+
+
 # ---------------------------------------------------------------------------- clocks
 class ClockSampler:
     """nvidia-smi clocks and throttle reasons sampled during the timed region."""
@@ -727,6 +740,7 @@ def run_gibbs(args, cfg):
                          "achieved": bytes_sweep / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": bytes_sweep / (ms * 1e-3) / 1e9 / peak, "traffic": load_traffic(args.config),
                          "peak_source": src},
+            "issue_roofline": issue_roofline(args.config, ms, clk),
             "e2e": {"value": args.steps / e2e, "unit": "sweeps/s", "h2d_bytes_per_step": h * w / args.steps,
                     "d2h_bytes_per_step": h * w / args.steps},
             "gpu_launches": 2 * args.steps, "clocks": clk,
