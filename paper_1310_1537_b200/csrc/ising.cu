@@ -313,12 +313,23 @@ __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const Gibb
     const U32x4 blk = site_philox_block(g0 + m, a.sweep, a.seed);
     uint32_t out = 0;
     if constexpr (MODEL == PM_MODEL_ISING) {
-      const uint32_t nd = down_bits(U[m]) + down_bits(D[m]) + down_bits(cur) + down_bits(sh);
+      // per byte: bit 1 is set for a -1 spin (0xFF) and clear for +1 (0x01), so the masked
+      // 4-way sum is 2 x (number of -1 neighbours) <= 8 per byte (no carries); scaled to the
+      // table's byte offset (x4 for u32 thresholds, x8 for u64) it is the LDS address offset
+      constexpr uint32_t M2 = 0x02020202u;
+      constexpr int SH = T32 ? 1 : 2;
+      const uint32_t off = ((U[m] & M2) + (D[m] & M2) + (cur & M2) + (sh & M2)) << SH;
+      const char* tbase = reinterpret_cast<const char*>(&tb.t[0]);
       uint32_t plus_bits = 0;  // bit 8b set <=> site b becomes +1
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        const uint32_t k = __byte_perm(nd, 0u, 0x4440u + b);
-        const bool plus = T32 ? (blk.v[b] < uint32_t(tb.t[k])) : (uint64_t(blk.v[b]) < uint64_t(tb.t[k]));
+        const uint32_t o = __byte_perm(off, 0u, 0x4440u + b);
+        bool plus;
+        if constexpr (T32) {
+          plus = blk.v[b] < *reinterpret_cast<const uint32_t*>(tbase + o);
+        } else {
+          plus = uint64_t(blk.v[b]) < *reinterpret_cast<const unsigned long long*>(tbase + o);
+        }
         plus_bits |= plus ? (1u << (8 * b)) : 0u;
       }
       out = 0xFFFFFFFFu - 0xFEu * plus_bits;  // per byte: 0x01 (+1) or 0xFF (-1), no borrows
