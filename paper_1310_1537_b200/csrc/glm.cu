@@ -343,7 +343,8 @@ int choose_geometry(pm_glm_s* h) {
     // fp32-X, K <= 128: 15 consumer warps, one 32-row stage each (PM_STREAM_NCW=7 disables;
     // measured: 16-row stages, 2 per warp, are 26 % slower -- per-stage overheads dominate)
     const char* e15 = std::getenv("PM_STREAM_NCW");
-    if (h->kind == KIND_STREAM && h->xtype == PM_X_F32 && kc <= 4 && h->pairs != 2 &&
+    // (the pairs consumer runs 7 warps: its two unrolled sub-tiles need the registers)
+    if (h->kind == KIND_STREAM && h->xtype == PM_X_F32 && kc <= 4 && h->pairs == 0 &&
         !(e15 && std::atoi(e15) == 7)) {
       const size_t fixed15 = stream_smem_bytes(h->K, xs, 0, kNCW15);
       int S15 = int((budget - (long)fixed15) / (long)per_stage);

@@ -197,7 +197,11 @@ __device__ __forceinline__ void consume_tile_pairs(const XT* xs, const double* y
   static_assert(KC % 2 == 0, "pairs layout needs an even register count");
   constexpr int KP = KC / 2;
   const bool last_ok = 64 * (KP - 1) + 2 * lane < K;
-#pragma unroll 1
+  // fp32-X: the two sub-tiles of a tile are unrolled so the compiler interleaves their
+  // latency chains (+4.5 % at c1f32 with 7 consumer warps, profiles/r01_ab_unroll.txt);
+  // fp64 keeps one sub-tile at a time (HBM-bound; unrolling measured no gain)
+  constexpr int kSubUnroll = std::is_same<XT, float>::value ? 2 : 1;
+#pragma unroll kSubUnroll
   for (int sub = 0; sub < TR / R; ++sub) {
     const char* xb = reinterpret_cast<const char*>(xs) + size_t(sub) * R * K * sizeof(XT);
     double x[R][KC];
