@@ -1098,7 +1098,8 @@ struct pm_hb_s {
   double* out_f = nullptr;
   double* out_g = nullptr;
   double* pin_in = nullptr;    // G*K + 2K
-  double* pin_out = nullptr;   // G + G*K
+  double* pin_out = nullptr;   // G + G*K (mapped)
+  double* pin_out_dev = nullptr;  // device alias of pin_out
   // small-K row-per-lane path (even K <= 32): balanced tile ranges + segment fold
   bool rows = false;
   int rows_grid = 0, rows_stages = 0, rows_ncw = 7, rows_tps = 1;
@@ -1115,8 +1116,8 @@ struct pm_hb_s {
 namespace {
 
 void free_hb(pm_hb_s* h) {
-  for (void* p : {(void*)h->X, (void*)h->y, (void*)h->poff, (void*)h->nrows, (void*)h->betas, (void*)h->mu_dev,
-                  (void*)h->sigma_dev, (void*)h->out_f, (void*)h->out_g, (void*)h->seg_base, (void*)h->gseg,
+  for (void* p : {(void*)h->X, (void*)h->y, (void*)h->poff, (void*)h->nrows, (void*)h->betas,
+                  (void*)h->out_f, (void*)h->out_g, (void*)h->seg_base, (void*)h->gseg,
                   (void*)h->part, (void*)h->cta_g0, (void*)h->gcount})
     if (p) cudaFree(p);
   h->seg_base = h->gseg = h->cta_g0 = nullptr;
@@ -1128,7 +1129,7 @@ void free_hb(pm_hb_s* h) {
   h->X = h->y = nullptr;
   h->poff = h->nrows = nullptr;
   h->betas = h->mu_dev = h->sigma_dev = h->out_f = h->out_g = nullptr;
-  h->pin_in = h->pin_out = nullptr;
+  h->pin_in = h->pin_out = h->pin_out_dev = nullptr;
   h->G = h->K = 0;
 }
 
@@ -1312,13 +1313,17 @@ int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64_t* off
   PM_CUDA(cudaMalloc(&h->nrows, sizeof(int64_t) * G));
   PM_CUDA(cudaMemcpyAsync(h->poff, poff.data(), sizeof(int64_t) * (G + 1), cudaMemcpyHostToDevice, h->stream));
   PM_CUDA(cudaMemcpyAsync(h->nrows, nr.data(), sizeof(int64_t) * G, cudaMemcpyHostToDevice, h->stream));
-  PM_CUDA(cudaMalloc(&h->betas, sizeof(double) * size_t(G) * K));
-  PM_CUDA(cudaMalloc(&h->mu_dev, sizeof(double) * K));
-  PM_CUDA(cudaMalloc(&h->sigma_dev, sizeof(double) * K));
+  // betas, mu, sigma contiguous on the device (one H2D copy per evaluation from pin_in)
+  PM_CUDA(cudaMalloc(&h->betas, sizeof(double) * (size_t(G) * K + 2 * K)));
+  h->mu_dev = h->betas + size_t(G) * K;
+  h->sigma_dev = h->mu_dev + K;
   PM_CUDA(cudaMalloc(&h->out_f, sizeof(double) * G));
   PM_CUDA(cudaMalloc(&h->out_g, sizeof(double) * size_t(G) * K));
   PM_CUDA(cudaHostAlloc(&h->pin_in, sizeof(double) * (size_t(G) * K + 2 * K), cudaHostAllocPortable));
-  PM_CUDA(cudaHostAlloc(&h->pin_out, sizeof(double) * (size_t(G) + size_t(G) * K), cudaHostAllocPortable));
+  // mapped: pm_hb_eval's fold writes (f, g) straight into host memory (no D2H copies)
+  PM_CUDA(cudaHostAlloc(&h->pin_out, sizeof(double) * (size_t(G) + size_t(G) * K),
+                        cudaHostAllocPortable | cudaHostAllocMapped));
+  PM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->pin_out_dev), h->pin_out, 0));
   PM_CUDA(cudaStreamSynchronize(h->stream));
   const size_t fixed = stream_smem_bytes(K, 8, 0, kHbNCW);
   const size_t per_stage = stream_smem_bytes(K, 8, 1, 0) - stream_smem_bytes(K, 8, 0, 0);
@@ -1409,13 +1414,9 @@ static int hb_stage(pm_hb_t h, const double* betas, const double* mu, const doub
     std::memcpy(h->pin_in + size_t(G) * K, mu, sizeof(double) * K);
     std::memcpy(h->pin_in + size_t(G) * K + K, sigma, sizeof(double) * K);
   }
-  PM_CUDA(cudaMemcpyAsync(h->betas, h->pin_in, sizeof(double) * size_t(G) * K, cudaMemcpyHostToDevice, h->stream));
-  if (prior) {
-    PM_CUDA(cudaMemcpyAsync(h->mu_dev, h->pin_in + size_t(G) * K, sizeof(double) * K, cudaMemcpyHostToDevice,
-                            h->stream));
-    PM_CUDA(cudaMemcpyAsync(h->sigma_dev, h->pin_in + size_t(G) * K + K, sizeof(double) * K,
-                            cudaMemcpyHostToDevice, h->stream));
-  }
+  // one copy: betas, then mu and sigma right after them (contiguous on both sides)
+  PM_CUDA(cudaMemcpyAsync(h->betas, h->pin_in, sizeof(double) * (size_t(G) * K + (prior ? 2 * K : 0)),
+                          cudaMemcpyHostToDevice, h->stream));
   a.X = h->X;
   a.y = h->y;
   a.poff = h->poff;
@@ -1442,12 +1443,10 @@ int pm_hb_eval(pm_hb_t h, const double* betas, const double* mu, const double* s
   if (rc) return rc;
   const int G = h->G, K = h->K;
   const bool grad = want_grad != 0 && g_out != nullptr;
+  a.out_f = h->pin_out_dev;  // the fold writes the results into mapped host memory
+  a.out_g = h->pin_out_dev + G;
   cudaError_t e = launch_hb_any(h, a, grad);
   if (e != cudaSuccess) return cuda_fail(e, "hb kernel launch");
-  PM_CUDA(cudaMemcpyAsync(h->pin_out, h->out_f, sizeof(double) * G, cudaMemcpyDeviceToHost, h->stream));
-  if (grad)
-    PM_CUDA(cudaMemcpyAsync(h->pin_out + G, h->out_g, sizeof(double) * size_t(G) * K, cudaMemcpyDeviceToHost,
-                            h->stream));
   PM_CUDA(cudaStreamSynchronize(h->stream));
   std::memcpy(f_out, h->pin_out, sizeof(double) * G);
   if (grad) std::memcpy(g_out, h->pin_out + G, sizeof(double) * size_t(G) * K);
