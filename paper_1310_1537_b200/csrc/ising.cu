@@ -402,21 +402,56 @@ __device__ inline void lat_xchg_publish(const PackedArgs& a) {
 // ---------------------------------------------------------------- layout conversion
 // grid [H][W] <-> packed colour arrays.  par0 = global row of grid row 0 (colour parity),
 // aoff = array row of grid row 0 (1 for strips, whose arrays start with a halo row).
+// One thread per (row, pair of columns): the two sites of a pair have opposite colours, so
+// the thread moves one byte to each colour array (no 64-bit division per site).
 __global__ void pack_kernel(const int8_t* __restrict__ grid, int H, int W, int8_t* pk0, int8_t* pk1, int par0,
                             int aoff) {
-  const int64_t n = int64_t(H) * W;
+  const int W2 = W >> 1;
+  const int64_t n = int64_t(H) * W2;
   for (int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < n; f += int64_t(gridDim.x) * blockDim.x) {
-    const int i = int(f / W), j = int(f % W);
-    ((par0 + i + j) & 1 ? pk1 : pk0)[int64_t(i + aoff) * (W >> 1) + (j >> 1)] = grid[f];
+    const int i = int(f / W2), q = int(f - int64_t(i) * W2);
+    const char2 v = reinterpret_cast<const char2*>(grid + int64_t(i) * W)[q];
+    const int8_t* src = reinterpret_cast<const int8_t*>(&v);
+    const int c0 = (par0 + i) & 1;  // colour of column 2q
+    const int64_t o = int64_t(i + aoff) * W2 + q;
+    (c0 ? pk1 : pk0)[o] = src[0];
+    (c0 ? pk0 : pk1)[o] = src[1];
   }
 }
 __global__ void unpack_kernel(int8_t* __restrict__ grid, int H, int W, const int8_t* pk0, const int8_t* pk1,
                               int par0, int aoff) {
-  const int64_t n = int64_t(H) * W;
+  const int W2 = W >> 1;
+  const int64_t n = int64_t(H) * W2;
   for (int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < n; f += int64_t(gridDim.x) * blockDim.x) {
-    const int i = int(f / W), j = int(f % W);
-    grid[f] = ((par0 + i + j) & 1 ? pk1 : pk0)[int64_t(i + aoff) * (W >> 1) + (j >> 1)];
+    const int i = int(f / W2), q = int(f - int64_t(i) * W2);
+    const int c0 = (par0 + i) & 1;
+    const int64_t o = int64_t(i + aoff) * W2 + q;
+    char2 v;
+    v.x = (c0 ? pk1 : pk0)[o];
+    v.y = (c0 ? pk0 : pk1)[o];
+    reinterpret_cast<char2*>(grid + int64_t(i) * W)[q] = v;
   }
+}
+// count of invalid values (Ising: not +-1; Potts: not 0..3) in n bytes, 16 at a time
+__global__ void count_invalid_spins_kernel(const int8_t* __restrict__ s, int64_t n, int potts,
+                                           unsigned long long* bad) {
+  unsigned long long local = 0;
+  const int64_t n16 = n / 16;
+  for (int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < n16; f += int64_t(gridDim.x) * blockDim.x) {
+    const uint4 v = reinterpret_cast<const uint4*>(s)[f];
+    for (uint32_t w : {v.x, v.y, v.z, v.w}) {
+      for (int b = 0; b < 4; ++b) {
+        const int8_t x = int8_t(w >> (8 * b));
+        local += potts ? !(x >= 0 && x <= 3) : !(x == 1 || x == -1);
+      }
+    }
+  }
+  for (int64_t f = n16 * 16 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < n;
+       f += int64_t(gridDim.x) * blockDim.x) {
+    const int8_t x = s[f];
+    local += potts ? !(x >= 0 && x <= 3) : !(x == 1 || x == -1);
+  }
+  if (local) atomicAdd(bad, local);
 }
 
 // ---------------------------------------------------------------- host tables
@@ -612,19 +647,31 @@ int pm_lat_destroy(pm_lat_t h) {
 int pm_lat_set_spins(pm_lat_t h, const int8_t* s) {
   if (!h || !s) return fail(PM_EINVAL, "null argument");
   const int64_t n = int64_t(h->H) * h->W;
-  for (int64_t f = 0; f < n; ++f) {
-    if (h->model == PM_MODEL_ISING ? !(s[f] == 1 || s[f] == -1) : !(s[f] >= 0 && s[f] <= 3))
-      return fail(PM_EINVAL, h->model == PM_MODEL_ISING ? "spins must be -1 or +1" : "Potts states must be 0..3");
-  }
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard g(h->device);
+  // validated on the device (the reference checks the values, ising.py:64-70) before the
+  // lattice state is touched: upload to the staging buffer, count invalid values, then pack
+  if (!h->scratch) PM_CUDA(cudaMalloc(&h->scratch, size_t(n) + 16));
+  unsigned long long* bad = nullptr;
+  PM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(unsigned long long), h->stream));
+  PM_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned long long), h->stream));
+  PM_CUDA(cudaMemcpyAsync(h->scratch, s, n, cudaMemcpyHostToDevice, h->stream));
+  count_invalid_spins_kernel<<<grid_for(h, n / 16 + 1), 256, 0, h->stream>>>(h->scratch, n,
+                                                                             h->model == PM_MODEL_POTTS4, bad);
+  unsigned long long nbad = 0;
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&nbad, bad, sizeof(nbad), cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaFreeAsync(bad, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "pm_lat_set_spins");
+  if (nbad) return fail(PM_EINVAL, h->model == PM_MODEL_ISING ? "spins must be -1 or +1" : "Potts states must be 0..3");
   if (h->packed) {
-    PM_CUDA(cudaMemcpyAsync(h->scratch, s, n, cudaMemcpyHostToDevice, h->stream));
-    pack_kernel<<<grid_for(h, n), 256, 0, h->stream>>>(h->scratch, h->H, h->W, h->pk0, h->pk1, h->row0, h->strip);
-    PM_CUDA(cudaGetLastError());
+    pack_kernel<<<grid_for(h, n / 2), 256, 0, h->stream>>>(h->scratch, h->H, h->W, h->pk0, h->pk1, h->row0,
+                                                          h->strip);
   } else {
-    PM_CUDA(cudaMemcpyAsync(h->pk0, s, n, cudaMemcpyHostToDevice, h->stream));
+    PM_CUDA(cudaMemcpyAsync(h->pk0, h->scratch, n, cudaMemcpyDeviceToDevice, h->stream));
   }
+  PM_CUDA(cudaGetLastError());
   PM_CUDA(cudaStreamSynchronize(h->stream));
   return PM_OK;
 }
@@ -635,8 +682,8 @@ int pm_lat_get_spins(pm_lat_t h, int8_t* s) {
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard g(h->device);
   if (h->packed) {
-    unpack_kernel<<<grid_for(h, n), 256, 0, h->stream>>>(h->scratch, h->H, h->W, h->pk0, h->pk1, h->row0,
-                                                         h->strip);
+    unpack_kernel<<<grid_for(h, n / 2), 256, 0, h->stream>>>(h->scratch, h->H, h->W, h->pk0, h->pk1, h->row0,
+                                                             h->strip);
     PM_CUDA(cudaGetLastError());
     PM_CUDA(cudaMemcpyAsync(s, h->scratch, n, cudaMemcpyDeviceToHost, h->stream));
   } else {

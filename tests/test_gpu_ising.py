@@ -259,3 +259,25 @@ def test_strips_peer_halo_exchange_match_single_lattice(gpu, n_strips, model):
     np.testing.assert_array_equal(got, ref)
     for s in strips:
         s.close()
+
+
+@pytest.mark.parametrize("model", ["ising", "potts"])
+def test_set_spins_rejects_invalid_values_on_device(gpu, model):
+    """pm_lat_set_spins validates on the device before touching the lattice: an invalid
+    value raises ValueError (the reference's check, ising.py:64-70) and the state stays."""
+    if model == "ising":
+        s0 = ising_spins(64, 96, seed=4)
+        lat = IsingLattice(s0, np.zeros(s0.shape), 0.5, boundary="periodic")
+    else:
+        s0 = potts_states(64, 96, seed=4)
+        lat = PottsLattice(s0, 0.7, boundary="periodic")
+    part = color_lattice(lat)
+    dev = part.device
+    dev.set_spins(s0)
+    invalid = (0, 5, -2) if model == "ising" else (-1, 5, 4)
+    for pos, v in zip(((0, 0), (63, 95), (17, 33)), invalid):
+        bad = s0.copy()
+        bad[pos] = v
+        with pytest.raises(ValueError):
+            dev.set_spins(bad)
+        np.testing.assert_array_equal(dev.get_spins(), s0)
