@@ -35,6 +35,11 @@ bool pdl_default() {
 }
 
 constexpr int kPottsIdx = 625;  // n0 + 5 n1 + 25 n2 + 125 n3, n_a in 0..4
+// Packed fast path: a neighbour in state a contributes code {0, 1, 5, 21}[a]; the 35
+// neighbour multisets (n0 + n1 + n2 + n3 = 4) have distinct code sums n1 + 5 n2 + 21 n3 <= 84,
+// so one byte per site indexes an 85-entry threshold table.
+constexpr int kPottsCodes = 85;
+constexpr uint32_t kPottsCodeBytes = 0x15050100u;  // bytes {0, 1, 5, 21}
 
 struct LatView {
   int8_t* pk0;  // packed colour 0  (W even) or grid (W odd)
@@ -213,16 +218,37 @@ __device__ __forceinline__ uint32_t pow5_bytes(uint32_t x) {
   return __byte_perm(0x7D190501u, 0u, sel);              // bytes {1, 5, 25, 125}[s]
 }
 
+__device__ __forceinline__ uint32_t lane_id() {
+  uint32_t l;
+  asm("mov.u32 %0, %%laneid;" : "=r"(l));
+  return l;
+}
+
+// prmt.b32 without __byte_perm's selector masking (selector nibbles here are 0..7)
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
+// Potts packed path: per byte, the compact code {0, 1, 5, 21}[state]
+__device__ __forceinline__ uint32_t code_bytes(uint32_t x) {
+  const uint32_t t = x | (x >> 4);                       // byte0 = s0 | s1<<4, byte2 = s2 | s3<<4
+  return prmt(kPottsCodeBytes, 0u, prmt(t, 0u, 0x0020u));
+}
+
 // Threshold tables in shared memory.  T32: every threshold ceil(p*2^32) is < 2^32 (checked on
 // the host), so the exact test u < p is the 32-bit compare word < T; otherwise 64-bit.
 template <int MODEL, bool T32>
 struct GibbsTables {
   // Ising: by number of -1 neighbours nd = 0..4 (nsum = 4 - 2 nd)
-  // Potts: by idx = sum of 5^state over the 4 neighbours; T32 packs the 3 thresholds in a uint4
+  // Potts T32: by the compact code sum e (0..84), threshold a of entry e replicated per lane at
+  //   word (3e + a) * 32 + lane, so every lane reads its own bank (random e, no conflicts)
+  // Potts 64-bit: by idx = sum of 5^state over the 4 neighbours
   using IsingT = typename std::conditional<T32, uint32_t, unsigned long long>::type;
   typename std::conditional<MODEL == PM_MODEL_ISING, IsingT[8],
-                            typename std::conditional<T32, uint4[kPottsIdx], unsigned long long[kPottsIdx * 3]>::type>::type
-      t;
+                            typename std::conditional<T32, uint32_t[kPottsCodes * 3 * 32],
+                                                      unsigned long long[kPottsIdx * 3]>::type>::type t;
 };
 
 // Thread = NG consecutive 16-site groups of one packed row (setup amortised over 16*NG sites).
@@ -235,7 +261,7 @@ __device__ inline void lat_xchg_publish(const PackedArgs& a);
 // XCHG: the strip peer-memory halo exchange (PackedArgs xmb ...) is compiled in
 template <int MODEL, bool T32, int NG, bool XCHG>
 __global__ void __launch_bounds__(256, NG == 1 ? 6 : 4)
-    gibbs_packed_kernel(PackedArgs a, const unsigned long long* __restrict__ pthr, const uint4* __restrict__ pthr32) {
+    gibbs_packed_kernel(PackedArgs a, const unsigned long long* __restrict__ pthr, const uint32_t* __restrict__ pcomp) {
   __shared__ GibbsTables<MODEL, T32> tb;
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   if constexpr (MODEL == PM_MODEL_ISING) {
@@ -245,8 +271,12 @@ __global__ void __launch_bounds__(256, NG == 1 ? 6 : 4)
       for (int k = 0; k < 5; ++k) tb.t[k] = a.thr[8 - 2 * k];
     }
   } else if constexpr (T32) {
+    // replicate the compact table (85 x 3 words) across the 32 lanes: 4 lanes per 16-byte store
     uint4* dst = reinterpret_cast<uint4*>(&tb.t[0]);
-    for (int t = tid; t < kPottsIdx; t += blockDim.x * blockDim.y) dst[t] = pthr32[t];
+    for (int t = tid; t < kPottsCodes * 3 * 8; t += blockDim.x * blockDim.y) {
+      const uint32_t v = __ldg(pcomp + (t >> 3));
+      dst[t] = make_uint4(v, v, v, v);
+    }
   } else {
     unsigned long long* dst = reinterpret_cast<unsigned long long*>(&tb.t[0]);
     for (int t = tid; t < kPottsIdx * 3; t += blockDim.x * blockDim.y) dst[t] = pthr[t];
@@ -334,25 +364,33 @@ __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const Gibb
       }
       out = 0xFFFFFFFFu - 0xFEu * plus_bits;  // per byte: 0x01 (+1) or 0xFF (-1), no borrows
     } else {
-      const uint32_t p1 = pow5_bytes(U[m]), p2 = pow5_bytes(D[m]);
-      const uint32_t p3 = pow5_bytes(cur), p4 = pow5_bytes(sh);
-      // two 16-bit lanes per word so the sums (<= 500) cannot overflow
-      const uint32_t ev = (p1 & 0x00FF00FFu) + (p2 & 0x00FF00FFu) + (p3 & 0x00FF00FFu) + (p4 & 0x00FF00FFu);
-      const uint32_t od = ((p1 >> 8) & 0x00FF00FFu) + ((p2 >> 8) & 0x00FF00FFu) + ((p3 >> 8) & 0x00FF00FFu) +
-                          ((p4 >> 8) & 0x00FF00FFu);
+      if constexpr (T32) {
+        // code sums <= 84 per byte: no carries
+        const uint32_t e4 = code_bytes(U[m]) + code_bytes(D[m]) + code_bytes(cur) + code_bytes(sh);
+        const uint32_t* lt = &tb.t[0] + lane_id();
+        uint32_t st[4];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const uint32_t idx = ((b & 1) ? od : ev) >> (16 * (b >> 1)) & 0xFFFFu;
-        const uint32_t w = blk.v[b];
-        uint32_t st;
-        if constexpr (T32) {
-          const uint4 th = reinterpret_cast<const uint4*>(&tb.t[0])[idx];
-          st = uint32_t(w >= th.x) + uint32_t(w >= th.y) + uint32_t(w >= th.z);
-        } else {
-          const unsigned long long* t3 = reinterpret_cast<const unsigned long long*>(&tb.t[0]) + idx * 3;
-          st = uint32_t(uint64_t(w) >= t3[0]) + uint32_t(uint64_t(w) >= t3[1]) + uint32_t(uint64_t(w) >= t3[2]);
+        for (int b = 0; b < 4; ++b) {
+          const uint32_t* t3 = lt + prmt(e4, 0u, 0x4440u + b) * 96;
+          const uint32_t w = blk.v[b];
+          st[b] = uint32_t(w >= t3[0]) + uint32_t(w >= t3[32]) + uint32_t(w >= t3[64]);
         }
-        out |= st << (8 * b);
+        out = prmt(prmt(st[0], st[1], 0x0040u), prmt(st[2], st[3], 0x0040u), 0x5410u);
+      } else {
+        const uint32_t p1 = pow5_bytes(U[m]), p2 = pow5_bytes(D[m]);
+        const uint32_t p3 = pow5_bytes(cur), p4 = pow5_bytes(sh);
+        // two 16-bit lanes per word so the sums (<= 500) cannot overflow
+        const uint32_t ev = (p1 & 0x00FF00FFu) + (p2 & 0x00FF00FFu) + (p3 & 0x00FF00FFu) + (p4 & 0x00FF00FFu);
+        const uint32_t od = ((p1 >> 8) & 0x00FF00FFu) + ((p2 >> 8) & 0x00FF00FFu) + ((p3 >> 8) & 0x00FF00FFu) +
+                            ((p4 >> 8) & 0x00FF00FFu);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const uint32_t idx = ((b & 1) ? od : ev) >> (16 * (b >> 1)) & 0xFFFFu;
+          const uint32_t w = blk.v[b];
+          const unsigned long long* t3 = reinterpret_cast<const unsigned long long*>(&tb.t[0]) + idx * 3;
+          const uint32_t st = uint32_t(uint64_t(w) >= t3[0]) + uint32_t(uint64_t(w) >= t3[1]) + uint32_t(uint64_t(w) >= t3[2]);
+          out |= st << (8 * b);
+        }
       }
     }
     res[m] = out;
@@ -517,7 +555,7 @@ struct pm_lat_s {
   bool has_potts = false;
   double* cdf = nullptr;
   unsigned long long* pthr = nullptr;
-  uint4* pthr32 = nullptr;    // Potts thresholds as (t0, t1, t2, 0) when all < 2^32
+  uint32_t* pthr32 = nullptr;  // Potts packed path: [85][3] thresholds by code sum, when all < 2^32
   bool pdl = pdl_default();   // packed half-sweeps launched with PDL (PM_PDL=0 disables)
   bool t32 = false;           // every threshold of the active model fits 32 bits
   // uniforms staging
@@ -753,18 +791,23 @@ int pm_lat_set_potts(pm_lat_t h, double coupling) {
     thr[t] = thr32(cdf[t]);
     if (thr[t] > 0xFFFFFFFFull) fits = false;
   }
-  std::vector<uint4> t4(kPottsIdx);
-  for (int i = 0; i < kPottsIdx; ++i)
-    t4[i] = make_uint4(uint32_t(thr[3 * i]), uint32_t(thr[3 * i + 1]), uint32_t(thr[3 * i + 2]), 0u);
+  // compact table of the packed path: entry n1 + 5 n2 + 21 n3 of the multiset (n0, n1, n2, n3)
+  std::vector<uint32_t> tc(kPottsCodes * 3, 0u);
+  for (int idx = 0; idx < kPottsIdx; ++idx) {
+    const int n0 = idx % 5, n1 = (idx / 5) % 5, n2 = (idx / 25) % 5, n3 = idx / 125;
+    if (n0 + n1 + n2 + n3 != 4) continue;
+    const int e = n1 + 5 * n2 + 21 * n3;
+    for (int a = 0; a < 3; ++a) tc[3 * e + a] = uint32_t(thr[3 * idx + a]);
+  }
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard g(h->device);
   cudaStreamSynchronize(h->stream);
   if (!h->cdf) PM_CUDA(cudaMalloc(&h->cdf, sizeof(double) * kPottsIdx * 3));
   if (!h->pthr) PM_CUDA(cudaMalloc(&h->pthr, sizeof(unsigned long long) * kPottsIdx * 3));
-  if (!h->pthr32) PM_CUDA(cudaMalloc(&h->pthr32, sizeof(uint4) * kPottsIdx));
+  if (!h->pthr32) PM_CUDA(cudaMalloc(&h->pthr32, sizeof(uint32_t) * kPottsCodes * 3));
   PM_CUDA(cudaMemcpy(h->cdf, cdf.data(), sizeof(double) * kPottsIdx * 3, cudaMemcpyHostToDevice));
   PM_CUDA(cudaMemcpy(h->pthr, thr.data(), sizeof(unsigned long long) * kPottsIdx * 3, cudaMemcpyHostToDevice));
-  PM_CUDA(cudaMemcpy(h->pthr32, t4.data(), sizeof(uint4) * kPottsIdx, cudaMemcpyHostToDevice));
+  PM_CUDA(cudaMemcpy(h->pthr32, tc.data(), sizeof(uint32_t) * kPottsCodes * 3, cudaMemcpyHostToDevice));
   h->t32 = fits;
   h->has_potts = true;
   return PM_OK;
@@ -808,7 +851,12 @@ static void launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t seed, cud
     pa.status = h->xticket + 1;
   }
   const int W2 = h->W / 2;
-  const int ng = (W2 % 64 == 0) ? 4 : (W2 % 32 == 0) ? 2 : 1;   // 16-site groups per thread
+  static const int ng_cap = [] {  // PM_GIBBS_NG=1|2|4 caps the groups per thread (A/B knob)
+    const char* e = std::getenv("PM_GIBBS_NG");
+    const int v = e ? std::atoi(e) : 4;
+    return (v == 1 || v == 2) ? v : 4;
+  }();
+  const int ng = (W2 % 64 == 0 && ng_cap >= 4) ? 4 : (W2 % 32 == 0 && ng_cap >= 2) ? 2 : 1;  // 16-site groups per thread
   const int per_row = W2 / (16 * ng);
   const int bx = std::min(256, per_row);
   const int by = std::max(1, 256 / bx);
@@ -818,9 +866,9 @@ static void launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t seed, cud
   cudaError_t e = cudaSuccess;  // a failed launch is also the thread's last error (callers check it)
 #define PM_LAUNCH_PACKED(M, T, N)                                                                      \
   e = pa.xmb ? launch_pdl(h->pdl, gibbs_packed_kernel<M, T, N, true>, grid, block, 0, st, pa,          \
-                          (const unsigned long long*)h->pthr, (const uint4*)h->pthr32)                 \
+                          (const unsigned long long*)h->pthr, (const uint32_t*)h->pthr32)                 \
              : launch_pdl(h->pdl, gibbs_packed_kernel<M, T, N, false>, grid, block, 0, st, pa,         \
-                          (const unsigned long long*)h->pthr, (const uint4*)h->pthr32)
+                          (const unsigned long long*)h->pthr, (const uint32_t*)h->pthr32)
 #define PM_LAUNCH_NG(M, T)            \
   do {                                \
     if (ng == 4)                      \
