@@ -98,15 +98,16 @@ def load_traffic(key: str):
 
 def issue_roofline(config: str, ms_per_sweep: float, clk: dict):
     """The Gibbs sweep's real bound: warp instructions issued per second (ncu count of one
-    Ising half-sweep launch, profiles/traffic.json) against 148 SMs x 4 schedulers x the
+    Ising / Potts half-sweep launch, profiles/traffic.json) against 148 SMs x 4 schedulers x the
     median SM clock sampled during the timed region."""
-    n = load_traffic("c4_warp_inst_per_half_sweep") if config == "c4" else None
+    n = load_traffic(f"{config}_warp_inst_per_half_sweep") if config in ("c4", "c4potts") else None
     if not n or not clk or not clk.get("sm_mhz"):
         return None
     achieved = 2 * n / (ms_per_sweep * 1e-3)
     peak = 148 * 4 * clk["sm_mhz"] * 1e6
     return {"achieved": achieved, "peak": peak, "unit": "warp instructions/s", "frac": achieved / peak,
-            "source": "ncu smsp__inst_executed.sum per half-sweep (profiles/r01_ncu_gibbs_packed_raw.csv)"}
+            "source": "ncu smsp__inst_executed.sum per half-sweep (profiles/r01_ncu_gibbs_%s_raw.csv)"
+            % ("packed" if config == "c4" else "potts")}
 
 
 # ---------------------------------------------------------------------------- clocks
