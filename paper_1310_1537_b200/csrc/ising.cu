@@ -34,6 +34,15 @@ bool pdl_default() {
   return !(e && e[0] == '0');
 }
 
+// Resident CTAs per SM the packed kernel is register-budgeted for (NG >= 2): Ising 4
+// (64 registers), Potts 3 (80 registers, no spills): profiles/r01_ab_gibbs_minb.txt
+#ifndef PM_GIBBS_MINB_ISING
+#define PM_GIBBS_MINB_ISING 4
+#endif
+#ifndef PM_GIBBS_MINB_POTTS
+#define PM_GIBBS_MINB_POTTS 3
+#endif
+
 constexpr int kPottsIdx = 625;  // n0 + 5 n1 + 25 n2 + 125 n3, n_a in 0..4
 // Packed fast path: a neighbour in state a contributes code {0, 1, 5, 21}[a]; the 35
 // neighbour multisets (n0 + n1 + n2 + n3 = 4) have distinct code sums n1 + 5 n2 + 21 n3 <= 84,
@@ -260,7 +269,7 @@ __device__ inline void lat_xchg_publish(const PackedArgs& a);
 
 // XCHG: the strip peer-memory halo exchange (PackedArgs xmb ...) is compiled in
 template <int MODEL, bool T32, int NG, bool XCHG>
-__global__ void __launch_bounds__(256, NG == 1 ? 6 : 4)
+__global__ void __launch_bounds__(256, NG == 1 ? 6 : MODEL == PM_MODEL_ISING ? PM_GIBBS_MINB_ISING : PM_GIBBS_MINB_POTTS)
     gibbs_packed_kernel(PackedArgs a, const unsigned long long* __restrict__ pthr, const uint32_t* __restrict__ pcomp) {
   __shared__ GibbsTables<MODEL, T32> tb;
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
@@ -851,11 +860,14 @@ static void launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t seed, cud
     pa.status = h->xticket + 1;
   }
   const int W2 = h->W / 2;
-  static const int ng_cap = [] {  // PM_GIBBS_NG=1|2|4 caps the groups per thread (A/B knob)
+  // 16-site groups per thread: Ising 2, Potts 4 (profiles/r01_ab_gibbs_minb.txt);
+  // PM_GIBBS_NG=1|2|4 overrides (A/B knob)
+  static const int ng_env = [] {
     const char* e = std::getenv("PM_GIBBS_NG");
-    const int v = e ? std::atoi(e) : 4;
-    return (v == 1 || v == 2) ? v : 4;
+    const int v = e ? std::atoi(e) : 0;
+    return (v == 1 || v == 2 || v == 4) ? v : 0;
   }();
+  const int ng_cap = ng_env ? ng_env : (h->model == PM_MODEL_ISING ? 2 : 4);
   const int ng = (W2 % 64 == 0 && ng_cap >= 4) ? 4 : (W2 % 32 == 0 && ng_cap >= 2) ? 2 : 1;  // 16-site groups per thread
   const int per_row = W2 / (16 * ng);
   const int bx = std::min(256, per_row);
