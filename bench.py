@@ -96,6 +96,23 @@ def load_traffic(key: str):
         return None
 
 
+class L2Scrub:
+    """Evicts the inputs from L2 between timed launches: a 512 MiB write (larger than the
+    126 MB L2), then a 256 MiB read of a second buffer so the timed launch does not pay
+    for writing the scrub's dirty lines back to HBM (cold inputs, clean L2)."""
+
+    def __init__(self, device):
+        import torch
+        self.torch = torch
+        self.dirty = torch.empty(512 << 20, dtype=torch.uint8, device=device)
+        self.clean = torch.ones(256 << 20, dtype=torch.uint8, device=device)
+
+    def __call__(self):
+        self.dirty.zero_()
+        self.clean.max()
+        self.torch.cuda.synchronize(self.dirty.device)
+
+
 def issue_roofline(config: str, ms_per_sweep: float, clk: dict):
     """The Gibbs sweep's real bound: warp instructions issued per second (ncu count of one
     Ising / Potts half-sweep launch, profiles/traffic.json) against 148 SMs x 4 schedulers x the
@@ -421,11 +438,7 @@ def run_glm(args, cfg):
     block = np.ascontiguousarray(betas[warmup:warmup + steps])
     xs_bytes = 8 if cfg["x_storage"] == "f64" else 4
     flush_l2 = n_local * (k * xs_bytes + 8) < 256e6   # inputs not larger than the 126 MB L2
-    scrub = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local}") if flush_l2 else None
-
-    def flush():
-        scrub.zero_()                                  # 512 MiB write evicts X and y from L2
-        torch.cuda.synchronize(local)
+    flush = L2Scrub(f"cuda:{local}") if flush_l2 else None   # evicts X and y from L2
 
     if not dist_mode and flush_l2:
         # one launch at a time, L2 flushed before each, CUDA events around the launch only
@@ -502,7 +515,7 @@ def run_glm(args, cfg):
             "data": "synthetic (SURVEY §8d generator: X[:,0]=1, X[:,1:]~N(0,1), y~Bern(sigmoid(X beta_true)))",
             "config": {"workload": cfg["desc"], "N": n_full, "K": k, "rows_per_gpu": n_local,
                        "x_storage": cfg["x_storage"], "parallelism": f"row-shard x{ws}",
-                       "l2": (f"L2 flushed (512 MiB write) before every timed evaluation; inputs "
+                       "l2": (f"L2 flushed (512 MiB write + 256 MiB read of a clean buffer) before every timed evaluation; inputs "
                               f"{bytes_eval_local/1e6:.1f} MB < L2" if flush_l2 else
                               f"inputs larger than L2 ({bytes_eval_local/1e9:.2f} GB per GPU per eval)"),
                        "prior": "N(0, 10^2) iid", "beta": "fresh N(0, 0.1^2) per step"},
@@ -710,14 +723,13 @@ def run_gibbs(args, cfg):
     clk = clocks.stop()
     # cold-L2 variant: the 2 x 32 MiB lattice state is L2-resident across sweeps by design;
     # also time single sweeps after evicting it (512 MiB write)
-    scrub = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    flush = L2Scrub(f"cuda:{local}")
     cold_ms = 0.0
     n_cold = min(50, args.steps)
     for t in range(n_cold):
-        scrub.zero_()
-        torch.cuda.synchronize()
+        flush()
         cold_ms += dev.time_sweeps(1, 2, rng.seed, 0, rng.sweep + args.steps + t)
-    del scrub
+    del flush
     # end to end: spins in from host, sweeps, spins out
     t0 = time.perf_counter()
     part.pack_from(lat)
@@ -734,7 +746,7 @@ def run_gibbs(args, cfg):
             "data": "synthetic iid uniform initial state",
             "config": {"workload": cfg["desc"], "H": h, "W": w, "beta_J": 0.4407,
                        "l2": "lattice state (2 x 32 MiB packed int8) is L2-resident across the sweeps by design; "
-                             "cold_l2_sweeps_per_s flushes L2 (512 MiB write) before each timed sweep"},
+                             "cold_l2_sweeps_per_s flushes L2 (512 MiB write + 256 MiB clean read) before each timed sweep"},
             "cold_l2_sweeps_per_s": 1000.0 * n_cold / cold_ms,
             "msite_per_s": h * w / (ms * 1e-3) / 1e6,
             "roofline": {"bound": "issue (Philox4x32) -- HBM fraction reported for context",
