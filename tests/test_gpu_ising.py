@@ -120,11 +120,14 @@ def test_odd_width_and_random_bias_against_oracle(gpu):
         np.testing.assert_array_equal(lat.s, ref)
 
 
-@pytest.mark.parametrize("periodic,shape", [(True, (32, 32)), (True, (64, 128)), (False, (9, 11)),
-                                            (True, (6, 10)), (False, (32, 64))])
-def test_potts_matches_c_oracle(gpu, periodic, shape):
+# packed fast path: (32, 32) -> 16-site groups NG=1, (96, 64) -> NG=2, (64, 128) -> NG=4;
+# coupling 40 puts thresholds at 2^32 (cdf rounds to 1), so the 64-bit threshold table is used
+@pytest.mark.parametrize("periodic,shape,coupling", [(True, (32, 32), 1.0986), (True, (64, 128), 1.0986),
+                                                     (True, (96, 64), 1.0986), (False, (9, 11), 1.0986),
+                                                     (True, (6, 10), 1.0986), (False, (32, 64), 1.0986),
+                                                     (True, (64, 128), 40.0), (True, (96, 64), 40.0)])
+def test_potts_matches_c_oracle(gpu, periodic, shape, coupling):
     s0 = potts_states(*shape, seed=1)
-    coupling = 1.0986
     lat = PottsLattice(s0, coupling, boundary="periodic" if periodic else "free")
     part = color_lattice(lat)
     ising.potts_sweeps(lat, part, SitePhilox(77), 40)

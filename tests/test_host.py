@@ -159,3 +159,19 @@ def test_run_region_contract():
     assert run_region([lambda: run_region([lambda: 1, lambda: 2]), lambda: [3]]) == [[1, 2], [3]]
     assert run_region([]) == []
     del before
+
+
+def test_potts_compact_code_sums_are_unique():
+    """The packed Potts kernel indexes its threshold table by the sum of per-neighbour codes
+    {0, 1, 5, 21}[state] (ising.cu kPottsCodeBytes): the 35 neighbour multisets of q=4 states
+    over 4 neighbours must give distinct sums that fit one byte and the 85-entry table."""
+    import itertools
+    codes = (0, 1, 5, 21)
+    sums = {}
+    for ms in itertools.combinations_with_replacement(range(4), 4):
+        e = sum(codes[a] for a in ms)
+        assert e not in sums, (ms, sums.get(e))
+        sums[e] = ms
+    assert len(sums) == 35 and max(sums) == 84
+    # the byte constant holds the codes in state order
+    assert [(0x15050100 >> (8 * a)) & 0xFF for a in range(4)] == list(codes)
