@@ -345,7 +345,10 @@ __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const Gibb
   const int o = (i + a.colour) & 1;
   const int qe = o ? ((q0 + 16 * NG == a.W2) ? 0 : q0 + 16 * NG) : ((q0 == 0) ? a.W2 - 1 : q0 - 1);
   const uint32_t edge = uint32_t(uint8_t(__ldg(orow + qe)));
-  const uint64_t g0 = (uint64_t(a.colour) * uint64_t(a.n0) + uint64_t(i) * a.W2 + q0) >> 2;  // Philox block
+  // Philox block of the first word.  The packed path only runs on lattices with fewer than
+  // 2^34 - 256 sites (packed_blocks_fit), so every block index of the half-sweep fits 32 bits:
+  // the counter's high word is 0 and g0 + m is a 32-bit add (no carry chain per word)
+  const uint32_t g0 = uint32_t((uint64_t(a.colour) * uint64_t(a.n0) + uint64_t(i) * a.W2 + q0) >> 2);
   uint32_t res[NW];
 #pragma unroll
   for (int m = 0; m < NW; ++m) {
@@ -353,7 +356,7 @@ __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const Gibb
     // byte b of `sh` = the other horizontal neighbour of site 4m+b (funnel shift across words)
     const uint32_t sh = o == 0 ? __funnelshift_l(m == 0 ? (edge << 24) : M[m - 1], cur, 8)
                                : __funnelshift_r(cur, m == NW - 1 ? edge : M[m + 1], 8);
-    const U32x4 blk = site_philox_block(g0 + m, a.sweep, a.seed);
+    const U32x4 blk = site_philox_block(uint64_t(g0 + uint32_t(m)), a.sweep, a.seed);
     uint32_t out = 0;
     if constexpr (MODEL == PM_MODEL_ISING) {
       // per byte: bit 1 is set for a -1 spin (0xFF) and clear for +1 (0x01), so the masked
@@ -616,8 +619,13 @@ LatView view_of(pm_lat_s* h) {
   return v;
 }
 
+// Philox4x32 block indices (site / 4) of a whole lattice fit 32 bits with margin for a
+// thread's words: the packed kernel's 32-bit counter arithmetic
+bool packed_blocks_fit(int64_t H, int64_t W) { return H * W / 4 < (int64_t(1) << 32) - 64; }
+
 bool fast_path_ok(pm_lat_s* h) {
   return h->packed && h->boundary == PM_BOUNDARY_PERIODIC && (h->H % 2 == 0) && ((h->W / 2) % 16 == 0) &&
+         packed_blocks_fit(h->strip ? h->H_global : h->H, h->W) &&
          (h->model == PM_MODEL_POTTS4 || h->n_class == 1);
 }
 
@@ -911,6 +919,7 @@ int pm_lat_create_strip(int device, int32_t height, int32_t width, int32_t row0,
   if ((width / 2) % 16) return fail(PM_EINVAL, "strips need width % 32 == 0 (16-site packed groups)");
   if (rows < 1 || row0 < 0 || row0 + rows > height) return fail(PM_ERANGE, "strip rows out of range");
   if (model != PM_MODEL_ISING && model != PM_MODEL_POTTS4) return fail(PM_EINVAL, "bad model");
+  if (!packed_blocks_fit(height, width)) return fail(PM_EINVAL, "strips need a lattice of fewer than 2^34 sites");
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
