@@ -50,19 +50,29 @@ constexpr int kPottsIdx = 625;  // n0 + 5 n1 + 25 n2 + 125 n3, n_a in 0..4
 constexpr int kPottsCodes = 85;
 constexpr uint32_t kPottsCodeBytes = 0x15050100u;  // bytes {0, 1, 5, 21}
 
+// Packed Ising colour arrays store e = 1 - s per site (0x00 for +1, 0x02 for -1): the packed
+// kernel's neighbour count is then a plain byte-wise sum of 4 words (2 per -1 neighbour, no
+// masks).  pack/unpack and LatView convert; Potts states and unpacked grids are stored as is.
+__host__ __device__ __forceinline__ int8_t enc_spin(int8_t v, int enc) { return enc ? int8_t(1 - v) : v; }
+
 struct LatView {
   int8_t* pk0;  // packed colour 0  (W even) or grid (W odd)
   int8_t* pk1;  // packed colour 1  (W even)
   int H, W, W2;
   int packed;
 
+  int enc;     // packed Ising arrays hold 1 - s (0x00 for +1, 0x02 for -1; see enc_spin)
+
   __device__ __forceinline__ int8_t get(int i, int j) const {
-    if (packed) return ((i + j) & 1 ? pk1 : pk0)[int64_t(i) * W2 + (j >> 1)];
+    if (packed) {
+      const int8_t v = ((i + j) & 1 ? pk1 : pk0)[int64_t(i) * W2 + (j >> 1)];
+      return enc ? int8_t(1 - v) : v;
+    }
     return pk0[int64_t(i) * W + j];
   }
   __device__ __forceinline__ void set(int i, int j, int8_t v) const {
     if (packed)
-      ((i + j) & 1 ? pk1 : pk0)[int64_t(i) * W2 + (j >> 1)] = v;
+      ((i + j) & 1 ? pk1 : pk0)[int64_t(i) * W2 + (j >> 1)] = enc ? int8_t(1 - v) : v;
     else
       pk0[int64_t(i) * W + j] = v;
   }
@@ -217,8 +227,6 @@ __device__ __forceinline__ uint32_t w_of(const uint4& v, int m) {
   return m == 0 ? v.x : m == 1 ? v.y : m == 2 ? v.z : v.w;
 }
 
-// Ising: per byte, 1 if the spin is -1 (0xFF) and 0 if +1 (0x01): bit 1 of each byte.
-__device__ __forceinline__ uint32_t down_bits(uint32_t x) { return (x >> 1) & 0x01010101u; }
 
 // Potts: per byte, 5^state for states 0..3 (PRMT table lookup, selector nibbles = states).
 __device__ __forceinline__ uint32_t pow5_bytes(uint32_t x) {
@@ -359,12 +367,11 @@ __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const Gibb
     const U32x4 blk = site_philox_block(uint64_t(g0 + uint32_t(m)), a.sweep, a.seed);
     uint32_t out = 0;
     if constexpr (MODEL == PM_MODEL_ISING) {
-      // per byte: bit 1 is set for a -1 spin (0xFF) and clear for +1 (0x01), so the masked
-      // 4-way sum is 2 x (number of -1 neighbours) <= 8 per byte (no carries); scaled to the
+      // packed bytes are 1 - s (0x02 for -1, 0x00 for +1), so the plain 4-way byte sum is
+      // 2 x (number of -1 neighbours) <= 8 per byte (no carries, no masks); scaled to the
       // table's byte offset (x4 for u32 thresholds, x8 for u64) it is the LDS address offset
-      constexpr uint32_t M2 = 0x02020202u;
       constexpr int SH = T32 ? 1 : 2;
-      const uint32_t off = ((U[m] & M2) + (D[m] & M2) + (cur & M2) + (sh & M2)) << SH;
+      const uint32_t off = (U[m] + D[m] + cur + sh) << SH;
       const char* tbase = reinterpret_cast<const char*>(&tb.t[0]);
       uint32_t plus_bits = 0;  // bit 8b set <=> site b becomes +1
 #pragma unroll
@@ -378,7 +385,7 @@ __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const Gibb
         }
         plus_bits |= plus ? (1u << (8 * b)) : 0u;
       }
-      out = 0xFFFFFFFFu - 0xFEu * plus_bits;  // per byte: 0x01 (+1) or 0xFF (-1), no borrows
+      out = 0x02020202u - 2u * plus_bits;  // per byte: 0x00 (+1) or 0x02 (-1), no borrows
     } else {
       if constexpr (T32) {
         // code sums <= 84 per byte: no carries
@@ -459,7 +466,7 @@ __device__ inline void lat_xchg_publish(const PackedArgs& a) {
 // One thread per (row, pair of columns): the two sites of a pair have opposite colours, so
 // the thread moves one byte to each colour array (no 64-bit division per site).
 __global__ void pack_kernel(const int8_t* __restrict__ grid, int H, int W, int8_t* pk0, int8_t* pk1, int par0,
-                            int aoff) {
+                            int aoff, int enc) {
   const int W2 = W >> 1;
   const int64_t n = int64_t(H) * W2;
   for (int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < n; f += int64_t(gridDim.x) * blockDim.x) {
@@ -468,12 +475,12 @@ __global__ void pack_kernel(const int8_t* __restrict__ grid, int H, int W, int8_
     const int8_t* src = reinterpret_cast<const int8_t*>(&v);
     const int c0 = (par0 + i) & 1;  // colour of column 2q
     const int64_t o = int64_t(i + aoff) * W2 + q;
-    (c0 ? pk1 : pk0)[o] = src[0];
-    (c0 ? pk0 : pk1)[o] = src[1];
+    (c0 ? pk1 : pk0)[o] = enc_spin(src[0], enc);
+    (c0 ? pk0 : pk1)[o] = enc_spin(src[1], enc);
   }
 }
 __global__ void unpack_kernel(int8_t* __restrict__ grid, int H, int W, const int8_t* pk0, const int8_t* pk1,
-                              int par0, int aoff) {
+                              int par0, int aoff, int enc) {
   const int W2 = W >> 1;
   const int64_t n = int64_t(H) * W2;
   for (int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < n; f += int64_t(gridDim.x) * blockDim.x) {
@@ -481,8 +488,8 @@ __global__ void unpack_kernel(int8_t* __restrict__ grid, int H, int W, const int
     const int c0 = (par0 + i) & 1;
     const int64_t o = int64_t(i + aoff) * W2 + q;
     char2 v;
-    v.x = (c0 ? pk1 : pk0)[o];
-    v.y = (c0 ? pk0 : pk1)[o];
+    v.x = enc_spin((c0 ? pk1 : pk0)[o], enc);
+    v.y = enc_spin((c0 ? pk0 : pk1)[o], enc);
     reinterpret_cast<char2*>(grid + int64_t(i) * W)[q] = v;
   }
 }
@@ -616,6 +623,7 @@ LatView view_of(pm_lat_s* h) {
   v.W = h->W;
   v.W2 = h->W / 2;
   v.packed = h->packed;
+  v.enc = h->packed && h->model == PM_MODEL_ISING;
   return v;
 }
 
@@ -726,7 +734,7 @@ int pm_lat_set_spins(pm_lat_t h, const int8_t* s) {
   if (nbad) return fail(PM_EINVAL, h->model == PM_MODEL_ISING ? "spins must be -1 or +1" : "Potts states must be 0..3");
   if (h->packed) {
     pack_kernel<<<grid_for(h, n / 2), 256, 0, h->stream>>>(h->scratch, h->H, h->W, h->pk0, h->pk1, h->row0,
-                                                          h->strip);
+                                                          h->strip, h->model == PM_MODEL_ISING);
   } else {
     PM_CUDA(cudaMemcpyAsync(h->pk0, h->scratch, n, cudaMemcpyDeviceToDevice, h->stream));
   }
@@ -742,7 +750,7 @@ int pm_lat_get_spins(pm_lat_t h, int8_t* s) {
   DeviceGuard g(h->device);
   if (h->packed) {
     unpack_kernel<<<grid_for(h, n / 2), 256, 0, h->stream>>>(h->scratch, h->H, h->W, h->pk0, h->pk1, h->row0,
-                                                             h->strip);
+                                                             h->strip, h->model == PM_MODEL_ISING);
     PM_CUDA(cudaGetLastError());
     PM_CUDA(cudaMemcpyAsync(s, h->scratch, n, cudaMemcpyDeviceToHost, h->stream));
   } else {
