@@ -50,10 +50,17 @@ constexpr int kPottsIdx = 625;  // n0 + 5 n1 + 25 n2 + 125 n3, n_a in 0..4
 constexpr int kPottsCodes = 85;
 constexpr uint32_t kPottsCodeBytes = 0x15050100u;  // bytes {0, 1, 5, 21}
 
-// Packed Ising colour arrays store e = 1 - s per site (0x00 for +1, 0x02 for -1): the packed
-// kernel's neighbour count is then a plain byte-wise sum of 4 words (2 per -1 neighbour, no
-// masks).  pack/unpack and LatView convert; Potts states and unpacked grids are stored as is.
-__host__ __device__ __forceinline__ int8_t enc_spin(int8_t v, int enc) { return enc ? int8_t(1 - v) : v; }
+// Packed colour arrays store an encoding of each site's value so that the packed kernel's
+// neighbour statistic is a plain byte-wise sum of 4 words (no masks, no per-byte lookups):
+//   enc 1 (Ising): e = 1 - s (0x00 for +1, 0x02 for -1): the sum is 2 x (number of -1's);
+//   enc 2 (Potts q=4): e = {0, 1, 5, 21}[state], the compact code (kPottsCodeBytes).
+// pack/unpack and LatView convert; unpacked grids (odd W) are stored as is (enc 0).
+__host__ __device__ __forceinline__ int8_t enc_site(int8_t v, int enc) {
+  return enc == 1 ? int8_t(1 - v) : enc == 2 ? int8_t(v == 0 ? 0 : v == 1 ? 1 : v == 2 ? 5 : 21) : v;
+}
+__host__ __device__ __forceinline__ int8_t dec_site(int8_t e, int enc) {
+  return enc == 1 ? int8_t(1 - e) : enc == 2 ? int8_t(e == 0 ? 0 : e == 1 ? 1 : e == 5 ? 2 : 3) : e;
+}
 
 struct LatView {
   int8_t* pk0;  // packed colour 0  (W even) or grid (W odd)
@@ -61,18 +68,18 @@ struct LatView {
   int H, W, W2;
   int packed;
 
-  int enc;     // packed Ising arrays hold 1 - s (0x00 for +1, 0x02 for -1; see enc_spin)
+  int enc;     // packed byte encoding (enc_site / dec_site)
 
   __device__ __forceinline__ int8_t get(int i, int j) const {
     if (packed) {
       const int8_t v = ((i + j) & 1 ? pk1 : pk0)[int64_t(i) * W2 + (j >> 1)];
-      return enc ? int8_t(1 - v) : v;
+      return dec_site(v, enc);
     }
     return pk0[int64_t(i) * W + j];
   }
   __device__ __forceinline__ void set(int i, int j, int8_t v) const {
     if (packed)
-      ((i + j) & 1 ? pk1 : pk0)[int64_t(i) * W2 + (j >> 1)] = enc ? int8_t(1 - v) : v;
+      ((i + j) & 1 ? pk1 : pk0)[int64_t(i) * W2 + (j >> 1)] = enc_site(v, enc);
     else
       pk0[int64_t(i) * W + j] = v;
   }
@@ -228,12 +235,6 @@ __device__ __forceinline__ uint32_t w_of(const uint4& v, int m) {
 }
 
 
-// Potts: per byte, 5^state for states 0..3 (PRMT table lookup, selector nibbles = states).
-__device__ __forceinline__ uint32_t pow5_bytes(uint32_t x) {
-  const uint32_t t = x | (x >> 4);                       // byte0 = s0 | s1<<4, byte2 = s2 | s3<<4
-  const uint32_t sel = (t & 0xFFu) | ((t >> 8) & 0xFF00u);
-  return __byte_perm(0x7D190501u, 0u, sel);              // bytes {1, 5, 25, 125}[s]
-}
 
 __device__ __forceinline__ uint32_t lane_id() {
   uint32_t l;
@@ -248,15 +249,6 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   return d;
 }
 
-// Potts packed path: per byte, the compact code {0, 1, 5, 21}[state]
-__device__ __forceinline__ uint32_t code_bytes(uint32_t x) {
-  // t = x | (x >> 4) (byte0 = s0 | s1<<4, byte2 = s2 | s3<<4); states <= 3 so the bits do
-  // not overlap and | is +: one LEA.HI (x + (x >> 4)) instead of a shift and a LOP3.
-  // (An IMAD.HI with an opaque 2^28 moves it to the FMA pipe instead: 2.5 % slower,
-  // profiles/r01_ab_potts_lane.txt)
-  const uint32_t t = x + (x >> 4);
-  return prmt(kPottsCodeBytes, 0u, prmt(t, 0u, 0x0020u));
-}
 
 // Threshold tables in shared memory.  T32: every threshold ceil(p*2^32) is < 2^32 (checked on
 // the host), so the exact test u < p is the 32-bit compare word < T; otherwise 64-bit.
@@ -265,11 +257,11 @@ struct GibbsTables {
   // Ising: by number of -1 neighbours nd = 0..4 (nsum = 4 - 2 nd)
   // Potts T32: by the compact code sum e (0..84), threshold a of entry e replicated per lane at
   //   word (3e + a) * 32 + lane, so every lane reads its own bank (random e, no conflicts)
-  // Potts 64-bit: by idx = sum of 5^state over the 4 neighbours
+  // Potts 64-bit: by the compact code sum e, entry 3e + a (no lane replication: rare path)
   using IsingT = typename std::conditional<T32, uint32_t, unsigned long long>::type;
   typename std::conditional<MODEL == PM_MODEL_ISING, IsingT[8],
                             typename std::conditional<T32, uint32_t[kPottsCodes * 3 * 32],
-                                                      unsigned long long[kPottsIdx * 3]>::type>::type t;
+                                                      unsigned long long[kPottsCodes * 3]>::type>::type t;
 };
 
 // Thread = NG consecutive 16-site groups of one packed row (setup amortised over 16*NG sites).
@@ -300,7 +292,7 @@ __global__ void __launch_bounds__(256, NG == 1 ? 6 : MODEL == PM_MODEL_ISING ? P
     }
   } else {
     unsigned long long* dst = reinterpret_cast<unsigned long long*>(&tb.t[0]);
-    for (int t = tid; t < kPottsIdx * 3; t += blockDim.x * blockDim.y) dst[t] = pthr[t];
+    for (int t = tid; t < kPottsCodes * 3; t += blockDim.x * blockDim.y) dst[t] = pthr[t];
   }
   __syncthreads();
   // PDL: the tables above are host-built (memcpy); the lattice is written by the previous
@@ -388,8 +380,8 @@ __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const Gibb
       out = 0x02020202u - 2u * plus_bits;  // per byte: 0x00 (+1) or 0x02 (-1), no borrows
     } else {
       if constexpr (T32) {
-        // code sums <= 84 per byte: no carries
-        const uint32_t e4 = code_bytes(U[m]) + code_bytes(D[m]) + code_bytes(cur) + code_bytes(sh);
+        // packed bytes hold the codes already (enc 2): code sums <= 84 per byte, no carries
+        const uint32_t e4 = U[m] + D[m] + cur + sh;
         const uint32_t* lt = &tb.t[0] + lane_id();
         uint32_t st[4];
 #pragma unroll
@@ -398,22 +390,19 @@ __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const Gibb
           const uint32_t w = blk.v[b];
           st[b] = uint32_t(w >= t3[0]) + uint32_t(w >= t3[32]) + uint32_t(w >= t3[64]);
         }
-        out = prmt(prmt(st[0], st[1], 0x0040u), prmt(st[2], st[3], 0x0040u), 0x5410u);
+        // new states as PRMT selector nibbles, then their codes in one lookup
+        out = prmt(kPottsCodeBytes, 0u, st[0] | (st[1] << 4) | (st[2] << 8) | (st[3] << 12));
       } else {
-        const uint32_t p1 = pow5_bytes(U[m]), p2 = pow5_bytes(D[m]);
-        const uint32_t p3 = pow5_bytes(cur), p4 = pow5_bytes(sh);
-        // two 16-bit lanes per word so the sums (<= 500) cannot overflow
-        const uint32_t ev = (p1 & 0x00FF00FFu) + (p2 & 0x00FF00FFu) + (p3 & 0x00FF00FFu) + (p4 & 0x00FF00FFu);
-        const uint32_t od = ((p1 >> 8) & 0x00FF00FFu) + ((p2 >> 8) & 0x00FF00FFu) + ((p3 >> 8) & 0x00FF00FFu) +
-                            ((p4 >> 8) & 0x00FF00FFu);
+        const uint32_t e4 = U[m] + D[m] + cur + sh;  // code sums, as in the 32-bit path
+        const unsigned long long* tt = reinterpret_cast<const unsigned long long*>(&tb.t[0]);
+        uint32_t st[4];
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          const uint32_t idx = ((b & 1) ? od : ev) >> (16 * (b >> 1)) & 0xFFFFu;
-          const uint32_t w = blk.v[b];
-          const unsigned long long* t3 = reinterpret_cast<const unsigned long long*>(&tb.t[0]) + idx * 3;
-          const uint32_t st = uint32_t(uint64_t(w) >= t3[0]) + uint32_t(uint64_t(w) >= t3[1]) + uint32_t(uint64_t(w) >= t3[2]);
-          out |= st << (8 * b);
+          const unsigned long long* t3 = tt + prmt(e4, 0u, 0x4440u + b) * 3;
+          const uint64_t w = blk.v[b];
+          st[b] = uint32_t(w >= t3[0]) + uint32_t(w >= t3[1]) + uint32_t(w >= t3[2]);
         }
+        out = prmt(kPottsCodeBytes, 0u, st[0] | (st[1] << 4) | (st[2] << 8) | (st[3] << 12));
       }
     }
     res[m] = out;
@@ -475,8 +464,8 @@ __global__ void pack_kernel(const int8_t* __restrict__ grid, int H, int W, int8_
     const int8_t* src = reinterpret_cast<const int8_t*>(&v);
     const int c0 = (par0 + i) & 1;  // colour of column 2q
     const int64_t o = int64_t(i + aoff) * W2 + q;
-    (c0 ? pk1 : pk0)[o] = enc_spin(src[0], enc);
-    (c0 ? pk0 : pk1)[o] = enc_spin(src[1], enc);
+    (c0 ? pk1 : pk0)[o] = enc_site(src[0], enc);
+    (c0 ? pk0 : pk1)[o] = enc_site(src[1], enc);
   }
 }
 __global__ void unpack_kernel(int8_t* __restrict__ grid, int H, int W, const int8_t* pk0, const int8_t* pk1,
@@ -488,8 +477,8 @@ __global__ void unpack_kernel(int8_t* __restrict__ grid, int H, int W, const int
     const int c0 = (par0 + i) & 1;
     const int64_t o = int64_t(i + aoff) * W2 + q;
     char2 v;
-    v.x = enc_spin((c0 ? pk1 : pk0)[o], enc);
-    v.y = enc_spin((c0 ? pk0 : pk1)[o], enc);
+    v.x = dec_site((c0 ? pk1 : pk0)[o], enc);
+    v.y = dec_site((c0 ? pk0 : pk1)[o], enc);
     reinterpret_cast<char2*>(grid + int64_t(i) * W)[q] = v;
   }
 }
@@ -577,7 +566,7 @@ struct pm_lat_s {
   // Potts
   bool has_potts = false;
   double* cdf = nullptr;
-  unsigned long long* pthr = nullptr;
+  unsigned long long* pthr = nullptr;  // Potts packed path, 64-bit thresholds: [85][3] by code sum
   uint32_t* pthr32 = nullptr;  // Potts packed path: [85][3] thresholds by code sum, when all < 2^32
   bool pdl = pdl_default();   // packed half-sweeps launched with PDL (PM_PDL=0 disables)
   bool t32 = false;           // every threshold of the active model fits 32 bits
@@ -623,7 +612,7 @@ LatView view_of(pm_lat_s* h) {
   v.W = h->W;
   v.W2 = h->W / 2;
   v.packed = h->packed;
-  v.enc = h->packed && h->model == PM_MODEL_ISING;
+  v.enc = h->packed ? (h->model == PM_MODEL_ISING ? 1 : 2) : 0;
   return v;
 }
 
@@ -734,7 +723,7 @@ int pm_lat_set_spins(pm_lat_t h, const int8_t* s) {
   if (nbad) return fail(PM_EINVAL, h->model == PM_MODEL_ISING ? "spins must be -1 or +1" : "Potts states must be 0..3");
   if (h->packed) {
     pack_kernel<<<grid_for(h, n / 2), 256, 0, h->stream>>>(h->scratch, h->H, h->W, h->pk0, h->pk1, h->row0,
-                                                          h->strip, h->model == PM_MODEL_ISING);
+                                                          h->strip, h->model == PM_MODEL_ISING ? 1 : 2);
   } else {
     PM_CUDA(cudaMemcpyAsync(h->pk0, h->scratch, n, cudaMemcpyDeviceToDevice, h->stream));
   }
@@ -750,7 +739,7 @@ int pm_lat_get_spins(pm_lat_t h, int8_t* s) {
   DeviceGuard g(h->device);
   if (h->packed) {
     unpack_kernel<<<grid_for(h, n / 2), 256, 0, h->stream>>>(h->scratch, h->H, h->W, h->pk0, h->pk1, h->row0,
-                                                             h->strip, h->model == PM_MODEL_ISING);
+                                                             h->strip, h->model == PM_MODEL_ISING ? 1 : 2);
     PM_CUDA(cudaGetLastError());
     PM_CUDA(cudaMemcpyAsync(s, h->scratch, n, cudaMemcpyDeviceToHost, h->stream));
   } else {
@@ -822,20 +811,24 @@ int pm_lat_set_potts(pm_lat_t h, double coupling) {
   }
   // compact table of the packed path: entry n1 + 5 n2 + 21 n3 of the multiset (n0, n1, n2, n3)
   std::vector<uint32_t> tc(kPottsCodes * 3, 0u);
+  std::vector<unsigned long long> tc64(kPottsCodes * 3, 0ull);
   for (int idx = 0; idx < kPottsIdx; ++idx) {
     const int n0 = idx % 5, n1 = (idx / 5) % 5, n2 = (idx / 25) % 5, n3 = idx / 125;
     if (n0 + n1 + n2 + n3 != 4) continue;
     const int e = n1 + 5 * n2 + 21 * n3;
-    for (int a = 0; a < 3; ++a) tc[3 * e + a] = uint32_t(thr[3 * idx + a]);
+    for (int a = 0; a < 3; ++a) {
+      tc[3 * e + a] = uint32_t(thr[3 * idx + a]);
+      tc64[3 * e + a] = thr[3 * idx + a];
+    }
   }
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard g(h->device);
   cudaStreamSynchronize(h->stream);
   if (!h->cdf) PM_CUDA(cudaMalloc(&h->cdf, sizeof(double) * kPottsIdx * 3));
-  if (!h->pthr) PM_CUDA(cudaMalloc(&h->pthr, sizeof(unsigned long long) * kPottsIdx * 3));
+  if (!h->pthr) PM_CUDA(cudaMalloc(&h->pthr, sizeof(unsigned long long) * kPottsCodes * 3));
   if (!h->pthr32) PM_CUDA(cudaMalloc(&h->pthr32, sizeof(uint32_t) * kPottsCodes * 3));
   PM_CUDA(cudaMemcpy(h->cdf, cdf.data(), sizeof(double) * kPottsIdx * 3, cudaMemcpyHostToDevice));
-  PM_CUDA(cudaMemcpy(h->pthr, thr.data(), sizeof(unsigned long long) * kPottsIdx * 3, cudaMemcpyHostToDevice));
+  PM_CUDA(cudaMemcpy(h->pthr, tc64.data(), sizeof(unsigned long long) * kPottsCodes * 3, cudaMemcpyHostToDevice));
   PM_CUDA(cudaMemcpy(h->pthr32, tc.data(), sizeof(uint32_t) * kPottsCodes * 3, cudaMemcpyHostToDevice));
   h->t32 = fits;
   h->has_potts = true;

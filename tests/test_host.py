@@ -163,7 +163,7 @@ def test_run_region_contract():
 
 def test_potts_compact_code_sums_are_unique():
     """The packed Potts kernel indexes its threshold table by the sum of per-neighbour codes
-    {0, 1, 5, 21}[state] (ising.cu kPottsCodeBytes): the 35 neighbour multisets of q=4 states
+    {0, 1, 5, 21}[state] (ising.cu kPottsCodeBytes; the packed arrays store these codes): the 35 neighbour multisets of q=4 states
     over 4 neighbours must give distinct sums that fit one byte and the 85-entry table."""
     import itertools
     codes = (0, 1, 5, 21)
