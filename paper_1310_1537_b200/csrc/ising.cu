@@ -55,11 +55,14 @@ constexpr uint32_t kPottsCodeBytes = 0x15050100u;  // bytes {0, 1, 5, 21}
 //   enc 1 (Ising): e = 1 - s (0x00 for +1, 0x02 for -1): the sum is 2 x (number of -1's);
 //   enc 2 (Potts q=4): e = {0, 1, 5, 21}[state], the compact code (kPottsCodeBytes).
 // pack/unpack and LatView convert; unpacked grids (odd W) are stored as is (enc 0).
+// (branch-free: a select chain here compiled to a slow per-byte lookup in pack/unpack)
 __host__ __device__ __forceinline__ int8_t enc_site(int8_t v, int enc) {
-  return enc == 1 ? int8_t(1 - v) : enc == 2 ? int8_t(v == 0 ? 0 : v == 1 ? 1 : v == 2 ? 5 : 21) : v;
+  const int code = int((kPottsCodeBytes >> (8 * (v & 3))) & 0xFFu);
+  return enc == 1 ? int8_t(1 - v) : enc == 2 ? int8_t(code) : v;
 }
 __host__ __device__ __forceinline__ int8_t dec_site(int8_t e, int enc) {
-  return enc == 1 ? int8_t(1 - e) : enc == 2 ? int8_t(e == 0 ? 0 : e == 1 ? 1 : e == 5 ? 2 : 3) : e;
+  const int state = int(e > 0) + int(e > 1) + int(e > 5);
+  return enc == 1 ? int8_t(1 - e) : enc == 2 ? int8_t(state) : e;
 }
 
 struct LatView {
