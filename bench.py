@@ -15,10 +15,15 @@ partials are all-gathered and summed in rank order (--force-dist runs that rank 
 as a 1-rank group on one GPU).  c4 at N>1 splits the lattice into row strips with halo
 exchange; the other configs are replicas.
 
-`--impl reference` times the reference algorithm's CPU implementation on this host
-(the numpy restatement in oracle/glm_oracle.py, PLF over all host threads, OpenBLAS
-single-threaded per worker: the reference's fastest setting), on a
-bounded row sample per step, scaled to the full N.
+`--impl reference` times the UNMODIFIED reference on this host's cores: `parmcmc` 0.1.0
+installed from the reference tree into baseline/_ref by __graft_entry__.build()
+(pip --target, git-ignored, travels to the GPU box like libpmb200.so), called through its
+own public API -- glm.loglike_grad(DesignMatrix, beta, ExecPlan(PLF, workers)) plus the
+GaussianPrior terms -- on the FULL config (every step evaluates all N rows; no sample
+scaling).  Both BASELINE.md §3 thread settings run, each in a fresh subprocess:
+(i) PLF workers=1 with OPENBLAS_NUM_THREADS=C, (ii) PLF workers=C with OpenBLAS 1; the
+faster is the line's value.  Without baseline/_ref the numpy restatement in
+oracle/glm_oracle.py stands in (kind "port").
 """
 
 from __future__ import annotations
@@ -39,15 +44,28 @@ def _early_args():
     p = argparse.ArgumentParser(add_help=False)
     p.add_argument("--impl", default="b200")
     p.add_argument("--cpu-worker", action="store_true")
+    p.add_argument("--ref-worker", action="store_true")
+    p.add_argument("--setting", default="ii")
     a, _ = p.parse_known_args()
     return a
 
 
+def _affinity_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 _EA = _early_args()
-if _EA.impl == "reference" or _EA.cpu_worker:
-    # the reference's best CPU setting: workers = cores, one BLAS thread each (set before numpy loads)
+if _EA.cpu_worker or (_EA.ref_worker and _EA.setting == "ii"):
+    # BASELINE.md §3 setting (ii): workers = cores, one BLAS thread each (set before numpy loads)
     for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[var] = "1"
+elif _EA.ref_worker:
+    # setting (i): one PLF worker, OpenBLAS over all cores
+    for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[var] = str(_affinity_cores())
 
 import numpy as np  # noqa: E402
 
@@ -284,43 +302,140 @@ def cpu_baseline_other(config: str) -> dict:
 
 
 def cpu_worker_main(args):
-    """Subprocess body: time the oracle port on a bounded sample (OPENBLAS set to 1 above)."""
-    if "n" not in CONFIGS[args.config]:
-        return cpu_worker_other(args)
-    from oracle import glm_oracle as gl
-    from paper_1310_1537_b200.synthetic import baseline_design
-    cores = host_cores()
-    x, y, _, betas = baseline_design(args.sample_rows, args.k, seed=7, n_eval=args.reps + 3)
-    x = x.astype(np.float32).astype(np.float64) if args.x_storage == "f32" else x
-    mu, sigma = np.zeros(args.k), np.full(args.k, 10.0)
-    for i in range(3):
-        gl.log_posterior_grad(x, y, betas[i], mu, sigma, workers=cores)
-    times = []
-    for i in range(args.reps):
-        t0 = time.perf_counter()
-        gl.log_posterior_grad(x, y, betas[3 + i], mu, sigma, workers=cores)
-        times.append(time.perf_counter() - t0)
-    print(json.dumps({"median_s": statistics.median(times), "times": times, "cores": cores}))
+    """Subprocess body for the non-GLM configs' CPU baselines (cpu_worker_other)."""
+    return cpu_worker_other(args)
 
 
-def cpu_baseline(cfg: dict, n_full: int, budget_s: float = 20.0) -> dict:
-    """Run the oracle port in a fresh subprocess (OpenBLAS single-threaded per worker)."""
-    k = cfg["k"]
-    sample_rows = min(n_full, 2_000_000)
-    reps = 5
-    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--cpu-worker", "--sample-rows", str(sample_rows),
-           "--k", str(k), "--reps", str(reps), "--x-storage", cfg.get("x_storage", "f64")]
+# ---------------------------------------------------------------------------- reference (CPU)
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_installed() -> bool:
+    """The unmodified reference package, pip-installed by __graft_entry__.build()."""
+    return os.path.isfile(os.path.join(REF_DIR, "parmcmc", "glm.py"))
+
+
+def save_glm_inputs(x, y, betas) -> str:
+    """Park the inputs as .npy files (memory-mapped by the timing subprocesses, so the
+    8 GB design is generated once): /dev/shm when it has room, else the temp dir."""
+    import tempfile
+    need = x.nbytes + y.nbytes + betas.nbytes + (1 << 28)
+    base = None
     try:
-        out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, check=True).stdout
-        res = json.loads(out.strip().splitlines()[-1])
-    except Exception as exc:  # reported, never fatal
-        return {"value": None, "unit": "evals/s", "cores": host_cores(), "kind": "port",
-                "sample": f"failed: {exc}"}
-    per_eval_full = res["median_s"] * n_full / sample_rows
-    return {"value": 1.0 / per_eval_full, "unit": "evals/s", "cores": res["cores"], "kind": "port",
-            "sample": (f"oracle/glm_oracle.py log_posterior_grad (numpy PLF, {res['cores']} workers x 1 BLAS thread) "
-                       f"on {sample_rows} rows x K={k}, median of {reps} evals after 3 warm-up = "
-                       f"{res['median_s']*1e3:.1f} ms, scaled x{n_full/sample_rows:g} to N={n_full}")}
+        st = os.statvfs("/dev/shm")
+        if st.f_bavail * st.f_frsize > 2 * need:
+            base = "/dev/shm"
+    except OSError:
+        pass
+    d = tempfile.mkdtemp(prefix="pm_ref_", dir=base)
+    np.save(os.path.join(d, "x.npy"), x)
+    np.save(os.path.join(d, "y.npy"), y)
+    np.save(os.path.join(d, "betas.npy"), betas)
+    return d
+
+
+def ref_worker_main(args):
+    """Subprocess: time the CPU log-posterior + gradient on the full inputs in args.data.
+    Unmodified reference (baseline/_ref): f = loglike_grad(...).f + sum_k prior.logpdf_coord,
+    g = loglike_grad(...).g - (beta - mu) / sigma^2 (glm.py:351-364, sampler.py:55-58)."""
+    cores = _affinity_cores()
+    workers = 1 if args.setting == "i" else cores
+    x = np.load(os.path.join(args.data, "x.npy"), mmap_mode="r")
+    y = np.load(os.path.join(args.data, "y.npy"))
+    betas = np.load(os.path.join(args.data, "betas.npy"))
+    k = x.shape[1]
+    mu, sigma = np.zeros(k), np.full(k, 10.0)
+    if args.ref_kind == "reference":
+        sys.path.insert(0, REF_DIR)
+        from parmcmc import glm as rglm
+        from parmcmc.sampler import GaussianPrior
+        data = rglm.DesignMatrix(x, y)
+        plan = rglm.ExecPlan(rglm.Strategy.PLF, workers=workers)
+        prior = GaussianPrior(mu, sigma)
+
+        def evaluate(beta):
+            r = rglm.loglike_grad(data, beta, plan)
+            f = r.f + sum(prior.logpdf_coord(j, float(beta[j])) for j in range(k))
+            return f, r.g - (beta - prior.mu) / prior.sigma ** 2
+        what = (f"unmodified parmcmc (baseline/_ref) glm.loglike_grad + GaussianPrior.logpdf_coord, "
+                f"ExecPlan(PLF, workers={workers})")
+    else:
+        from oracle import glm_oracle as gl
+        xa = np.ascontiguousarray(x)
+
+        def evaluate(beta):
+            return gl.log_posterior_grad(xa, y, beta, mu, sigma, workers=workers)
+        what = f"oracle/glm_oracle.py log_posterior_grad (numpy restatement of PLF), {workers} workers"
+    for i in range(args.warmup):
+        evaluate(betas[i % len(betas)])
+    times = []
+    f = None
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        f, _ = evaluate(betas[(args.warmup + i) % len(betas)])
+        times.append(time.perf_counter() - t0)
+    print(json.dumps({"times": times, "total_s": sum(times), "median_s": statistics.median(times),
+                      "cores": cores, "workers": workers, "blas": os.environ.get("OPENBLAS_NUM_THREADS"),
+                      "setting": args.setting, "kind": args.ref_kind, "what": what, "last_f": f}))
+
+
+def run_ref_settings(data_dir: str, steps: int, warmup: int, settings=("ii", "i")) -> dict:
+    """each thread setting in a fresh subprocess (the BLAS env var must be
+    set before numpy loads); returns {"settings": {...}, "best": name, "kind": ...}."""
+    kind = "reference" if reference_installed() else "port"
+    out = {}
+    for st in settings:
+        cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--ref-worker", "--setting", st, "--data", data_dir,
+               "--steps", str(steps), "--warmup", str(warmup), "--ref-kind", kind]
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=1800, check=True)
+            out[st] = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as exc:  # reported, never fatal
+            tail = getattr(exc, "stderr", "") or ""
+            out[st] = {"error": f"{exc} {tail[-300:]}"}
+    ok = {k: v for k, v in out.items() if "total_s" in v}
+    best = min(ok, key=lambda k: ok[k]["total_s"] / len(ok[k]["times"])) if ok else None
+    return {"settings": out, "best": best, "kind": kind}
+
+
+def _settings_summary(res: dict) -> str:
+    parts = []
+    for st, v in res["settings"].items():
+        if "total_s" in v:
+            rate = len(v["times"]) / v["total_s"]
+            parts.append(f"({st}) workers={v['workers']} OPENBLAS_NUM_THREADS={v['blas']}: {rate:.3f} evals/s "
+                         f"(median {v['median_s']*1e3:.0f} ms){' <- faster' if st == res['best'] else ''}")
+        else:
+            parts.append(f"({st}) failed: {v.get('error', '?')[:200]}")
+    return "; ".join(parts)
+
+
+def glm_inputs(cfg: dict, n_betas: int, seed: int = 7):
+    from paper_1310_1537_b200.synthetic import baseline_design
+    x, y, _, betas = baseline_design(cfg["n"], cfg["k"], seed=seed, n_eval=max(n_betas, 2))
+    if cfg.get("x_storage") == "f32":  # fp32-X: the reference runs on the fp32-rounded X (as f64)
+        x = x.astype(np.float32).astype(np.float64)
+    return x, y, np.ascontiguousarray(betas)
+
+
+def cpu_baseline(cfg: dict, x, y, betas) -> dict:
+    """The GPU arm's cpu_baseline: the unmodified reference on the same full inputs, both
+    thread settings, 2 warm-up + 3 timed evaluations each (~10-20 s of CPU work at c1)."""
+    import shutil
+    d = save_glm_inputs(x, y, betas)
+    try:
+        res = run_ref_settings(d, steps=3, warmup=2)
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
+    best = res["settings"].get(res["best"]) if res["best"] else None
+    if best is None:
+        return {"value": None, "unit": "evals/s", "cores": host_cores(), "kind": res["kind"],
+                "sample": _settings_summary(res)}
+    return {"value": len(best["times"]) / best["total_s"], "unit": "evals/s", "cores": best["cores"],
+            "kind": res["kind"],
+            "sample": (f"{best['what']}: full N={cfg['n']} rows x K={cfg['k']} per evaluation (no scaling), "
+                       f"same X/y as the GPU arm, 3 timed evaluations after 2 warm-up per setting; "
+                       + _settings_summary(res))}
 
 
 # ---------------------------------------------------------------------------- reference arm
@@ -328,37 +443,35 @@ def run_reference(args, cfg):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    from oracle import glm_oracle as gl
-    from paper_1310_1537_b200.synthetic import baseline_design
+    import shutil
     cores = host_cores()
     n_full, k = cfg["n"], cfg["k"]
-    # bounded sample per step so the whole K-step run stays within a few minutes
-    sample_rows = min(n_full, max(100_000, min(1_000_000, int(1e8 // max(args.steps, 1)))))
-    x, y, _, betas = baseline_design(sample_rows, k, seed=7, n_eval=args.steps + args.warmup + 1)
-    if cfg.get("x_storage") == "f32":
-        x = x.astype(np.float32).astype(np.float64)
-    mu, sigma = np.zeros(k), np.full(k, 10.0)
-    for i in range(args.warmup):
-        gl.log_posterior_grad(x, y, betas[i], mu, sigma, workers=cores)
-    t0 = time.perf_counter()
-    for i in range(args.steps):
-        gl.log_posterior_grad(x, y, betas[args.warmup + i], mu, sigma, workers=cores)
-    wall = time.perf_counter() - t0
-    scale = n_full / sample_rows
-    ms_per_step = wall / args.steps * 1e3 * scale
+    x, y, betas = glm_inputs(cfg, args.warmup + args.steps)
+    d = save_glm_inputs(x, y, betas)
+    del x, y
+    try:
+        res = run_ref_settings(d, steps=args.steps, warmup=args.warmup)
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
+    if res["best"] is None:
+        print(json.dumps({"impl": "reference", "unavailable": _settings_summary(res)[:400]}), flush=True)
+        return
+    best = res["settings"][res["best"]]
+    ms_per_step = best["total_s"] / len(best["times"]) * 1e3
     value = 1000.0 / ms_per_step
+    sample = (f"{best['what']}: every step evaluates the full N={n_full} x K={k} design (no sample scaling); "
+              f"{args.warmup} warm-up + {args.steps} timed steps per setting, each setting in a fresh "
+              f"subprocess; " + _settings_summary(res))
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY §8d generator, seed 7)",
-        "config": {"workload": cfg["desc"], "N": n_full, "K": k, "sample_rows_per_step": sample_rows,
-                   "x_storage": cfg.get("x_storage", "f64")},
+        "config": {"workload": cfg["desc"], "N": n_full, "K": k, "x_storage": cfg.get("x_storage", "f64"),
+                   "rows_per_step": n_full, "thread_setting": res["best"]},
         "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "port",
-                         "sample": (f"oracle/glm_oracle.py (numpy restatement of parmcmc PLF, glm.py:418-436) "
-                                    f"with {cores} workers x 1 OpenBLAS thread; each step evaluates {sample_rows} "
-                                    f"rows and is scaled x{scale:g} to N={n_full}")},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": res["kind"], "sample": sample},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "median_ms_per_step": best["median_s"] * 1e3,
     }
     print(json.dumps(line), flush=True)
 
@@ -370,7 +483,7 @@ def run_glm(args, cfg):
     from paper_1310_1537_b200 import glm as pglm
     from paper_1310_1537_b200.parallel import partition
     from paper_1310_1537_b200.sampler import GaussianPrior
-    from paper_1310_1537_b200.synthetic import baseline_design
+    from paper_1310_1537_b200.synthetic import baseline_design_rows
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -392,10 +505,18 @@ def run_glm(args, cfg):
     a, b = partition(n_full, ws)[rank]
     n_local = b - a
     steps, warmup = args.steps, args.warmup
-    # rank-local shard of the global design (per-rank seed: generating another rank's
-    # prefix would cost its full stream)
-    x, y, _, betas = baseline_design(n_local, k, seed=1000 + rank, n_eval=1)
-    betas = np.random.default_rng(99).normal(0.0, 0.1, (warmup + 2 * steps, k))  # same on every rank
+    # ONE global design (seed 7, the reference arm's inputs): every rank draws the whole
+    # generator stream chunk by chunk and keeps its own rows (bit-identical to slicing the
+    # single-process design); rank 0 of a multi-rank run keeps all rows for the check below
+    n_betas = warmup + 2 * steps
+    if ws == 1 or rank == 0:
+        x_all, y_all, betas = glm_inputs(cfg, n_betas)
+        x, y = x_all[a:b], y_all[a:b]
+    else:
+        x, y, _, betas = baseline_design_rows(n_full, k, 7, a, b, n_eval=n_betas)
+        x_all = y_all = None
+        if cfg.get("x_storage") == "f32":
+            x = x.astype(np.float32).astype(np.float64)
     data = pglm.DesignMatrix(x, y)
     del x
     prior = GaussianPrior.isotropic(k, 0.0, 10.0)
@@ -493,6 +614,25 @@ def run_glm(args, cfg):
     barrier()
     assert np.isfinite(res.f) and np.all(np.isfinite(res.g))
 
+    # rank path: rank 0 checks the folded (f, g) against a 1-GPU evaluation of ALL rows of
+    # the same global design (different CTA partition, so within 1e-10, not bitwise)
+    check = None
+    if dist_mode:
+        probe = betas[0]
+        got = step_e2e(probe)
+        if rank == 0:
+            full = pglm.DesignMatrix(x_all, y_all)
+            ref = pglm.log_posterior_grad(full, probe, prior, pglm.ExecPlan(pglm.Strategy.B200, device=local,
+                                                                              x_storage=cfg["x_storage"]))
+            rf = abs(got.f - ref.f) / max(abs(ref.f), 1.0)
+            rg = float(np.max(np.abs(got.g - ref.g) / np.maximum(np.abs(ref.g), 1.0)))
+            check = {"beta": "first warm-up beta", "rel_f": rf, "rel_g": rg, "tol": 1e-10,
+                     "ok": bool(rf < 1e-10 and rg < 1e-10)}
+            full.release_device()
+            del full
+            assert check["ok"], check
+        barrier()
+
     # max over ranks
     t = torch.tensor([dev_ms, e2e_s, kern_ms], dtype=torch.float64, device=f"cuda:{local}")
     if dist_mode:
@@ -546,8 +686,10 @@ def run_glm(args, cfg):
                                             "NVLink/NVSwitch), flag + wait, rank-ordered fold (no NCCL call)")
         elif dist_mode:
             line["config"]["collective"] = "NCCL all_gather_into_tensor of K+1 doubles + pm_fold_rows per step"
+        if dist_mode and check is not None:
+            line["check_vs_1gpu"] = check
         if ws == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(cfg, n_full)
+            line["cpu_baseline"] = cpu_baseline(cfg, x_all, y_all, betas[:5])
         print(json.dumps(line), flush=True)
     if dist_mode:
         dist.destroy_process_group()
@@ -910,9 +1052,16 @@ def main():
     p.add_argument("--k", type=int, default=0, help=argparse.SUPPRESS)
     p.add_argument("--reps", type=int, default=5, help=argparse.SUPPRESS)
     p.add_argument("--x-storage", default="f64", help=argparse.SUPPRESS)
+    p.add_argument("--ref-worker", action="store_true", help=argparse.SUPPRESS)
+    p.add_argument("--setting", default="ii", choices=["i", "ii"], help=argparse.SUPPRESS)
+    p.add_argument("--data", default="", help=argparse.SUPPRESS)
+    p.add_argument("--ref-kind", default="reference", choices=["reference", "port"], help=argparse.SUPPRESS)
     args = p.parse_args()
     if args.cpu_worker:
         cpu_worker_main(args)
+        return
+    if args.ref_worker:
+        ref_worker_main(args)
         return
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -93,7 +93,10 @@ PM_API int pm_glm_eval(pm_glm_t h, const double* beta, int with_prior, int want_
 
 /* Split form of pm_glm_eval for several handles in flight (the reference's
  * SHARDED strategy, glm.py:439-454, one shard per device): _launch enqueues the
- * kernel on the handle's stream, _wait synchronises and returns the result. */
+ * kernel on the handle's stream, _wait synchronises and returns the result.
+ * One evaluation may be in flight per handle: _launch returns PM_ESTATE until the
+ * matching _wait.  pm_glm_eval holds the handle's mutex across both halves, so
+ * threads sharing one handle each get their own (f, g). */
 PM_API int pm_glm_launch(pm_glm_t h, const double* beta, int with_prior, int want_grad);
 PM_API int pm_glm_wait(pm_glm_t h, double* f_out, double* g_out);
 
@@ -124,6 +127,14 @@ PM_API int pm_xchg_status(pm_xchg_t x, int32_t* timed_out);
 PM_API int pm_xchg_destroy(pm_xchg_t x);
 PM_API int pm_glm_eval_xchg(pm_glm_t h, const double* beta, int with_prior, pm_xchg_t x, double* dev_out,
                             void* stream);
+/* Split form of pm_glm_eval_xchg: phase 1 = stream + deposit + raise the flags (no wait,
+ * dev_out untouched), phase 2 = the same evaluation again, then wait for every rank's flag
+ * and fold (no deposit; same epoch), phase 3 = pm_glm_eval_xchg.  Phase 1 and 2 alternate
+ * per handle (PM_ESTATE otherwise).  With a host barrier between every rank's phase 1 and
+ * any rank's phase 2 no kernel ever waits on a kernel that is still running, so ranks that
+ * SHARE one GPU (processes time-sliced on it) can drive the real IPC exchange. */
+PM_API int pm_glm_eval_xchg_phase(pm_glm_t h, const double* beta, int with_prior, pm_xchg_t x, int phase,
+                                  double* dev_out, void* stream);
 /* out[c] = in[0][c] + in[1][c] + ... + in[world-1][c] in ascending row order (the reference's
  * ascending-worker merge, glm.py:243-250), c < width; device pointers, one launch on `stream`
  * (NULL = the legacy default stream).  Bitwise identical on every rank given the same input. */

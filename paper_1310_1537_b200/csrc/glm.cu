@@ -391,6 +391,7 @@ GlmArgs make_args(pm_glm_s* h, bool with_prior, double* out) {
   a.beta_dev = h->beta_dev;
   a.xw = 0;  // no peer exchange (pm_glm_eval_xchg sets these)
   a.xrank = 0;
+  a.xphase = 3;
   a.xepoch = 0;
   for (int p = 0; p < kMaxXchgRanks; ++p) a.xpeer[p] = nullptr;
   a.xstatus = nullptr;
@@ -405,7 +406,7 @@ int check_beta(pm_glm_s* h, const double* beta) {
 
 // enqueue one evaluation writing (f, g) to `out` on stream `st` (caller holds the mutex)
 struct XchgLaunch {  // peer exchange fields of one evaluation (pm_glm_eval_xchg)
-  int world = 0, rank = 0;
+  int world = 0, rank = 0, phase = 3;
   unsigned long long epoch = 0;
   double* peer[kMaxXchgRanks] = {};
   unsigned* status = nullptr;
@@ -417,6 +418,7 @@ int enqueue_eval(pm_glm_s* h, const double* beta, bool with_prior, bool grad, do
   if (xl) {
     a.xw = xl->world;
     a.xrank = xl->rank;
+    a.xphase = xl->phase;
     a.xepoch = xl->epoch;
     for (int p = 0; p < kMaxXchgRanks; ++p) a.xpeer[p] = xl->peer[p];
     a.xstatus = xl->status;
@@ -588,10 +590,14 @@ int pm_glm_set_prior(pm_glm_t h, const double* mu, const double* sigma) {
   return PM_OK;
 }
 
-int pm_glm_launch(pm_glm_t h, const double* beta, int with_prior, int want_grad) {
-  if (!h) return fail(PM_EINVAL, "null handle");
-  std::lock_guard<std::mutex> lk(h->mu);
+}  // extern "C"
+
+namespace {
+// launch / wait bodies; the caller holds h->mu.  pm_glm_eval holds it across both so two
+// threads sharing a handle cannot interleave (one's (f, g) read out of the other's launch).
+int glm_launch_locked(pm_glm_s* h, const double* beta, int with_prior, int want_grad) {
   if (h->K == 0) return fail(PM_ESTATE, "no data uploaded");
+  if (h->launched) return fail(PM_ESTATE, "an evaluation is already in flight (pm_glm_wait first)");
   if (with_prior && !h->has_prior) return fail(PM_ESTATE, "with_prior set but no prior configured");
   int rc = check_beta(h, beta);
   if (rc) return rc;
@@ -603,22 +609,37 @@ int pm_glm_launch(pm_glm_t h, const double* beta, int with_prior, int want_grad)
   return PM_OK;
 }
 
-int pm_glm_wait(pm_glm_t h, double* f_out, double* g_out) {
-  if (!h) return fail(PM_EINVAL, "null handle");
-  std::lock_guard<std::mutex> lk(h->mu);
+int glm_wait_locked(pm_glm_s* h, double* f_out, double* g_out) {
   if (!h->launched) return fail(PM_ESTATE, "pm_glm_wait without a launch");
   DeviceGuard g(h->device);
-  PM_CUDA(cudaStreamSynchronize(h->stream));
   h->launched = false;
+  PM_CUDA(cudaStreamSynchronize(h->stream));
   if (f_out) *f_out = h->out_host[0];
   if (g_out && h->last_want_grad) std::memcpy(g_out, h->out_host + 1, sizeof(double) * h->K);
   return PM_OK;
 }
+}  // namespace
+
+extern "C" {
+
+int pm_glm_launch(pm_glm_t h, const double* beta, int with_prior, int want_grad) {
+  if (!h) return fail(PM_EINVAL, "null handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return glm_launch_locked(h, beta, with_prior, want_grad);
+}
+
+int pm_glm_wait(pm_glm_t h, double* f_out, double* g_out) {
+  if (!h) return fail(PM_EINVAL, "null handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return glm_wait_locked(h, f_out, g_out);
+}
 
 int pm_glm_eval(pm_glm_t h, const double* beta, int with_prior, int want_grad, double* f_out, double* g_out) {
-  int rc = pm_glm_launch(h, beta, with_prior, want_grad);
+  if (!h) return fail(PM_EINVAL, "null handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  int rc = glm_launch_locked(h, beta, with_prior, want_grad);
   if (rc) return rc;
-  return pm_glm_wait(h, f_out, g_out);
+  return glm_wait_locked(h, f_out, g_out);
 }
 
 // ---- peer-memory exchange of row-sharded ranks (replaces NCCL all-gather + fold) ----
@@ -629,6 +650,7 @@ struct pm_xchg_s {
   bool opened[kMaxXchgRanks] = {};   // IPC mappings to close
   unsigned* status = nullptr;       // device u32: 1 after a wait timeout
   unsigned long long epoch = 0;
+  bool half_open = false;           // split form: a phase-1 launch awaits its phase-2 launch
   std::mutex mu;
 };
 
@@ -723,9 +745,11 @@ int pm_xchg_destroy(pm_xchg_t x) {
   return PM_OK;
 }
 
-int pm_glm_eval_xchg(pm_glm_t h, const double* beta, int with_prior, pm_xchg_t x, double* dev_out, void* stream) {
+int pm_glm_eval_xchg_phase(pm_glm_t h, const double* beta, int with_prior, pm_xchg_t x, int phase, double* dev_out,
+                           void* stream) {
   if (!h || !x) return fail(PM_EINVAL, "null handle");
-  if (!dev_out) return fail(PM_EINVAL, "dev_out is null");
+  if (!dev_out && phase != 1) return fail(PM_EINVAL, "dev_out is null");
+  if (phase < 1 || phase > 3) return fail(PM_EINVAL, "phase must be 1, 2 or 3");
   std::lock_guard<std::mutex> lk(h->mu);
   std::lock_guard<std::mutex> lx(x->mu);
   if (h->K == 0) return fail(PM_ESTATE, "no data uploaded");
@@ -733,6 +757,8 @@ int pm_glm_eval_xchg(pm_glm_t h, const double* beta, int with_prior, pm_xchg_t x
   if (x->device != h->device) return fail(PM_EINVAL, "exchange and design on different devices");
   for (int p = 0; p < x->world; ++p)
     if (!x->peer[p]) return fail(PM_ESTATE, "peer mailbox not opened (pm_xchg_open_peer)");
+  if ((phase == 2) != x->half_open)
+    return fail(PM_ESTATE, phase == 2 ? "phase 2 without a phase-1 launch" : "phase-1 launch awaits its phase 2");
   int rc = check_beta(h, beta);
   if (rc) return rc;
   if (with_prior && !h->has_prior) return fail(PM_ESTATE, "no prior set (pm_glm_set_prior)");
@@ -745,16 +771,23 @@ int pm_glm_eval_xchg(pm_glm_t h, const double* beta, int with_prior, pm_xchg_t x
   XchgLaunch xl;
   xl.world = x->world;
   xl.rank = x->rank;
-  xl.epoch = ++x->epoch;
+  xl.phase = phase;
+  xl.epoch = phase == 2 ? x->epoch : x->epoch + 1;  // phase 2 folds the epoch phase 1 deposited
   for (int p = 0; p < x->world; ++p) xl.peer[p] = x->peer[p];
   xl.status = x->status;
   rc = enqueue_eval(h, beta, with_prior != 0, true, dev_out, st, &xl);
   if (rc) return rc;
+  x->epoch = xl.epoch;
+  x->half_open = phase == 1;
   if (st != h->stream) {
     PM_CUDA(cudaEventRecord(h->ev_b, st));
     PM_CUDA(cudaStreamWaitEvent(h->stream, h->ev_b, 0));
   }
   return PM_OK;
+}
+
+int pm_glm_eval_xchg(pm_glm_t h, const double* beta, int with_prior, pm_xchg_t x, double* dev_out, void* stream) {
+  return pm_glm_eval_xchg_phase(h, beta, with_prior, x, 3, dev_out, stream);
 }
 
 int pm_glm_eval_device(pm_glm_t h, const double* beta, int with_prior, int want_grad, double* dev_out,

@@ -600,6 +600,7 @@ struct GlmArgs {
   // deposits this rank's (K+1) partial into every rank's mailbox over NVLink, raises its flag
   // there, waits for all ranks' flags in its own mailbox and folds in ascending rank order
   int xw, xrank;
+  int xphase;                 // 3: deposit + wait/fold (one launch); 1 / 2: one half only (split form)
   unsigned long long xepoch;  // >= 1, +1 per evaluation, identical on every rank
   double* xpeer[kMaxXchgRanks];  // mailbox base of every rank, mapped into this process
   unsigned* xstatus;          // local: set to 1 on a wait timeout
@@ -621,17 +622,20 @@ __device__ inline void xchg_finish(const GlmArgs& a, int ncols, int* flag) {
   __syncthreads();
   if (threadIdx.x == 0) {
     timed_out = 0;
-    asm volatile("fence.sc.sys;" ::: "memory");
     const size_t fo = xchg_flags_offset(a.xw, width);
-    for (int p = 0; p < a.xw; ++p) {
-      unsigned long long* f = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(a.xpeer[p]) + fo) + a.xrank;
-      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(a.xepoch) : "memory");
+    if (a.xphase & 1) {
+      asm volatile("fence.sc.sys;" ::: "memory");
+      for (int p = 0; p < a.xw; ++p) {
+        unsigned long long* f =
+            reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(a.xpeer[p]) + fo) + a.xrank;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(a.xepoch) : "memory");
+      }
     }
     const unsigned long long* mine =
         reinterpret_cast<const unsigned long long*>(reinterpret_cast<const char*>(a.xpeer[a.xrank]) + fo);
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    for (int r = 0; r < a.xw; ++r) {
+    for (int r = 0; r < ((a.xphase & 2) ? a.xw : 0); ++r) {
       while (true) {
         unsigned long long e;
         asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(e) : "l"(mine + r) : "memory");
@@ -649,6 +653,7 @@ __device__ inline void xchg_finish(const GlmArgs& a, int ncols, int* flag) {
     }
   }
   __syncthreads();
+  if (!(a.xphase & 2)) return;
   const double* data = a.xpeer[a.xrank] + size_t(a.xepoch & 1) * a.xw * width;
   for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
     double acc = __ldcv(data + c);
@@ -737,7 +742,7 @@ __device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& s
       }
       if (a.xw == 0) {
         a.out[c] = v;
-      } else {  // deposit into slot [parity][xrank] of every rank's mailbox (P2P stores)
+      } else if (a.xphase & 1) {  // deposit into slot [parity][xrank] of every rank's mailbox (P2P stores)
         const size_t o = (size_t(a.xepoch & 1) * a.xw + a.xrank) * size_t(K + 1) + c;
         for (int p = 0; p < a.xw; ++p) a.xpeer[p][o] = v;
       }

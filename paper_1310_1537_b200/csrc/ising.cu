@@ -584,6 +584,8 @@ struct pm_lat_s {
   unsigned* xticket = nullptr;             // [0] ticket, [1] status
   unsigned long long xcount[2] = {0, 0};   // deposits made per colour (identical on every rank)
   bool xready = false;                     // initial deposit done: half-sweeps use the mailbox
+  cudaEvent_t strip_done = nullptr;        // recorded after each strip half-sweep on the caller's
+                                           // stream; spin I/O on h->stream waits for it
 };
 
 namespace {
@@ -695,6 +697,10 @@ int pm_lat_destroy(pm_lat_t h) {
   {
     std::lock_guard<std::mutex> lk(h->mu);
     DeviceGuard g(h->device);
+    if (h->strip_done) {
+      cudaEventSynchronize(h->strip_done);
+      cudaEventDestroy(h->strip_done);
+    }
     cudaStreamSynchronize(h->stream);
     free_lat(h);
     cudaStreamDestroy(h->stream);
@@ -708,6 +714,10 @@ int pm_lat_set_spins(pm_lat_t h, const int8_t* s) {
   const int64_t n = int64_t(h->H) * h->W;
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard g(h->device);
+  // the neighbours' mailboxes hold this strip's boundary rows from the initial deposit:
+  // repacking the own rows now would leave those halos stale
+  if (h->strip && h->xready) return fail(PM_ESTATE, "set_spins after pm_lat_strip_xchg_start");
+  if (h->strip_done) PM_CUDA(cudaStreamWaitEvent(h->stream, h->strip_done, 0));
   // validated on the device (the reference checks the values, ising.py:64-70) before the
   // lattice state is touched: upload to the staging buffer, count invalid values, then pack
   if (!h->scratch) PM_CUDA(cudaMalloc(&h->scratch, size_t(n) + 16));
@@ -740,6 +750,7 @@ int pm_lat_get_spins(pm_lat_t h, int8_t* s) {
   const int64_t n = int64_t(h->H) * h->W;
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard g(h->device);
+  if (h->strip_done) PM_CUDA(cudaStreamWaitEvent(h->stream, h->strip_done, 0));
   if (h->packed) {
     unpack_kernel<<<grid_for(h, n / 2), 256, 0, h->stream>>>(h->scratch, h->H, h->W, h->pk0, h->pk1, h->row0,
                                                              h->strip, h->model == PM_MODEL_ISING ? 1 : 2);
@@ -843,7 +854,7 @@ static int lat_sweeps_impl(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t 
                            int32_t* acc_out = nullptr, int64_t* flips_out = nullptr);
 
 // One half-sweep (colour c) of the packed fast path; for a strip, the own rows of the strip.
-static void launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t seed, cudaStream_t st) {
+static cudaError_t launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t seed, cudaStream_t st) {
   const int Hg = h->strip ? h->H_global : h->H;
   PackedArgs pa;
   pa.other = c == 0 ? h->pk1 : h->pk0;
@@ -864,7 +875,9 @@ static void launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t seed, cud
   pa.ticket = pa.status = nullptr;
   if (h->strip && h->xready) {
     // read the other colour's latest deposit, write this colour's next one
-    const unsigned long long kr = h->xcount[c ^ 1], kw = ++h->xcount[c];
+    // (xcount[c] advances only once the launch succeeded: a failed launch must not desync the
+    // deposit numbers the neighbours wait for)
+    const unsigned long long kr = h->xcount[c ^ 1], kw = h->xcount[c] + 1;
     pa.xmb = h->xmb;
     pa.xup = h->xup;
     pa.xdown = h->xdown;
@@ -912,7 +925,8 @@ static void launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t seed, cud
   else PM_LAUNCH_NG(PM_MODEL_POTTS4, false);
 #undef PM_LAUNCH_NG
 #undef PM_LAUNCH_PACKED
-  (void)e;
+  if (e == cudaSuccess && pa.xmb) h->xcount[c] = pa.kwrite;
+  return e;
 }
 
 int pm_lat_create_strip(int device, int32_t height, int32_t width, int32_t row0, int32_t rows, int model,
@@ -966,8 +980,12 @@ int pm_lat_strip_half_sweep(pm_lat_t h, int colour, uint64_t seed, uint64_t swee
   if (h->model == PM_MODEL_ISING && h->n_class != 1) return fail(PM_EINVAL, "strips need a uniform field");
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard g(h->device);
-  launch_packed(h, colour, sweep, seed, stream ? static_cast<cudaStream_t>(stream) : h->stream);
-  PM_CUDA(cudaGetLastError());
+  const cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+  PM_CUDA(launch_packed(h, colour, sweep, seed, st));
+  if (st != h->stream) {  // order later spin I/O (h->stream) after this half-sweep
+    if (!h->strip_done) PM_CUDA(cudaEventCreateWithFlags(&h->strip_done, cudaEventDisableTiming));
+    PM_CUDA(cudaEventRecord(h->strip_done, st));
+  }
   return PM_OK;
 }
 
@@ -1177,7 +1195,7 @@ static int lat_sweeps_impl(pm_lat_t h, int32_t n_sweeps, int rng_mode, uint64_t 
       const int64_t nc = c == 0 ? n0 : n1;
       if (nc == 0) continue;
       if (fast) {
-        launch_packed(h, c, stream_pos + uint64_t(t), key0, h->stream);
+        PM_CUDA(launch_packed(h, c, stream_pos + uint64_t(t), key0, h->stream));
       } else {
         GenericArgs a;
         a.lat = view_of(h);

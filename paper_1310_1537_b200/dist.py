@@ -118,6 +118,13 @@ class PeerExchange:
         self._lib.call("pm_glm_eval_xchg", dev.handle, self._lib.dptr(beta), int(with_prior), self._h,
                        ctypes.c_void_p(out_ptr), ctypes.c_void_p(stream))
 
+    def eval_phase(self, dev, beta, with_prior: bool, phase: int, out_ptr: int, stream: int) -> None:
+        """Split form (pm_glm_eval_xchg_phase): 1 = deposit + flags, 2 = wait + fold.  With a
+        barrier between every rank's phase 1 and any rank's phase 2, no kernel waits on a
+        running kernel, so ranks sharing one GPU can use the real IPC exchange."""
+        self._lib.call("pm_glm_eval_xchg_phase", dev.handle, self._lib.dptr(beta), int(with_prior), self._h,
+                       int(phase), ctypes.c_void_p(out_ptr or None), ctypes.c_void_p(stream))
+
     def timed_out(self) -> bool:
         v = ctypes.c_int32()
         self._lib.call("pm_xchg_status", self._h, ctypes.byref(v))

@@ -219,16 +219,30 @@ class ColorPartition:
         model = _lib.PM_MODEL_POTTS4 if isinstance(lat, PottsLattice) else _lib.PM_MODEL_ISING
         self._periodic = lat.boundary == "periodic"
         self.device = LatticeDevice(h, w, lat.boundary, model, device)
+        # the bias is snapshotted here, as the reference's packed_b (ising.py:134-136); the
+        # coupling is re-read before every sweep call (the reference reads lat.w on every
+        # half-sweep, ising.py:184), see sync_coupling
+        self._coupling = None
         if model == _lib.PM_MODEL_ISING:
             b = np.ascontiguousarray(lat.b, dtype=np.float64)
             uniform_b = bool(np.all(b == b.flat[0]))
-            if uniform_b and b.flat[0] == 0.0:
-                _lib.call("pm_lat_set_ising", self.device.handle, float(lat.w), None)
-            else:
-                _lib.call("pm_lat_set_ising", self.device.handle, float(lat.w), _lib.dptr(b.ravel()))
-        else:
-            _lib.call("pm_lat_set_potts", self.device.handle, float(lat.coupling))
+            self._bias = None if (uniform_b and b.flat[0] == 0.0) else b.ravel().copy()
+        self.sync_coupling(lat)
         self.pack_from(lat)
+
+    def sync_coupling(self, lat) -> None:
+        """Upload the probability tables again if the lattice's coupling changed since the
+        last upload (e.g. an annealing schedule that sets lat.w between sweeps)."""
+        if isinstance(lat, PottsLattice):
+            c = float(lat.coupling)
+            if c != self._coupling:
+                _lib.call("pm_lat_set_potts", self.device.handle, c)
+                self._coupling = c
+        else:
+            w = float(lat.w)
+            if w != self._coupling:
+                _lib.call("pm_lat_set_ising", self.device.handle, w, _lib.dptr(self._bias))
+                self._coupling = w
 
     @property
     def n_sites(self) -> int:
@@ -266,6 +280,7 @@ def _run(lat, part: ColorPartition, rng_buffer, n_sweeps: int, diag: dict | None
     n0, n1 = part.colors[0].size, part.colors[1].size
     consumed = n_sweeps * (n0 + n1)
     dev = part.device
+    part.sync_coupling(lat)
     if isinstance(rng_buffer, SitePhilox):
         mode, k0, k1, pos, u = _lib.PM_RNG_PHILOX4X32, rng_buffer.seed, 0, rng_buffer.sweep, None
         advance = lambda: rng_buffer.advance(n_sweeps)  # noqa: E731

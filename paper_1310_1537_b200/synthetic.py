@@ -40,6 +40,32 @@ def baseline_design(n: int, k: int, seed: int = 0, intercept: bool = True, n_eva
     return x, y, beta_true, beta_eval
 
 
+def baseline_design_rows(n: int, k: int, seed: int, row0: int, row1: int, n_eval: int = 1):
+    """Rows [row0, row1) of baseline_design(n, k, seed, n_eval=n_eval) -- bit-identical (the
+    generator stream is consumed chunk by chunk exactly as there; rows outside the range are
+    drawn and dropped), holding only the requested rows in memory.  One rank's shard of
+    the one global design."""
+    gen = np.random.default_rng(seed)
+    kz = k - 1
+    step = max(1, (1 << 24) // max(kz, 1))
+    x = np.empty((row1 - row0, k))
+    for a in range(0, n, step):
+        b = min(n, a + step)
+        block = gen.standard_normal((b - a, kz))
+        lo, hi = max(a, row0), min(b, row1)
+        if lo < hi:
+            x[lo - row0:hi - row0, 0] = 1.0
+            x[lo - row0:hi - row0, 1:] = block[lo - a:hi - a]
+    beta_true = gen.normal(0.0, 0.5, k)
+    u = gen.random(n)[row0:row1]
+    y = np.empty(row1 - row0)
+    for a in range(0, row1 - row0, step):
+        b = min(row1 - row0, a + step)
+        y[a:b] = (u[a:b] < expit(x[a:b] @ beta_true)).astype(np.float64)
+    beta_eval = gen.normal(0.0, 0.1, (n_eval, k)) if n_eval > 1 else gen.normal(0.0, 0.1, k)
+    return x, y, beta_true, beta_eval
+
+
 def hb_design(n_groups: int, k: int, seed: int = 0, mean_rows: int = 2000, tau: float = 0.3):
     """Config 3: n_g~Poisson(mean_rows) (>=1); mu~N(0,0.5^2); beta_g~N(mu,tau^2 I); X~N(0,1);
     y_g~Bern(sigmoid(X_g beta_g)); the evaluation point is a fresh beta_g~N(mu,tau^2 I).

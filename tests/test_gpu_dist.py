@@ -162,10 +162,12 @@ def test_peer_exchange_single_rank_matches_single_gpu_path(gpu):
 
 def test_peer_exchange_two_ranks_one_process(gpu):
     """Two row shards on one GPU, each with its own design handle and mailbox, exchanging
-    through peer memory (same-process mailbox pointers): the two kernels run on separate
-    streams and only their finishing CTAs wait on each other (one SM each), bounded by the
-    kernel's 10 s timeout.  Both ranks must hold the ascending-rank fold of the two partials,
-    bit-identical to the NCCL path's pm_fold_rows and within 1e-10 of the oracle."""
+    through peer memory (same-process mailbox pointers).  Kernels that wait on one another
+    must not share a GPU (nothing guarantees they are co-resident), so the split form is
+    used: both ranks' phase-1 launches (stream + deposit + flags), then both phase-2
+    launches (wait -- already satisfied -- and fold), all in order on one stream.  Both
+    ranks must hold the ascending-rank fold of the two partials, bit-identical to the NCCL
+    path's pm_fold_rows and within 1e-10 of the oracle."""
     import ctypes
 
     import torch
@@ -183,15 +185,26 @@ def test_peer_exchange_two_ranks_one_process(gpu):
     boxes = [_mailbox(h) for h in xs]
     for r in range(2):
         _lib.call("pm_xchg_set_peer_ptr", xs[r], 1 - r, ctypes.c_void_p(boxes[1 - r]))
-    streams = [torch.cuda.Stream(device=0) for _ in range(2)]
+    stream = torch.cuda.Stream(device=0)
     outs = [torch.empty(k + 1, dtype=torch.float64, device="cuda:0") for _ in range(2)]
     part = [torch.empty(k + 1, dtype=torch.float64, device="cuda:0") for _ in range(2)]
     try:
-        for i in range(4):
+        # phase 2 before phase 1, and phase 1 twice, are refused
+        beta = gen.normal(0, 0.2, k)
+        with pytest.raises(RuntimeError):
+            _lib.call("pm_glm_eval_xchg_phase", devs[0].handle, _lib.dptr(beta), 1, xs[0], 2,
+                      ctypes.c_void_p(outs[0].data_ptr()), ctypes.c_void_p(stream.cuda_stream))
+        for i in range(6):
             beta = gen.normal(0, 0.2, k)
-            for r in range(2):
-                _lib.call("pm_glm_eval_xchg", devs[r].handle, _lib.dptr(beta), int(r == 0), xs[r],
-                          ctypes.c_void_p(outs[r].data_ptr()), ctypes.c_void_p(streams[r].cuda_stream))
+            for phase in (1, 2):
+                for r in range(2):
+                    _lib.call("pm_glm_eval_xchg_phase", devs[r].handle, _lib.dptr(beta), int(r == 0), xs[r], phase,
+                              ctypes.c_void_p(outs[r].data_ptr() if phase == 2 else None),
+                              ctypes.c_void_p(stream.cuda_stream))
+                if phase == 1 and i == 0:
+                    with pytest.raises(RuntimeError):
+                        _lib.call("pm_glm_eval_xchg_phase", devs[0].handle, _lib.dptr(beta), 1, xs[0], 1,
+                                  None, ctypes.c_void_p(stream.cuda_stream))
             torch.cuda.synchronize()
             a, b = outs[0].cpu().numpy(), outs[1].cpu().numpy()
             assert np.array_equal(a, b), i

@@ -292,3 +292,60 @@ def test_fp64_stream_layouts(gpu, monkeypatch, pairs):
         assert rel(r.f, f) < TOL and grel(r.g, g) < TOL, k
         assert rel(glm.loglike(d, beta), f) < TOL, k
         d.release_device()
+
+
+def test_handle_shared_by_threads_c_abi(gpu):
+    """include/pmb200.h promises that calls on one handle are serialised, so one handle
+    can serve pool threads (the reference's HB COARSE mapping, hb.py:152-161).  8 threads
+    x 100 pm_glm_eval calls straight through the C ABI on ONE handle, each with its own
+    beta: every result equals that beta's single-thread value bit for bit, and a second
+    pm_glm_launch before pm_glm_wait is refused (PM_ESTATE)."""
+    import ctypes
+    import threading
+
+    from paper_1310_1537_b200 import _lib
+    x, y, _, _ = baseline_design(60_013, 32, seed=11)
+    d = DesignMatrix(x, y)
+    dev = d.on_device(0)
+    prior = GaussianPrior.isotropic(32, 0.0, 10.0)
+    dev.set_prior(prior.mu, prior.sigma)
+    lib = _lib.load()
+    gen = np.random.default_rng(12)
+    n_threads, n_evals = 8, 100
+    betas = gen.normal(0, 0.1, (n_threads, 4, 32))  # 4 distinct betas per thread, cycled
+    ref = {}
+    for t in range(n_threads):
+        for j in range(4):
+            f = ctypes.c_double()
+            g = np.empty(32)
+            _lib.check(lib.pm_glm_eval(dev.handle, _lib.dptr(betas[t, j]), 1, 1, ctypes.byref(f), _lib.dptr(g)),
+                       "pm_glm_eval")
+            ref[t, j] = (f.value, g)
+    errors = []
+
+    def worker(t):
+        try:
+            for i in range(n_evals):
+                j = i % 4
+                f = ctypes.c_double()
+                g = np.empty(32)
+                rc = lib.pm_glm_eval(dev.handle, _lib.dptr(betas[t, j]), 1, 1, ctypes.byref(f), _lib.dptr(g))
+                if rc != 0:
+                    errors.append((t, i, "rc", rc))
+                elif f.value != ref[t, j][0] or not np.array_equal(g, ref[t, j][1]):
+                    errors.append((t, i, "mismatch"))
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append((t, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(n_threads)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors[:5]
+    # one evaluation in flight per handle
+    _lib.check(lib.pm_glm_launch(dev.handle, _lib.dptr(betas[0, 0]), 1, 1), "pm_glm_launch")
+    assert lib.pm_glm_launch(dev.handle, _lib.dptr(betas[0, 1]), 1, 1) == _lib.PM_ESTATE
+    f = ctypes.c_double()
+    _lib.check(lib.pm_glm_wait(dev.handle, ctypes.byref(f), None), "pm_glm_wait")
+    assert f.value == ref[0, 0][0]

@@ -226,31 +226,31 @@ def test_partition_accessors_match_reference(gpu):
 def test_strips_peer_halo_exchange_match_single_lattice(gpu, n_strips, model):
     """Strips exchanging halo rows through peer memory (the half-sweep kernels store their
     boundary rows into the neighbours' double-buffered mailboxes and raise flags; no host
-    copies): here all strips live on one GPU with same-process mailbox pointers, each on its
-    own stream, so neighbouring kernels wait on each other's flags (only the blocks holding
-    a boundary row wait).  Bit-identical to one lattice, and no wait timed out."""
+    copies): here all strips live on one GPU with same-process mailbox pointers.  A
+    half-sweep waits only for the neighbours' deposits of the previous half-sweep, so all
+    strips' launches go in order on ONE stream (kernels that wait on a running kernel must
+    not share a GPU).  Bit-identical to one lattice, and no wait timed out."""
     import torch
     from paper_1310_1537_b200.dist import LatticeStrip, strip_bounds
     H, W, sweeps, seed = 96, 128, 20, 41
     full = ising_spins(H, W, seed=8) if model == "ising" else potts_states(H, W, seed=8)
-    strips, streams = [], []
+    strips = []
     for k in range(n_strips):
         a, b = strip_bounds(H, n_strips, k)
         s = LatticeStrip(H, W, a, b - a, 0, model=model, w=0.8814, coupling=1.0986)
         s.set_spins(full[a:b])
         strips.append(s)
-        streams.append(torch.cuda.Stream(device=0))
+    st = torch.cuda.Stream(device=0)
     boxes = [s.xchg_mailbox() for s in strips]
     for k, s in enumerate(strips):
         s.xchg_set_peers(up=boxes[(k - 1) % n_strips], down=boxes[(k + 1) % n_strips])
     torch.cuda.synchronize()
-    for s, st in zip(strips, streams):
-        with torch.cuda.stream(st):
+    with torch.cuda.stream(st):
+        for s in strips:
             s.xchg_start()
-    for t in range(sweeps):
-        for c in (0, 1):
-            for s, st in zip(strips, streams):
-                with torch.cuda.stream(st):
+        for t in range(sweeps):
+            for c in (0, 1):
+                for s in strips:
                     s.half_sweep(c, seed, t)
     torch.cuda.synchronize()
     assert not any(s.xchg_timed_out() for s in strips)
@@ -284,3 +284,34 @@ def test_set_spins_rejects_invalid_values_on_device(gpu, model):
         with pytest.raises(ValueError):
             dev.set_spins(bad)
         np.testing.assert_array_equal(dev.get_spins(), s0)
+
+
+@pytest.mark.parametrize("model", ["ising", "potts"])
+def test_coupling_change_between_sweeps_is_used(gpu, model):
+    """The reference reads lat.w on every half-sweep (ising.py:184; the bias is the
+    partition's packed_b snapshot), so an annealing caller that changes the coupling between
+    sweep calls must see the new value: 4 sweeps at one coupling, then 5 at another, bit-exact
+    against the oracle run in the same two segments (periodic packed path and free-boundary
+    generic path)."""
+    for periodic in (True, False):
+        bnd = "periodic" if periodic else "free"
+        if model == "ising":
+            s0 = ising_spins(64, 128, seed=12)
+            b = np.random.default_rng(2).normal(0, 0.3, s0.shape) if not periodic else np.zeros(s0.shape)
+            lat = IsingLattice(s0, b, 0.3, boundary=bnd)
+        else:
+            s0 = potts_states(64, 128, seed=12)
+            lat = PottsLattice(s0, 0.4, boundary=bnd)
+        part = color_lattice(lat)
+        rng = SitePhilox(99)
+        gibbs_sweeps(lat, part, rng, 4)
+        if model == "ising":
+            lat.w = 1.2
+            ref = go.ising_sweeps(s0, None if periodic else b, 0.3, periodic, 4, go.RNG_PHILOX4X32, 99, 0, 0)
+            ref = go.ising_sweeps(ref, None if periodic else b, 1.2, periodic, 5, go.RNG_PHILOX4X32, 99, 0, 4)
+        else:
+            lat.coupling = 1.3
+            ref = go.potts_sweeps(s0, 0.4, periodic, 4, go.RNG_PHILOX4X32, 99, 0, 0)
+            ref = go.potts_sweeps(ref, 1.3, periodic, 5, go.RNG_PHILOX4X32, 99, 0, 4)
+        gibbs_sweeps(lat, part, rng, 5)
+        np.testing.assert_array_equal(lat.s, ref, err_msg=bnd)
