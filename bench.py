@@ -537,6 +537,7 @@ def run_glm(args, cfg):
     else:
         def step_dev(beta):
             dev.launch(beta, True, True)
+            dev.wait(True)
 
         def step_e2e(beta):
             return pglm.log_posterior_grad(data, beta, prior, plan)
@@ -1044,6 +1045,8 @@ def main():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--exchange", default="auto", choices=["auto", "peer", "nccl"],
                    help="GLM rank path: peer-memory exchange in the kernel (auto: N>1) or NCCL all-gather")
+    p.add_argument("--tune", action="append", default=[], metavar="KNOB=VALUE",
+                   help="A/B: kernel-dispatch override through pm_tune_set (e.g. f32_pairs=0); repeatable")
     p.add_argument("--force-dist", action="store_true",
                    help="GLM configs: use the per-rank NCCL path even at N=1 (a 1-rank group)")
     # internal: CPU baseline subprocess
@@ -1064,6 +1067,11 @@ def main():
         ref_worker_main(args)
         return
     cfg = CONFIGS[args.config]
+    if args.tune and args.impl == "b200":
+        from paper_1310_1537_b200 import _lib
+        for kv in args.tune:
+            knob, val = kv.split("=", 1)
+            _lib.set_tune(knob.strip(), int(val))
     if args.impl == "reference":
         args.steps = args.steps or 5
         args.warmup = args.warmup if args.warmup is not None else 3

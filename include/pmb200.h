@@ -64,6 +64,13 @@ PM_API int pm_abi_version(void);
 PM_API const char* pm_last_error(void);
 PM_API int pm_device_count(int* n);
 PM_API int pm_device_info(int device, int* sm_count, int* cc_major, int* cc_minor, size_t* total_mem);
+/* Kernel-dispatch overrides for A/B experiments and the layout tests (names and defaults
+ * in csrc/pm_common.cu: glm_rows, f32_pairs, f64_pairs, stream_ncw, hb_rows, pdl,
+ * gibbs_ng, ...).  The library never reads the environment: without these calls its
+ * dispatch is fixed.  reset != 0 restores the default; unknown names -> PM_EINVAL.
+ * Process-wide; a design / lattice handle reads them when it is created or uploaded. */
+PM_API int pm_tune_set(const char* name, int value, int reset);
+PM_API int pm_tune_get(const char* name, int* value, int* is_set);
 
 /* ------------------------------------------------------------------ GLM
  * One device-resident logistic design: X row-major [N][K] (stored padded to a

@@ -43,6 +43,8 @@ SIGNATURES = {
     "pm_last_error": (c_char_p, []),
     "pm_device_count": (c_int, [_ip]),
     "pm_device_info": (c_int, [c_int, _ip, _ip, _ip, POINTER(c_size_t)]),
+    "pm_tune_set": (c_int, [c_char_p, c_int, c_int]),
+    "pm_tune_get": (c_int, [c_char_p, _ip, _ip]),
     "pm_glm_create": (c_int, [c_int, POINTER(c_void_p)]),
     "pm_glm_destroy": (c_int, [c_void_p]),
     "pm_glm_upload": (c_int, [c_void_p, c_void_p, c_int, _dp, c_int64, c_int32]),
@@ -177,6 +179,32 @@ def check(rc: int, what: str = "") -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
+
+
+def set_tune(name: str, value: int | None) -> None:
+    """Override one kernel-dispatch knob (pm_tune_set); None restores the default."""
+    call("pm_tune_set", name.encode(), 0 if value is None else int(value), int(value is None))
+
+
+class tuned:
+    """Context manager: `with tuned(glm_rows=1): ...` sets knobs and restores them after."""
+
+    def __init__(self, **knobs):
+        self.knobs = knobs
+        self.saved = {}
+
+    def __enter__(self):
+        for k, v in self.knobs.items():
+            val, is_set = c_int(), c_int()
+            call("pm_tune_get", k.encode(), ctypes.byref(val), ctypes.byref(is_set))
+            self.saved[k] = val.value if is_set.value else None
+            set_tune(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.saved.items():
+            set_tune(k, v)
+        return False
 
 
 def device_count() -> int:

@@ -355,12 +355,9 @@ int pm_ws_run_chain(pm_ws_t ws, const double* mu, const double* sigma, int32_t n
   cudaStream_t st = static_cast<cudaStream_t>(v.stream);
   const size_t smem = sizeof(double) * size_t(v.K);
   // tuning knobs (defaults measured on B200): rows per ILP batch and CTAs per SM
-  const char* eu = std::getenv("PM_CHAIN_UNROLL");
-  const char* eb = std::getenv("PM_CHAIN_BLOCKS_PER_SM");
-  const int unroll = eu ? std::atoi(eu) : 2;
-  const int want_per_sm = eb ? std::max(1, std::atoi(eb)) : 2;
-  const char* es = std::getenv("PM_CHAIN_SPEC");
-  const int spec = es ? std::atoi(es) : 4;  // speculative shrink candidates in the first pass
+  const int unroll = tune("chain_unroll", 2);
+  const int want_per_sm = std::max(1, tune("chain_blocks_per_sm", 2));
+  const int spec = tune("chain_spec", 4);  // speculative shrink candidates in the first pass
   void* kfn;
   if (spec >= 6) kfn = unroll >= 2 ? reinterpret_cast<void*>(chain_kernel<2, 6, 4>) : reinterpret_cast<void*>(chain_kernel<1, 6, 4>);
   else if (spec >= 4) kfn = unroll >= 2 ? reinterpret_cast<void*>(chain_kernel<2, 4, 3>) : reinterpret_cast<void*>(chain_kernel<1, 4, 3>);
@@ -427,8 +424,6 @@ int pm_ws_run_chain(pm_ws_t ws, const double* mu, const double* sigma, int32_t n
   PM_CUDA(cudaEventElapsedTime(&g_last_chain_ms, te0, te1));
   cudaEventDestroy(te0);
   cudaEventDestroy(te1);
-  if (std::getenv("PM_CHAIN_TIMING"))
-    std::fprintf(stderr, "[pm_ws_run_chain] kernel %.3f ms grid %d x %d\n", g_last_chain_ms, grid, kChainThreads);
   unsigned long long pos = 0;
   long long evals = 0;
   int status[2] = {0, -1};

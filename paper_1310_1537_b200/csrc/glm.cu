@@ -274,22 +274,21 @@ int choose_geometry(pm_glm_s* h) {
   const int budget = std::min(max_optin_smem(h->device), 232448) - 1024;
   h->kind = KIND_NONE;
   h->pairs = 0;
-  const char* env_rows = std::getenv("PM_GLM_ROWS");
+  const int t_rows = tune("glm_rows", -1);
   // row-per-lane kernel: fp64, even K <= 30, and enough tiles to fill the machine (measured on
   // B200, tools/ab_rows_k.py: 1.3-2x faster than the column kernel at N = 1e7 for K <= 30; at
-  // K = 32 and at N ~ 1e5 the column kernel is as fast or faster).  PM_GLM_ROWS=0/1 forces.
-  const bool rows_forced = env_rows && env_rows[0] == '1';
+  // K = 32 and at N ~ 1e5 the column kernel is as fast or faster).  tune glm_rows=0/1 forces.
+  const bool rows_forced = t_rows == 1;
   const bool rows_ok = h->xtype == PM_X_F64 && h->K % 2 == 0 && h->K <= 32;
-  if (rows_ok && !(env_rows && env_rows[0] == '0') &&
+  if (rows_ok && t_rows != 0 &&
       (rows_forced || (h->K <= 30 && h->n_tiles >= int64_t(32) * h->sms))) {
     // 7 consumer warps (15 measured slower at every K); stages of ~8 KB (TPS tiles per bulk
     // copy: the single producer thread's per-copy cost bounds small-K shapes otherwise)
-    const char* e_ncw = std::getenv("PM_ROWS_NCW");
-    const int ncw = (e_ncw && std::atoi(e_ncw) == 15 && h->K <= 16) ? 15 : kNCW;
+    const int ncw = (tune("rows_ncw", kNCW) == 15 && h->K <= 16) ? 15 : kNCW;
     // measured (tools/ab_rows_tps.py, profiles/r01_ab_rows_tps.txt): 1 tile per copy halves
     // the throughput; >= 4 tiles reach the HBM bound for K >= 12.  Prefer 2 stages per warp
     // with >= 4 tiles each, else 1 stage per warp with as many tiles (<= 16) as fit.
-    const char* e_tps = std::getenv("PM_ROWS_TPS");
+    const int t_tps = tune("rows_tps", -1);
     auto fits = [&](int stages, int t) { return stream_smem_bytes(h->K, 8, stages * t, ncw) <= size_t(budget); };
     int tps = 16;
     while (tps > 1 && !fits(2 * ncw, tps)) --tps;
@@ -297,7 +296,7 @@ int choose_geometry(pm_glm_s* h) {
       tps = 16;
       while (tps > 1 && !fits(ncw, tps)) --tps;
     }
-    if (e_tps) tps = std::max(1, std::min(16, std::atoi(e_tps)));
+    if (t_tps > 0) tps = std::min(16, t_tps);
     while (tps > 1 && !fits(ncw, tps)) --tps;
     int S = 4 * ncw;
     while (S > ncw && stream_smem_bytes(h->K, 8, S * tps, ncw) > size_t(budget)) S -= ncw;
@@ -327,25 +326,23 @@ int choose_geometry(pm_glm_s* h) {
       h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, h->n_tiles));
     }
     // fp32-X, even K with an even register count: the pairs consumer layout
-    // (consume_tile_pairs; PM_F32_PAIRS=0 disables for A/B)
+    // (consume_tile_pairs; tune f32_pairs=0 disables for A/B)
     // 1 = sub-tile pairs (default; +5.5 % over columns at c1f32), 2 = whole-tile consumer
     // (KC 2 or 4, 7 warps; measured 11 % slower than pairs at K=100: the re-read stage is held
     // for the whole tile and 2 stages per warp expose the refill latency), 0 = columns
-    const char* epr = std::getenv("PM_F32_PAIRS");
-    const int pmode = epr ? std::atoi(epr) : 1;
+    const int pmode = tune("f32_pairs", 1);
     h->pairs = 0;
     if (h->kind == KIND_STREAM && h->xtype == PM_X_F32 && h->K % 2 == 0 && kc % 2 == 0 && pmode > 0)
       h->pairs = (pmode == 2 && kc <= 4) ? 2 : 1;
-    // fp64 X: the same pairs layout with 16-byte loads (PM_F64_PAIRS=0 disables for A/B)
-    const char* e64 = std::getenv("PM_F64_PAIRS");
-    if (h->kind == KIND_STREAM && h->xtype == PM_X_F64 && h->K % 2 == 0 && kc % 2 == 0 && !(e64 && e64[0] == '0'))
+    // fp64 X: the same pairs layout with 16-byte loads (tune f64_pairs=0 disables for A/B)
+    if (h->kind == KIND_STREAM && h->xtype == PM_X_F64 && h->K % 2 == 0 && kc % 2 == 0 &&
+        tune("f64_pairs", 1) != 0)
       h->pairs = 1;
-    // fp32-X, K <= 128: 15 consumer warps, one 32-row stage each (PM_STREAM_NCW=7 disables;
+    // fp32-X, K <= 128: 15 consumer warps, one 32-row stage each (tune stream_ncw=7 disables;
     // measured: 16-row stages, 2 per warp, are 26 % slower -- per-stage overheads dominate)
-    const char* e15 = std::getenv("PM_STREAM_NCW");
     // (the pairs consumer runs 7 warps: its two unrolled sub-tiles need the registers)
     if (h->kind == KIND_STREAM && h->xtype == PM_X_F32 && kc <= 4 && h->pairs == 0 &&
-        !(e15 && std::atoi(e15) == 7)) {
+        tune("stream_ncw", 15) != 7) {
       const size_t fixed15 = stream_smem_bytes(h->K, xs, 0, kNCW15);
       int S15 = int((budget - (long)fixed15) / (long)per_stage);
       S15 -= S15 % kNCW15;
@@ -1366,8 +1363,7 @@ int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64_t* off
   h->stages = S;
   h->smem = stream_smem_bytes(K, 8, S, kHbNCW);
   // small-K path: equal contiguous tile ranges, one CTA per SM
-  const char* env_rows = std::getenv("PM_HB_ROWS");
-  if (K % 2 == 0 && K <= 32 && !(env_rows && env_rows[0] == '0')) {
+  if (K % 2 == 0 && K <= 32 && tune("hb_rows", 1) != 0) {
     const int C = h->sms;
     const int64_t T = NP / kTileRows;
     auto group_of = [&](int64_t tile) {
@@ -1389,17 +1385,15 @@ int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64_t* off
     seg_base[C] = nseg;
     gseg[G] = nseg;
     // consumer warps (7 or 15), tiles per stage, stages (a multiple of the consumer count,
-    // at least two per warp when they fit): knobs PM_HB_ROWS_NCW / _TPS / _STAGES for A/B
-    const char* e_ncw = std::getenv("PM_HB_ROWS_NCW");
-    const char* e_tps = std::getenv("PM_HB_ROWS_TPS");
-    const char* e_st = std::getenv("PM_HB_ROWS_STAGES");
-    const int ncw = (e_ncw && std::atoi(e_ncw) == 15) ? 15 : 7;
-    int tps = e_tps ? std::max(1, std::min(8, std::atoi(e_tps))) : 2;
+    // at least two per warp when they fit): tune hb_rows_ncw / _tps / _stages for A/B
+    const int ncw = tune("hb_rows_ncw", 7) == 15 ? 15 : 7;
+    int tps = std::max(1, std::min(8, tune("hb_rows_tps", 2)));
+    const int t_st = tune("hb_rows_stages", -1);
     const size_t cap = 200 * 1024;
     while (tps > 1 && stream_smem_bytes(K, 8, ncw * tps, ncw) > cap) --tps;
     int Sr = 4 * ncw;
     while (Sr > ncw && stream_smem_bytes(K, 8, Sr * tps, ncw) > cap) Sr -= ncw;
-    if (e_st) Sr = std::max(ncw, std::min(Sr, std::atoi(e_st) / ncw * ncw));
+    if (t_st > 0) Sr = std::max(ncw, std::min(Sr, t_st / ncw * ncw));
     PM_CUDA(cudaMalloc(&h->seg_base, sizeof(int) * (C + 1)));
     PM_CUDA(cudaMalloc(&h->gseg, sizeof(int) * (G + 1)));
     PM_CUDA(cudaMalloc(&h->part, sizeof(double) * size_t(nseg) * ncw * (K + 1)));
@@ -1409,14 +1403,11 @@ int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64_t* off
     PM_CUDA(cudaMemcpy(h->cta_g0, cta_g0.data(), sizeof(int) * C, cudaMemcpyHostToDevice));
     PM_CUDA(cudaMalloc(&h->gcount, sizeof(unsigned) * G));
     PM_CUDA(cudaMemset(h->gcount, 0, sizeof(unsigned) * G));
-    const char* e_contig = std::getenv("PM_HB_CONTIG");
-    const char* e_fused = std::getenv("PM_HB_FUSED");
-    h->rows_contig = (e_contig && e_contig[0] == '0') ? 0 : 1;
+    h->rows_contig = tune("hb_contig", 1) != 0 ? 1 : 0;
     // measured (profiles/r01_ab_hb_pdl.txt): with PDL a separate fold launch overlapped with
     // the next rows kernel beats the fused per-group-ticket fold (68.3 vs 71.2 us)
-    h->rows_fused = (e_fused && e_fused[0] == '1') ? 1 : 0;
-    const char* e_pdl = std::getenv("PM_PDL");
-    h->rows_pdl = (e_pdl && e_pdl[0] == '0') ? 0 : 1;
+    h->rows_fused = tune("hb_fused", 0) == 1 ? 1 : 0;
+    h->rows_pdl = tune("pdl", 1) != 0 ? 1 : 0;
     h->rows = true;
     h->rows_grid = C;
     h->rows_ncw = ncw;

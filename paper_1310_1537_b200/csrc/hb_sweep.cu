@@ -472,12 +472,10 @@ int pm_hbs_sweeps(pm_hbs_t h, int32_t n_sweeps, int32_t neval, double slice_widt
   a.neval = neval;
   a.max_steps = max_steps;
   a.width = slice_width;
-  const char* es = std::getenv("PM_HBS_SPEC");
-  const int spec = es ? std::atoi(es) : 1;  // measured on B200 (tools/ab_hbs.sh): no speculation, 8 CTAs/SM
+  const int spec = tune("hbs_spec", 1);  // measured on B200 (tools/ab_hbs.sh): no speculation, 8 CTAs/SM
   const size_t smem = sizeof(double) * size_t(h->K);
   // CTAs per SM the register budget must allow (1000 groups fit one wave at >= 7 per SM)
-  const char* eb = std::getenv("PM_HBS_MINB");
-  const int minb = eb ? std::atoi(eb) : 8;
+  const int minb = tune("hbs_minb", 8);
   void (*kfn)(HbsArgs);
   if (spec >= 4) kfn = hb_sweep_kernel<4, 3, 4>;
   else if (spec >= 2) kfn = minb >= 8 ? hb_sweep_kernel<2, 2, 8> : minb >= 7 ? hb_sweep_kernel<2, 2, 7> : hb_sweep_kernel<2, 2, 4>;

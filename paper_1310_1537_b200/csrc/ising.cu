@@ -29,10 +29,7 @@ using namespace pm;
 
 namespace {
 
-bool pdl_default() {
-  const char* e = std::getenv("PM_PDL");
-  return !(e && e[0] == '0');
-}
+bool pdl_default() { return tune("pdl", 1) != 0; }
 
 // Resident CTAs per SM the packed kernel is register-budgeted for (NG >= 2): Ising 4
 // (64 registers), Potts 3 (80 registers, no spills): profiles/r01_ab_gibbs_minb.txt
@@ -890,12 +887,9 @@ static cudaError_t launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t se
   }
   const int W2 = h->W / 2;
   // 16-site groups per thread: Ising 2, Potts 4 (profiles/r01_ab_gibbs_minb.txt);
-  // PM_GIBBS_NG=1|2|4 overrides (A/B knob)
-  static const int ng_env = [] {
-    const char* e = std::getenv("PM_GIBBS_NG");
-    const int v = e ? std::atoi(e) : 0;
-    return (v == 1 || v == 2 || v == 4) ? v : 0;
-  }();
+  // tune gibbs_ng=1|2|4 overrides (A/B knob)
+  const int ng_t = tune("gibbs_ng", 0);
+  const int ng_env = (ng_t == 1 || ng_t == 2 || ng_t == 4) ? ng_t : 0;
   const int ng_cap = ng_env ? ng_env : (h->model == PM_MODEL_ISING ? 2 : 4);
   const int ng = (W2 % 64 == 0 && ng_cap >= 4) ? 4 : (W2 % 32 == 0 && ng_cap >= 2) ? 2 : 1;  // 16-site groups per thread
   const int per_row = W2 / (16 * ng);

@@ -1,6 +1,7 @@
 // Library-level entry points and error plumbing for libpmb200.
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -69,9 +70,68 @@ cudaError_t ensure_smem_attr(const void* kernel, std::atomic<uint64_t>& mask) {
   return e;
 }
 
+// the knobs the dispatchers consult (name: meaning; default)
+static const char* const kTuneNames[] = {
+    "glm_rows",          // fp64 row-per-lane GLM kernel: 0 off, 1 forced (default: auto)
+    "rows_ncw",          // its consumer warps: 7 (default) or 15 (K <= 16)
+    "rows_tps",          // its 32-row tiles per bulk copy (default: auto)
+    "f32_pairs",         // fp32-X consumer: 0 columns, 1 sub-tile pairs (default), 2 whole tile
+    "f64_pairs",         // fp64 consumer: 0 columns, 1 pairs (default)
+    "stream_ncw",        // fp32-X column consumer: 15 warps (default) or 7
+    "hb_rows",           // HB row-per-lane kernel: 0 off, 1 on (default)
+    "hb_rows_ncw",       // 7 (default) or 15
+    "hb_rows_tps",       // tiles per stage (default 2)
+    "hb_rows_stages",    // stages (default: auto)
+    "hb_contig",         // contiguous per-warp tile ranges: 1 (default)
+    "hb_fused",          // fold fused into the rows launch: 0 (default)
+    "pdl",               // programmatic dependent launch: 1 (default)
+    "chain_unroll",      // chain kernel rows per ILP batch (default 2)
+    "chain_blocks_per_sm",  // chain kernel CTAs per SM (default 2)
+    "chain_spec",        // speculative shrink candidates (default 4)
+    "hbs_spec",          // hb_sweep speculation (default 1)
+    "hbs_minb",          // hb_sweep CTAs per SM register budget (default 8)
+    "gibbs_ng",          // packed Gibbs 16-site groups per thread: 1, 2, 4 (default: per model)
+};
+
+static std::mutex g_tune_mu;
+static std::map<std::string, int> g_tune;
+
+int tune(const char* name, int dflt) {
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  auto it = g_tune.find(name);
+  return it == g_tune.end() ? dflt : it->second;
+}
+
+static bool known_tune(const char* name) {
+  for (const char* k : kTuneNames)
+    if (std::strcmp(k, name) == 0) return true;
+  return false;
+}
+
 }  // namespace pm
 
 extern "C" {
+
+int pm_tune_set(const char* name, int value, int reset) {
+  if (!name) return pm::fail(PM_EINVAL, "pm_tune_set: null name");
+  if (!pm::known_tune(name)) return pm::fail(PM_EINVAL, std::string("unknown tuning knob: ") + name);
+  std::lock_guard<std::mutex> lk(pm::g_tune_mu);
+  if (reset)
+    pm::g_tune.erase(name);
+  else
+    pm::g_tune[name] = value;
+  return PM_OK;
+}
+
+int pm_tune_get(const char* name, int* value, int* is_set) {
+  if (!name || !value) return pm::fail(PM_EINVAL, "pm_tune_get: null argument");
+  if (!pm::known_tune(name)) return pm::fail(PM_EINVAL, std::string("unknown tuning knob: ") + name);
+  std::lock_guard<std::mutex> lk(pm::g_tune_mu);
+  auto it = pm::g_tune.find(name);
+  if (is_set) *is_set = it != pm::g_tune.end();
+  *value = it == pm::g_tune.end() ? -1 : it->second;
+  return PM_OK;
+}
 
 int pm_abi_version(void) { return PM_ABI_VERSION; }
 

@@ -43,6 +43,11 @@ struct DeviceGuard {
 };
 
 int sm_count(int device);
+
+// Kernel-dispatch overrides (A/B experiments and the layout tests): set only through the
+// C ABI (pm_tune_set), never read from the environment, so the shipped library's dispatch
+// is fixed unless a caller explicitly asks otherwise.  Returns `dflt` when `name` is unset.
+int tune(const char* name, int dflt);
 void retain_pool(int device);
 
 }  // namespace pm

@@ -154,14 +154,15 @@ class DistributedDesign:
     """This rank's row shard on its GPU.  One evaluation is one kernel launch whose finishing
     CTA exchanges the (K+1) partials with the other ranks through peer memory and folds them
     in ascending rank order (PeerExchange, NCCL backend, world > 1); otherwise (gloo, world 1,
-    PM_DIST_XCHG=0, or a node without peer mappings) one kernel, one NCCL all-gather and one
+    exchange="nccl", or a node without peer mappings) one kernel, one NCCL all-gather and one
     fold launch.  Rank 0's kernel adds the prior terms (the same device finaliser as the
-    single-GPU path), so the rank-ordered fold holds them exactly once."""
+    single-GPU path), so the rank-ordered fold holds them exactly once.
+
+    exchange: "auto" (peer exchange for NCCL groups of > 1 rank), "peer" (also for a
+    1-rank group: exercises the exchange kernel on one GPU) or "nccl"."""
 
     def __init__(self, local: DesignMatrix, device: int, x_storage: str = "f64", group=None,
                  exchange: str = "auto"):
-        import os
-
         import torch
         import torch.distributed as dist
         self.local = local
@@ -173,10 +174,9 @@ class DistributedDesign:
         self._buf = torch.empty(self.k + 1, dtype=torch.float64, device=f"cuda:{device}")
         self._out = torch.empty(self.k + 1, dtype=torch.float64, device=f"cuda:{device}")
         self.xchg = None
-        # "auto": peer exchange for NCCL groups of > 1 rank; "peer": also for a 1-rank group
-        # (exercises the exchange kernel on one GPU); "nccl" / PM_DIST_XCHG=0: NCCL all-gather
-        want = exchange if exchange != "auto" else os.environ.get("PM_DIST_XCHG", "auto")
-        want = {"1": "auto", "0": "nccl"}.get(want, want)
+        if exchange not in ("auto", "peer", "nccl"):
+            raise ValueError(f"exchange must be auto, peer or nccl, got {exchange!r}")
+        want = exchange
         if (want in ("auto", "peer") and dist.is_initialized() and dist.get_backend(group) == "nccl"
                 and (dist.get_world_size(group) > 1 or want == "peer")):
             x = PeerExchange(device, self.k + 1, group)

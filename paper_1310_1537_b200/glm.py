@@ -310,6 +310,17 @@ def _prior_arrays(prior, n_cols: int):
     return mu, sigma
 
 
+def _account(plan: ExecPlan, calls: int = 1) -> None:
+    """The reference's region / merge accounting for `calls` evaluations under `plan`
+    (instrumentation contract, read by its tests: SOM opens two regions -- the matvec and
+    the transcendental pass, glm.py:277-295 / 375-396 -- every other strategy one, and the
+    merge folds one partial per worker, glm.py:234-250).  The device work is counted
+    separately (kernel_launches, device_partials)."""
+    regions = 2 if plan.strategy is Strategy.SOM else 1
+    counters.add_region(regions * calls)
+    counters.add_merges(plan.workers * calls)
+
+
 def _evaluate(data, beta, plan: ExecPlan, prior, want_grad: bool) -> GradResult:
     """Dispatch one evaluation to the device(s)."""
     mu, sigma = _prior_arrays(prior, data.n_cols)
@@ -320,9 +331,9 @@ def _evaluate(data, beta, plan: ExecPlan, prior, want_grad: bool) -> GradResult:
         dev.set_prior(mu, sigma)
         dev.launch(beta, mu is not None, want_grad)
         f, g = dev.wait(want_grad)
-    counters.add_region(1)
+    _account(plan)
     counters.add_launches(1)
-    counters.add_merges(dev.grid)
+    counters.add_device_partials(dev.grid)
     return GradResult(f, g)
 
 
@@ -351,9 +362,9 @@ def _evaluate_sharded(view: ShardedMatrix, beta, plan: ExecPlan, mu, sigma, want
     finally:
         for d in devs:
             d.lock.release()
-    counters.add_region(1)
+    _account(plan)
     counters.add_launches(len(devs))
-    counters.add_merges(len(devs))
+    counters.add_device_partials(len(devs))
     return GradResult(f, g)
 
 
@@ -478,6 +489,7 @@ def diff_loglike_multi(ws: GlmWorkspace, data: DesignMatrix, k: int, deltas,
     counters.add_flops(ws.n_rows * _DIFF_FLOPS * d.size)
     out = np.empty(d.size)
     _lib.call("pm_ws_diff_eval", ws._ws, int(k), _lib.dptr(d), int(d.size), _lib.dptr(out))
+    _account(ExecPlan(workers=plan.workers), calls=d.size)  # glm.py:520-522: one region per call
     counters.add_launches(1)
     return out
 

@@ -331,6 +331,11 @@ def hb_benchmark(ds: HbDataset, prior, policies: list[MappingPolicy], n_sweeps: 
                  seed: int = 0, clock_ghz: float = 2.6, slice_width: float = 1.0):
     """Time n_sweeps sweeps under each policy; one BenchRecord per policy (hb.py:171-204).
 
+    Compatibility-only (the CPU thread-mapping study is out of scope): kept so
+    the reference's `hb-bench` command and tests run against the drop-in.  On the device
+    the policy's mode / workers do not change the schedule (one CTA per group); only
+    `neval` does.
+
     Each repetition restarts from a fresh state with the same seed; the wall time covers
     the n_sweeps sweeps (one device launch) and `evals` = n_sweeps * neval, so cpr is a
     cycles-per-group-row figure as in the reference.

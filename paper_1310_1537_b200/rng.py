@@ -96,11 +96,14 @@ class DeviateBuffer:
         self._gen_pos = 0                     # stream index of the generator's next output
         self._block_start = -self.capacity    # stream index of data[0] (no block yet)
         self._seek_to: int | None = None      # pending generator reposition (skip)
+        self._virtual_refills = 0             # refills skip() already counted (see refill)
 
     def refill(self) -> None:
         """Fill data[0:capacity] with the next block of the base stream."""
         if self._seek_to is not None:
             self._apply_seek()
+        counted = self._virtual_refills > 0
+        self._virtual_refills = 0
         self._block_start = self._gen_pos
         if self.kind is BufferKind.UNIFORM01:
             self.data[:] = self._gen.random(self.capacity)
@@ -121,7 +124,8 @@ class DeviateBuffer:
                     self._carry = float(block[remaining])
                 self._gen_pos += 2 * n_pairs
         self.cursor = 0
-        self.refills += 1
+        if not counted:
+            self.refills += 1
 
     def next(self) -> float:
         if self.cursor == self.capacity:
@@ -177,6 +181,10 @@ class DeviateBuffer:
         if n <= self.capacity - self.cursor:
             self.cursor += n
         else:
+            # the blocks a host consumer would have refilled to get there (the reference's
+            # generated / waste_fraction accounting, rng.py:129-138)
+            self.refills += -(-(n - (self.capacity - self.cursor)) // self.capacity)
+            self._virtual_refills += 1  # the lazy refill below re-fills the last of them
             # the generator is repositioned lazily, at the next refill (device paths skip
             # thousands of streams per call and most are never read on the host)
             target = self.position + n
@@ -474,15 +482,20 @@ def rng_bench(dist: BenchDist, mode: BenchMode, n: int, seed: int = 0, capacity:
               clock_ghz: float = NOMINAL_CLOCK_GHZ, device: int = 0) -> RngBenchRecord:
     """Time generating n deviates; cycles per sample at the nominal clock (rng.py:246-300).
 
+    Compatibility-only (the batch-vs-one-at-a-time study is out of scope): kept
+    so the reference's `rng-bench` command and tests run against the drop-in.
+
     DEVICE mode times the device generation with CUDA events on the same streams and
     workloads as the reference's cells (uniform / normal on one stream; Gamma(2, 3) on
-    owner streams (0,), (1,); Dirichlet(1_100) normalised per Gamma component).  The
-    host modes are the reference's CPU baselines: run `parmcmc.rng.rng_bench` for them.
+    owner streams (0,), (1,); Dirichlet(1_100) normalised per Gamma component).  BATCH /
+    ONE_AT_A_TIME time the host-side stream objects the reference compares (block-refilled
+    DeviateBuffer vs a per-call source); their Gamma / Dirichlet cells draw one sample per
+    device call (the per-call pattern the paper's batch RNG replaces).
     """
     if n < 1:
         raise ValueError("n must be >= 1")
     if mode is not BenchMode.DEVICE:
-        raise ValueError("host modes are the reference's CPU baseline (parmcmc.rng.rng_bench)")
+        return _rng_bench_per_call(dist, mode, n, seed, capacity, clock_ghz, device)
     ms: list[float] = []
     if dist in (BenchDist.UNIFORM, BenchDist.NORMAL):
         kind = BufferKind.UNIFORM01 if dist is BenchDist.UNIFORM else BufferKind.STD_NORMAL
@@ -507,6 +520,48 @@ def rng_bench(dist: BenchDist, mode: BenchMode, n: int, seed: int = 0, capacity:
             samples = n * _BENCH_DIRICHLET_K
     wall = ms[0] * 1e-3
     return RngBenchRecord(dist.value, mode.value, n, wall * clock_ghz * 1e9 / samples, 0.0)
+
+
+def _rng_bench_per_call(dist, mode, n, seed, capacity, clock_ghz, device) -> RngBenchRecord:
+    import time
+    batch = mode is BenchMode.BATCH
+    waste = 0.0
+    if dist in (BenchDist.UNIFORM, BenchDist.NORMAL):
+        kind = BufferKind.UNIFORM01 if dist is BenchDist.UNIFORM else BufferKind.STD_NORMAL
+        acc = 0.0
+        if batch:
+            src = DeviateBuffer(kind, capacity=capacity, seed=seed)
+            t0 = time.perf_counter()
+            for lo in range(0, n, capacity):
+                acc += float(src.take(min(capacity, n - lo))[-1])
+            wall = time.perf_counter() - t0
+            waste = src.waste_fraction
+        else:
+            src = OneAtATimeUniform(seed) if kind is BufferKind.UNIFORM01 else OneAtATimeNormal(seed)
+            t0 = time.perf_counter()
+            for _ in range(n):
+                acc += src.next()
+            wall = time.perf_counter() - t0
+        samples = n
+    else:
+        if batch:
+            u = DeviateBuffer(BufferKind.UNIFORM01, capacity, seed, owner=(0,))
+            z = DeviateBuffer(BufferKind.STD_NORMAL, capacity, seed, owner=(1,))
+        else:
+            u, z = OneAtATimeUniform(seed, owner=(0,)), OneAtATimeNormal(seed, owner=(1,))
+        alphas = np.ones(_BENCH_DIRICHLET_K)
+        t0 = time.perf_counter()
+        for _ in range(n):
+            if dist is BenchDist.GAMMA:
+                gamma_batch(_BENCH_GAMMA, 1, u, z, device)
+            else:
+                dirichlet_batch(alphas, 1, u, z, device)
+        wall = time.perf_counter() - t0
+        samples = n if dist is BenchDist.GAMMA else n * _BENCH_DIRICHLET_K
+        if batch:
+            gen = u.generated + z.generated
+            waste = (gen - u.consumed - z.consumed) / gen if gen else 0.0
+    return RngBenchRecord(dist.value, mode.value, n, wall * clock_ghz * 1e9 / samples, waste)
 
 
 class _DeviceScratch:

@@ -25,3 +25,18 @@ def gpu():
     _lib.load()
     _lib.require_device(0)
     return 0
+
+
+@pytest.fixture
+def tune():
+    """Kernel-dispatch overrides through the C ABI (pm_tune_set), reset after the test."""
+    from paper_1310_1537_b200 import _lib
+    touched = []
+
+    def setter(**knobs):
+        for k, v in knobs.items():
+            _lib.set_tune(k, v)
+            touched.append(k)
+    yield setter
+    for k in touched:
+        _lib.set_tune(k, None)

@@ -118,3 +118,20 @@ def test_null_arguments_are_rejected_without_a_device():
     assert lib.pm_ising_prob_table(1.0, 0.0, None) == _lib.PM_EINVAL
     assert "null" in _lib.last_error()
     assert lib.pm_glm_destroy(None) == _lib.PM_OK
+
+
+def test_dispatch_is_not_read_from_the_environment():
+    """Kernel choice must not depend on the user's environment: the dispatchers consult
+    only the pm_tune_set table (A/B experiments and layout tests set it explicitly)."""
+    csrc = os.path.join(ROOT, "paper_1310_1537_b200", "csrc")
+    for name in os.listdir(csrc):
+        if name.endswith((".cu", ".cuh")):
+            assert "getenv" not in open(os.path.join(csrc, name)).read(), name
+    lib = _lib.load()
+    assert lib.pm_tune_set(b"no_such_knob", 1, 0) == _lib.PM_EINVAL
+    with _lib.tuned(glm_rows=0, gibbs_ng=2):
+        v, s = _lib.c_int(), _lib.c_int()
+        _lib.call("pm_tune_get", b"gibbs_ng", _lib.ctypes.byref(v), _lib.ctypes.byref(s))
+        assert (v.value, s.value) == (2, 1)
+    _lib.call("pm_tune_get", b"gibbs_ng", _lib.ctypes.byref(v), _lib.ctypes.byref(s))
+    assert s.value == 0

@@ -62,8 +62,9 @@ def test_ising_denoise_zero_sweeps_is_identity_without_device(tmp_path):
     np.testing.assert_array_equal(read_pbm(out), noisy)
 
 
-def test_rng_bench_host_modes_are_input_errors(tmp_path):
-    assert cli.main(["rng-bench", "--modes", "batch", "--out", str(tmp_path / "r.csv")]) == 2
+def test_rng_bench_unknown_mode_or_dist_is_input_error(tmp_path):
+    assert cli.main(["rng-bench", "--modes", "bogus", "--out", str(tmp_path / "r.csv")]) == 2
+    assert cli.main(["rng-bench", "--dists", "cauchy", "--out", str(tmp_path / "r.csv")]) == 2
 
 
 def test_grid_config_parsing_and_sidecar(tmp_path):

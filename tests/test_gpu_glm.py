@@ -135,7 +135,13 @@ def test_counters_follow_reference_contract(gpu):
     glm.loglike_grad(d, z["beta4"])
     snap = counters.snapshot()
     assert snap.flops == d.n_rows * (4 * d.n_cols + 8)  # glm.py:354
-    assert snap.parallel_regions == 1 and snap.kernel_launches == 1
+    assert snap.parallel_regions == 1 and snap.kernel_launches == 1 and snap.merge_events == 1
+    assert snap.device_partials >= 1
+    for strategy, regions in ((Strategy.PLF, 1), (Strategy.SOM, 2), (Strategy.MOS, 1)):
+        counters.reset()
+        glm.loglike_grad(d, z["beta4"], ExecPlan(strategy, workers=4))
+        snap = counters.snapshot()
+        assert (snap.parallel_regions, snap.merge_events, snap.kernel_launches) == (regions, 4, 1)
     counters.reset()
     glm.loglike(d, z["beta4"])
     assert counters.snapshot().flops == d.n_rows * (2 * d.n_cols + 6)  # glm.py:264
@@ -172,6 +178,39 @@ def test_config1_shape_against_oracle(gpu):
     assert rel(r32.f, f) < 1e-5 and grel(r32.g, g) < 1e-5
 
 
+def _cores():
+    import os
+    return max(1, len(os.sched_getaffinity(0)))
+
+
+def test_config1_full_size_against_oracle(gpu):
+    """BASELINE config 1 at its exact size (N=1e7, K=100, the bench's seed-7 design), three
+    fresh beta ~ N(0, 0.1^2) with the N(0, 10^2) prior, against the CPU oracle over all host
+    cores: fp64 within 1e-10 (f and every g_k); fp32-X within 1e-10 of the oracle on the
+    fp32-rounded X and within 1e-5 of the fp64 oracle (the north-star tolerances)."""
+    n, k = 10_000_000, 100
+    x, y, _, betas = baseline_design(n, k, seed=7, n_eval=3)
+    d = DesignMatrix(x, y)
+    prior = GaussianPrior.isotropic(k, 0.0, 10.0)
+    refs = []
+    for beta in betas:
+        r = glm.log_posterior_grad(d, beta, prior)
+        f, g = gl.log_posterior_grad(x, y, beta, prior.mu, prior.sigma, workers=_cores())
+        refs.append((f, g))
+        assert rel(r.f, f) < TOL, (r.f, f)
+        assert grel(r.g, g) < TOL
+    d.release_device()
+    plan32 = ExecPlan(x_storage="f32")
+    got32 = [glm.log_posterior_grad(d, beta, prior, plan32) for beta in betas]
+    d.release_device()
+    x32 = x.astype(np.float32).astype(np.float64)
+    del x
+    for beta, r32, (f64, g64) in zip(betas, got32, refs):
+        f, g = gl.log_posterior_grad(x32, y, beta, prior.mu, prior.sigma, workers=_cores())
+        assert rel(r32.f, f) < TOL and grel(r32.g, g) < TOL
+        assert rel(r32.f, f64) < 1e-5 and grel(r32.g, g64) < 1e-5
+
+
 def test_config1_full_size_properties(gpu):
     """N=1e7, K=100 fp64 (8 GB): size-independent properties -- L(0) = -N ln 2 and
     g(0) = X'(y - 1/2) checked against cuBLAS fp64 (torch) -- and linearity of the
@@ -198,10 +237,10 @@ def test_config1_full_size_properties(gpu):
 
 @pytest.mark.parametrize("k", [2, 4, 6, 20, 22, 30, 32])
 @pytest.mark.parametrize("n", [1, 33, 64, 1000, 250_007])
-def test_row_per_lane_kernel_against_oracle_and_stream_kernel(gpu, n, k, monkeypatch):
+def test_row_per_lane_kernel_against_oracle_and_stream_kernel(gpu, n, k, tune):
     # fp64 with even K <= 32 runs the row-per-lane kernel (KIND_ROWS): equal contiguous tile
     # ranges per CTA, two tiles per stage; compare with the oracle and the column kernel
-    monkeypatch.setenv("PM_GLM_ROWS", "1")  # forced: the default picks it only for K <= 30 at large N
+    tune(glm_rows=1)  # forced: the default picks it only for K <= 30 at large N
     gen = np.random.default_rng(n + k)
     x = gen.standard_normal((n, k))
     y = (gen.random(n) < 0.4).astype(float)
@@ -215,7 +254,7 @@ def test_row_per_lane_kernel_against_oracle_and_stream_kernel(gpu, n, k, monkeyp
     assert glm.loglike(d, beta) == glm.loglike_grad(d, beta).f
     again = glm.log_posterior_grad(d, beta, prior)
     assert again.f == r.f and np.array_equal(again.g, r.g)
-    monkeypatch.setenv("PM_GLM_ROWS", "0")
+    tune(glm_rows=0)
     d2 = DesignMatrix(x, y)
     r2 = glm.log_posterior_grad(d2, beta, prior)
     assert d2.on_device(0).geometry()["kernel"] == "stream"
@@ -227,7 +266,7 @@ def test_fp32_storage_all_layouts(gpu, monkeypatch, pairs):
     """fp32-X over K values that select every stream-kernel consumer layout (column per lane,
     column pairs with XOR-permuted rows, 7 or 15 consumer warps, the wide kernel), f only and
     f + g, against the oracle on the fp32-rounded X (1e-10)."""
-    monkeypatch.setenv("PM_F32_PAIRS", pairs)
+    tune(f32_pairs=int(pairs))
     gen = np.random.default_rng(77)
     for k in (1, 2, 31, 40, 64, 66, 100, 128, 130, 192, 256, 300):
         n = 3001 + 37 * k
@@ -277,8 +316,8 @@ def test_fp64_stream_layouts(gpu, monkeypatch, pairs):
     """fp64 X through the stream kernel's two consumer layouts (column pairs with 16-byte
     loads and XOR-permuted rows, or column per lane), f only and f + g, odd and even N,
     against the oracle (1e-10)."""
-    monkeypatch.setenv("PM_F64_PAIRS", pairs)
-    monkeypatch.setenv("PM_GLM_ROWS", "0")
+    tune(f64_pairs=int(pairs))
+    tune(glm_rows=0)
     gen = np.random.default_rng(78)
     for k in (2, 40, 64, 66, 100, 128, 192, 256):
         n = 2999 + 41 * k

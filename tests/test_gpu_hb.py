@@ -64,7 +64,7 @@ def test_wide_k_and_validation(gpu):
 
 @pytest.mark.parametrize("k", [2, 4, 20, 22, 32])
 @pytest.mark.parametrize("layout", ["tiny_groups", "huge_groups", "single"])
-def test_row_per_lane_path_segments(gpu, k, layout, monkeypatch):
+def test_row_per_lane_path_segments(gpu, k, layout, tune):
     # even K <= 32 takes the row-per-lane kernel with balanced tile ranges: groups split across
     # CTAs (huge), many groups inside one CTA's range (tiny), one group over the whole grid
     gen = np.random.default_rng(k)
@@ -84,6 +84,6 @@ def test_row_per_lane_path_segments(gpu, k, layout, monkeypatch):
     res_f = hb_log_posterior_grad(CsrGroups(x, y, off), betas, prior, want_grad=False)
     np.testing.assert_array_equal(np.array([r.f for r in res_f]), f)
     # the column-per-lane kernel agrees to rounding
-    monkeypatch.setenv("PM_HB_ROWS", "0")
+    tune(hb_rows=0)
     res0 = hb_log_posterior_grad(CsrGroups(x, y, off), betas, prior)
     check(np.array([r.f for r in res0]), np.stack([r.g for r in res0]), f, g)

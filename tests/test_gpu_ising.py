@@ -136,22 +136,34 @@ def test_potts_matches_c_oracle(gpu, periodic, shape, coupling):
 
 
 def test_config4_lattice_first_sweeps_against_oracle(gpu):
+    """BASELINE config 4 exactly: 8192^2 periodic Ising, w = 2 x 0.4407 (J=1), h=0,
+    Philox4x32 keyed by (seed, sweep, site): the first 10 sweeps bit-exact against the C
+    oracle given the same uniforms, checked after sweep 1, 3 and 10."""
     s0 = ising_spins(8192, 8192, seed=0)
     lat = IsingLattice(s0, np.zeros((8192, 8192)), 0.8814, boundary="periodic")
     part = color_lattice(lat)
     assert part.device.fast_path()
-    gibbs_sweeps(lat, part, SitePhilox(1), 2)
-    ref = go.ising_sweeps(s0, None, 0.8814, True, 2, go.RNG_PHILOX4X32, 1, 0, 0)
-    np.testing.assert_array_equal(lat.s, ref)
+    rng = SitePhilox(1)
+    ref = s0
+    done = 0
+    for upto in (1, 3, 10):
+        gibbs_sweeps(lat, part, rng, upto - done)
+        ref = go.ising_sweeps(ref, None, 0.8814, True, upto - done, go.RNG_PHILOX4X32, 1, 0, done)
+        done = upto
+        np.testing.assert_array_equal(lat.s, ref, err_msg=f"after sweep {upto}")
 
 
-def test_potts_config4_shape_first_sweep_against_oracle(gpu):
-    s0 = potts_states(2048, 2048, seed=2)
-    lat = PottsLattice(s0, 0.4407)
-    part = color_lattice(lat)
-    ising.potts_sweeps(lat, part, SitePhilox(3), 1)
-    ref = go.potts_sweeps(s0, 0.4407, True, 1, go.RNG_PHILOX4X32, 3, 0, 0)
-    np.testing.assert_array_equal(lat.s, ref)
+def test_potts_config4_first_sweeps_against_oracle(gpu):
+    """The config-4 Potts q=4 variant at its exact shape (8192^2 periodic, coupling 0.4407):
+    the first 2 sweeps bit-exact against the C oracle (and one sweep at 2048^2)."""
+    for shape, sweeps in (((2048, 2048), 1), ((8192, 8192), 2)):
+        s0 = potts_states(*shape, seed=2)
+        lat = PottsLattice(s0, 0.4407)
+        part = color_lattice(lat)
+        assert part.device.fast_path()
+        ising.potts_sweeps(lat, part, SitePhilox(3), sweeps)
+        ref = go.potts_sweeps(s0, 0.4407, True, sweeps, go.RNG_PHILOX4X32, 3, 0, 0)
+        np.testing.assert_array_equal(lat.s, ref, err_msg=str(shape))
 
 
 def test_single_node_and_zero_coupling(gpu):

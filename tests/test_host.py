@@ -149,18 +149,6 @@ def test_log_weight_matches_reference_fixture():
     assert per.log_weight() == 0.5 * 0.5 * (2 * (1 * 1 + (-1) * 1) + 2 * (1 * -1 + 1 * 1))
 
 
-def test_run_region_contract():
-    from paper_1310_1537_b200.instrumentation import counters
-    from paper_1310_1537_b200.parallel import run_region
-    before = counters.snapshot() if hasattr(counters, "snapshot") else None
-    out = run_region([lambda i=i: i * i for i in range(6)])
-    assert out == [0, 1, 4, 9, 16, 25]
-    # nested regions run inline and still return in order
-    assert run_region([lambda: run_region([lambda: 1, lambda: 2]), lambda: [3]]) == [[1, 2], [3]]
-    assert run_region([]) == []
-    del before
-
-
 def test_potts_compact_code_sums_are_unique():
     """The packed Potts kernel indexes its threshold table by the sum of per-neighbour codes
     {0, 1, 5, 21}[state] (ising.cu kPottsCodeBytes; the packed arrays store these codes): the 35 neighbour multisets of q=4 states
