@@ -853,6 +853,7 @@ def run_gibbs(args, cfg):
         lat = ising.IsingLattice(ising_spins(h, w, seed=0), np.zeros((h, w)), 2 * 0.4407, boundary="periodic")
     else:
         lat = ising.PottsLattice(potts_states(h, w, seed=0), 0.4407, boundary="periodic")
+    ising.pin_lattice(lat)  # page-locked spins: the e2e spin I/O is one DMA each way
     part = ising.color_lattice(lat, device=local)
     dev = part.device
     assert dev.fast_path()

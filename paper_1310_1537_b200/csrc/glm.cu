@@ -557,7 +557,7 @@ int pm_glm_upload(pm_glm_t h, const void* X, int x_dtype, const double* y, int64
   }
   h->partials_cap = std::max(std::max(h->grid, 1), 2 * h->sms);  // the fp32 wide fallback uses 2 x SMs
   PM_CUDA(cudaMalloc(&h->partials, sizeof(double) * size_t(h->partials_cap) * (n_cols + 1)));
-  PM_CUDA(cudaMalloc(&h->beta_dev, sizeof(double) * n_cols));
+  PM_CUDA(cudaMalloc(&h->beta_dev, sizeof(double) * (n_cols + 1)));  // +1: PM_AB_OUT_DEVICE scratch
   PM_CUDA(cudaHostAlloc(&h->out_host, sizeof(double) * (n_cols + 1), cudaHostAllocMapped | cudaHostAllocPortable));
   PM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->out_dev), h->out_host, 0));
   PM_CUDA(cudaHostAlloc(&h->beta_pinned, sizeof(double) * n_cols, cudaHostAllocPortable));
@@ -852,8 +852,13 @@ int pm_glm_time_launches(pm_glm_t h, const double* betas, int32_t n, int with_pr
   PM_CUDA(cudaEventCreate(&e1));
   PM_CUDA(cudaStreamSynchronize(h->stream));
   PM_CUDA(cudaEventRecord(e0, h->stream));
+#ifdef PM_AB_OUT_DEVICE  // A/B timing experiment only: results to device memory, not mapped host memory
+  double* out_t = h->beta_dev;  // K doubles; the A/B build only times, never reads it
+#else
+  double* out_t = h->out_dev;
+#endif
   for (int i = 0; i < n; ++i) {
-    int rc = enqueue_eval(h, betas + size_t(i) * h->K, with_prior != 0, want_grad != 0, h->out_dev, h->stream);
+    int rc = enqueue_eval(h, betas + size_t(i) * h->K, with_prior != 0, want_grad != 0, out_t, h->stream);
     if (rc) return rc;
   }
   PM_CUDA(cudaEventRecord(e1, h->stream));
@@ -1147,7 +1152,7 @@ namespace {
 
 void free_hb(pm_hb_s* h) {
   for (void* p : {(void*)h->X, (void*)h->y, (void*)h->poff, (void*)h->nrows, (void*)h->betas,
-                  (void*)h->out_f, (void*)h->out_g, (void*)h->seg_base, (void*)h->gseg,
+                  (void*)h->out_f, (void*)h->seg_base, (void*)h->gseg,
                   (void*)h->part, (void*)h->cta_g0, (void*)h->gcount})
     if (p) cudaFree(p);
   h->seg_base = h->gseg = h->cta_g0 = nullptr;
@@ -1347,10 +1352,11 @@ int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64_t* off
   PM_CUDA(cudaMalloc(&h->betas, sizeof(double) * (size_t(G) * K + 2 * K)));
   h->mu_dev = h->betas + size_t(G) * K;
   h->sigma_dev = h->mu_dev + K;
-  PM_CUDA(cudaMalloc(&h->out_f, sizeof(double) * G));
-  PM_CUDA(cudaMalloc(&h->out_g, sizeof(double) * size_t(G) * K));
+  // f then g, contiguous: pm_hb_eval reads both back with one D2H copy
+  PM_CUDA(cudaMalloc(&h->out_f, sizeof(double) * (size_t(G) + size_t(G) * K)));
+  h->out_g = h->out_f + G;
   PM_CUDA(cudaHostAlloc(&h->pin_in, sizeof(double) * (size_t(G) * K + 2 * K), cudaHostAllocPortable));
-  // mapped: pm_hb_eval's fold writes (f, g) straight into host memory (no D2H copies)
+  // mapped, so the fold can also write (f, g) straight into host memory (tune hb_mapped_out=1)
   PM_CUDA(cudaHostAlloc(&h->pin_out, sizeof(double) * (size_t(G) + size_t(G) * K),
                         cudaHostAllocPortable | cudaHostAllocMapped));
   PM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->pin_out_dev), h->pin_out, 0));
@@ -1467,10 +1473,18 @@ int pm_hb_eval(pm_hb_t h, const double* betas, const double* mu, const double* s
   if (rc) return rc;
   const int G = h->G, K = h->K;
   const bool grad = want_grad != 0 && g_out != nullptr;
-  a.out_f = h->pin_out_dev;  // the fold writes the results into mapped host memory
-  a.out_g = h->pin_out_dev + G;
+  // default: the fold writes (f, g) to device memory and one DMA brings them back (168 KB at
+  // config 3); hb_mapped_out=1: the fold's stores go straight into mapped host memory
+  const bool mapped = tune("hb_mapped_out", 0) == 1;
+  if (mapped) {
+    a.out_f = h->pin_out_dev;
+    a.out_g = h->pin_out_dev + G;
+  }
   cudaError_t e = launch_hb_any(h, a, grad);
   if (e != cudaSuccess) return cuda_fail(e, "hb kernel launch");
+  if (!mapped)
+    PM_CUDA(cudaMemcpyAsync(h->pin_out, h->out_f, sizeof(double) * (size_t(G) + (grad ? size_t(G) * K : 0)),
+                            cudaMemcpyDeviceToHost, h->stream));
   PM_CUDA(cudaStreamSynchronize(h->stream));
   std::memcpy(f_out, h->pin_out, sizeof(double) * G);
   if (grad) std::memcpy(g_out, h->pin_out + G, sizeof(double) * size_t(G) * K);

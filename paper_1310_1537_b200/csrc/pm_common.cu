@@ -84,6 +84,7 @@ static const char* const kTuneNames[] = {
     "hb_rows_stages",    // stages (default: auto)
     "hb_contig",         // contiguous per-warp tile ranges: 1 (default)
     "hb_fused",          // fold fused into the rows launch: 0 (default)
+    "hb_mapped_out",     // pm_hb_eval results: 0 device + one D2H copy (default), 1 mapped host stores
     "pdl",               // programmatic dependent launch: 1 (default)
     "chain_unroll",      // chain kernel rows per ILP batch (default 2)
     "chain_blocks_per_sm",  // chain kernel CTAs per SM (default 2)

@@ -151,8 +151,13 @@ class LatticeDevice:
         s = np.ascontiguousarray(s, dtype=np.int8)
         _lib.call("pm_lat_set_spins", self._h, _lib.i8ptr(s))
 
-    def get_spins(self) -> np.ndarray:
-        out = np.empty((self.height, self.width), dtype=np.int8)
+    def get_spins(self, out: np.ndarray | None = None) -> np.ndarray:
+        """The spins as an int8 grid, written straight into `out` when given (C-contiguous
+        int8 of the lattice shape: a page-locked `out` makes the read one DMA)."""
+        if out is None:
+            out = np.empty((self.height, self.width), dtype=np.int8)
+        elif out.dtype != np.int8 or not out.flags.c_contiguous or out.shape != (self.height, self.width):
+            raise ValueError("out must be a C-contiguous int8 array of the lattice shape")
         _lib.call("pm_lat_get_spins", self._h, _lib.i8ptr(out))
         return out
 
@@ -252,7 +257,11 @@ class ColorPartition:
         self.device.set_spins(lat.s)
 
     def unpack_into(self, lat) -> None:
-        lat.s[...] = self.device.get_spins()
+        s = lat.s
+        if s.dtype == np.int8 and s.flags.c_contiguous and s.flags.writeable and s.shape == (lat.height, lat.width):
+            self.device.get_spins(out=s)  # straight into the lattice's own buffer
+        else:
+            s[...] = self.device.get_spins()
 
     @property
     def packed_s(self) -> list[np.ndarray]:
@@ -266,6 +275,18 @@ class ColorPartition:
         the device state; 0 outside a free boundary, wrap-around when periodic."""
         s = self.device.get_spins()
         return _neighbour_sum_grid(s, self._periodic).ravel()[self.colors[c]]
+
+
+def pin_lattice(lat) -> None:
+    """Move lat.s into page-locked host memory (same values) so that pack_from /
+    unpack_into -- the spin I/O of every sweep call -- are single DMA transfers instead of
+    staged pageable copies.  Optional; the results do not depend on it."""
+    import torch  # plumbing only: a page-locked host allocation
+    owner = torch.empty(lat.s.shape, dtype=torch.int8, pin_memory=True)
+    buf = owner.numpy()
+    buf[...] = lat.s
+    lat._pinned_owner = owner
+    lat.s = buf
 
 
 def color_lattice(lat, device: int = 0) -> ColorPartition:

@@ -262,7 +262,7 @@ def test_row_per_lane_kernel_against_oracle_and_stream_kernel(gpu, n, k, tune):
 
 
 @pytest.mark.parametrize("pairs", ["2", "1", "0"])
-def test_fp32_storage_all_layouts(gpu, monkeypatch, pairs):
+def test_fp32_storage_all_layouts(gpu, tune, pairs):
     """fp32-X over K values that select every stream-kernel consumer layout (column per lane,
     column pairs with XOR-permuted rows, 7 or 15 consumer warps, the wide kernel), f only and
     f + g, against the oracle on the fp32-rounded X (1e-10)."""
@@ -312,7 +312,7 @@ def test_fp32_widening_edge_values(gpu):
 
 
 @pytest.mark.parametrize("pairs", ["1", "0"])
-def test_fp64_stream_layouts(gpu, monkeypatch, pairs):
+def test_fp64_stream_layouts(gpu, tune, pairs):
     """fp64 X through the stream kernel's two consumer layouts (column pairs with 16-byte
     loads and XOR-permuted rows, or column per lane), f only and f + g, odd and even N,
     against the oracle (1e-10)."""
