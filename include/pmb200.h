@@ -151,6 +151,11 @@ PM_API int pm_fold_rows(const double* in_dev, int32_t world, int32_t width, doub
  * events on the handle's stream; *total_ms = elapsed device time. */
 PM_API int pm_glm_time_launches(pm_glm_t h, const double* betas, int32_t n, int with_prior,
                                 int want_grad, float* total_ms);
+/* Cold-cache variant: before each of the n launches the L2 is scrubbed on the same stream
+ * (512 MiB write + 256 MiB clean read); *total_ms = sum of the n launches' own event
+ * intervals (device time with inputs in HBM, not host launch latency). */
+PM_API int pm_glm_time_cold(pm_glm_t h, const double* betas, int32_t n, int with_prior,
+                            int want_grad, float* total_ms);
 
 /* The handle's CUDA stream (cudaStream_t), for event timing by the caller. */
 PM_API int pm_glm_stream(pm_glm_t h, void** stream);

@@ -64,6 +64,7 @@ SIGNATURES = {
     "pm_glm_eval_xchg": (c_int, [c_void_p, _dp, c_int, c_void_p, c_void_p, c_void_p]),
     "pm_glm_eval_xchg_phase": (c_int, [c_void_p, _dp, c_int, c_void_p, c_int, c_void_p, c_void_p]),
     "pm_glm_time_launches": (c_int, [c_void_p, _dp, c_int32, c_int, c_int, POINTER(ctypes.c_float)]),
+    "pm_glm_time_cold": (c_int, [c_void_p, _dp, c_int32, c_int, c_int, POINTER(ctypes.c_float)]),
     "pm_glm_stream": (c_int, [c_void_p, POINTER(c_void_p)]),
     "pm_glm_geometry": (c_int, [c_void_p, _ip, _ip, _ip, POINTER(c_size_t), _ip]),
     "pm_ws_create": (c_int, [c_void_p, _dp, POINTER(c_void_p)]),

@@ -165,9 +165,7 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
     grid.sync();
     // every CTA folds all CTA partials in the same fixed order: warp w folds delta m = w, w+8..
     for (int m = warp; m < M; m += kChainThreads / 32) {
-      double p = 0.0;
-      for (int b = lane; b < G; b += 32) p += __ldcg(a.partials + (size_t(parity) * G + b) * kChainMaxM + m);
-      p = warp_sum(p);
+      const double p = warp_sum(fold_lane(a.partials + size_t(parity) * G * kChainMaxM + m, kChainMaxM, G, lane));
       if (lane == 0) tot_s[m] = -p;
     }
     __syncthreads();

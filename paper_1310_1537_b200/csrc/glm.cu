@@ -68,6 +68,7 @@ struct pm_glm_s {
   // prior
   double* prior_mu = nullptr;
   double* prior_sigma = nullptr;
+  double* prior_terms = nullptr;  // [K+1] scratch of the kernels' prior_precompute
   bool has_prior = false;
   // scratch
   double* partials = nullptr;
@@ -98,6 +99,7 @@ void free_glm_data(pm_glm_s* h) {
   if (h->beta_pinned) cudaFreeHost(h->beta_pinned);
   if (h->prior_mu) cudaFree(h->prior_mu);
   if (h->prior_sigma) cudaFree(h->prior_sigma);
+  if (h->prior_terms) cudaFree(h->prior_terms);
   if (h->xt_cache) cudaFree(h->xt_cache);
   h->xt_cache = nullptr;
   h->X = nullptr;
@@ -107,7 +109,7 @@ void free_glm_data(pm_glm_s* h) {
   h->out_host = nullptr;
   h->out_dev = nullptr;
   h->beta_pinned = nullptr;
-  h->prior_mu = h->prior_sigma = nullptr;
+  h->prior_mu = h->prior_sigma = h->prior_terms = nullptr;
   h->has_prior = false;
   h->K = 0;
   h->n_rows = h->n_pad = h->n_tiles = 0;
@@ -382,6 +384,7 @@ GlmArgs make_args(pm_glm_s* h, bool with_prior, double* out) {
   a.evict_first = 1;
   a.prior_mu = h->prior_mu;
   a.prior_sigma = h->prior_sigma;
+  a.prior_terms = h->prior_terms;
   a.partials = h->partials;
   a.counter = h->counter;
   a.out = out;
@@ -392,6 +395,14 @@ GlmArgs make_args(pm_glm_s* h, bool with_prior, double* out) {
   a.xepoch = 0;
   for (int p = 0; p < kMaxXchgRanks; ++p) a.xpeer[p] = nullptr;
   a.xstatus = nullptr;
+#ifdef PM_AB_PHASES
+  static unsigned long long* stamps = nullptr;
+  if (!stamps) {
+    cudaMalloc(&stamps, sizeof(unsigned long long) * 8 * 4096);
+    cudaMemset(stamps, 0, sizeof(unsigned long long) * 8 * 4096);
+  }
+  a.stamps = stamps;
+#endif
   return a;
 }
 
@@ -581,6 +592,7 @@ int pm_glm_set_prior(pm_glm_t h, const double* mu, const double* sigma) {
   cudaStreamSynchronize(h->stream);
   if (!h->prior_mu) PM_CUDA(cudaMalloc(&h->prior_mu, sizeof(double) * h->K));
   if (!h->prior_sigma) PM_CUDA(cudaMalloc(&h->prior_sigma, sizeof(double) * h->K));
+  if (!h->prior_terms) PM_CUDA(cudaMalloc(&h->prior_terms, sizeof(double) * (h->K + 1)));
   PM_CUDA(cudaMemcpy(h->prior_mu, mu, sizeof(double) * h->K, cudaMemcpyHostToDevice));
   PM_CUDA(cudaMemcpy(h->prior_sigma, sigma, sizeof(double) * h->K, cudaMemcpyHostToDevice));
   h->has_prior = true;
@@ -866,6 +878,69 @@ int pm_glm_time_launches(pm_glm_t h, const double* betas, int32_t n, int with_pr
   PM_CUDA(cudaEventElapsedTime(total_ms, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  h->last_want_grad = want_grad;
+#ifdef PM_AB_PHASES
+  {  // phases of the LAST launch, ns relative to the first CTA's entry
+    GlmArgs a = make_args(h, false, nullptr);
+    const int G = h->grid;
+    std::vector<unsigned long long> st(size_t(G) * 8);
+    cudaMemcpy(st.data(), a.stamps, sizeof(unsigned long long) * st.size(), cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull, e_max = 0, p_max = 0, s_min = ~0ull, s_max = 0, k_max = 0, f_last = 0;
+    for (int b = 0; b < G; ++b) {
+      const unsigned long long* s = &st[size_t(b) * 8];
+      t0 = std::min(t0, s[0]);
+      e_max = std::max(e_max, s[0]);
+      p_max = std::max(p_max, s[1]);
+      s_min = std::min(s_min, s[2]);
+      s_max = std::max(s_max, s[2]);
+      k_max = std::max(k_max, s[3]);
+      f_last = std::max(f_last, s[4]);
+    }
+    std::fprintf(stderr,
+                 "[phases] grid %d: entry spread %.2f us, prologue done %.2f, stream done first %.2f last %.2f, "
+                 "tickets done %.2f, finish done %.2f (event %.2f us per launch)\n",
+                 G, (e_max - t0) * 1e-3, (p_max - t0) * 1e-3, (s_min - t0) * 1e-3, (s_max - t0) * 1e-3,
+                 (k_max - t0) * 1e-3, (f_last - t0) * 1e-3, *total_ms * 1e3 / n);
+    cudaMemset(a.stamps, 0, sizeof(unsigned long long) * st.size());
+  }
+#endif
+  return PM_OK;
+}
+
+int pm_glm_time_cold(pm_glm_t h, const double* betas, int32_t n, int with_prior, int want_grad,
+                     float* total_ms) {
+  if (!h || !betas || !total_ms) return fail(PM_EINVAL, "null argument");
+  if (n < 1) return fail(PM_EINVAL, "n must be >= 1");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->K == 0) return fail(PM_ESTATE, "no data uploaded");
+  if (with_prior && !h->has_prior) return fail(PM_ESTATE, "with_prior set but no prior configured");
+  for (int i = 0; i < n; ++i) {
+    int rc = check_beta(h, betas + size_t(i) * h->K);
+    if (rc) return rc;
+  }
+  DeviceGuard g(h->device);
+  std::vector<cudaEvent_t> ev(2 * size_t(n), nullptr);
+  for (auto& e : ev) PM_CUDA(cudaEventCreate(&e));
+  PM_CUDA(cudaStreamSynchronize(h->stream));
+  // per launch: scrub L2 on the SAME stream, then events around the launch alone -- the GPU
+  // goes straight from the scrub to the evaluation, so the interval is device time with cold
+  // inputs, not the host's launch latency
+  for (int i = 0; i < n; ++i) {
+    PM_CUDA(l2_scrub(h->device, h->stream));
+    PM_CUDA(cudaEventRecord(ev[2 * i], h->stream));
+    int rc = enqueue_eval(h, betas + size_t(i) * h->K, with_prior != 0, want_grad != 0, h->out_dev, h->stream);
+    if (rc) return rc;
+    PM_CUDA(cudaEventRecord(ev[2 * i + 1], h->stream));
+  }
+  PM_CUDA(cudaStreamSynchronize(h->stream));
+  float tot = 0.f;
+  for (int i = 0; i < n; ++i) {
+    float ms = 0.f;
+    PM_CUDA(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]));
+    tot += ms;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  *total_ms = tot;
   h->last_want_grad = want_grad;
   return PM_OK;
 }

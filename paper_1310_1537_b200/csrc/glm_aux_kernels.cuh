@@ -64,15 +64,11 @@ __global__ void __launch_bounds__(256) diff_eval_kernel(DiffArgs a, DeltaPack dp
   }
   __syncthreads();
   if (!flag) return;
-  if (threadIdx.x < M) {
-    double s0 = 0.0, s1 = 0.0;
-    int b = 0;
-    for (; b + 2 <= (int)gridDim.x; b += 2) {
-      s0 += __ldcg(a.partials + size_t(b) * kMaxDeltas + threadIdx.x);
-      s1 += __ldcg(a.partials + size_t(b + 1) * kMaxDeltas + threadIdx.x);
-    }
-    if (b < (int)gridDim.x) s0 += __ldcg(a.partials + size_t(b) * kMaxDeltas + threadIdx.x);
-    a.out[threadIdx.x] = -(s0 + s1);
+  // warp w folds delta m = w, w + 8, ...: lane-strided CTA partials (loads in flight
+  // together), then the fixed butterfly -- the order does not depend on M
+  for (int m = warp; m < M; m += blockDim.x >> 5) {
+    const double s = warp_sum(fold_lane(a.partials + m, kMaxDeltas, gridDim.x, lane));
+    if (lane == 0) a.out[m] = -s;
   }
   if (threadIdx.x == 0) *a.counter = 0u;
 }
@@ -612,6 +608,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) glm_rows_kernel(GlmArgs a, 
   }
   for (int k = threadIdx.x; k < K; k += blockDim.x) sm.sbeta[k] = beta.v[k];
   __syncthreads();
+  if (blockIdx.x == 0 && a.with_prior && warp == NCW) prior_precompute(a, sm.sbeta, lane);
   const int64_t C = gridDim.x, c = blockIdx.x;
   const int64_t t0 = c * a.n_tiles / C, t1 = (c + 1) * a.n_tiles / C;
   const int64_t n_units = (t1 - t0 + TPS - 1) / TPS;

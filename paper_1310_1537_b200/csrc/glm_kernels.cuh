@@ -592,6 +592,7 @@ struct GlmArgs {
   int evict_first;
   const double* prior_mu;     // device [K]
   const double* prior_sigma;  // device [K]
+  double* prior_terms;        // device [K+1] scratch: prior_precompute -> cta_reduce_finalize
   double* partials;           // [grid][K+1]
   unsigned int* counter;      // zero between launches
   double* out;                // [K+1]  (f, g)
@@ -604,7 +605,23 @@ struct GlmArgs {
   unsigned long long xepoch;  // >= 1, +1 per evaluation, identical on every rank
   double* xpeer[kMaxXchgRanks];  // mailbox base of every rank, mapped into this process
   unsigned* xstatus;          // local: set to 1 on a wait timeout
+#ifdef PM_AB_PHASES  // A/B timing experiment only: %globaltimer stamps per CTA, 8 slots each
+  unsigned long long* stamps;
+#endif
 };
+
+__device__ __forceinline__ void ab_stamp(const GlmArgs& a, int slot) {
+#ifdef PM_AB_PHASES
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.stamps[blockIdx.x * 8 + slot] = t;
+  }
+#else
+  (void)a;
+  (void)slot;
+#endif
+}
 
 // Peer exchange, second half (the finishing CTA only): publish this rank's deposits, wait for
 // every rank's, fold them in ascending rank order (dist.ordered_sum / pm_fold_rows: identical
@@ -662,6 +679,25 @@ __device__ inline void xchg_finish(const GlmArgs& a, int ncols, int* flag) {
   }
 }
 
+// Prior terms of the log-posterior (sampler.py:55-58, constants dropped), computed by ONE warp
+// of CTA 0 at the start of the launch, off the critical path (they depend only on beta, mu,
+// sigma): terms[0] = sum_k -0.5 ((beta_k - mu_k) / sigma_k)^2 (lane-strided partials, then
+// the fixed butterfly), terms[1+k] = (beta_k - mu_k) / sigma_k^2.  Ordered before CTA 0's
+// release ticket in cta_reduce_finalize, so the finishing CTA (acquire) reads them from L2;
+// in the tail they cost two loads instead of K dependent divisions (~2 us of a c0 launch).
+__device__ inline void prior_precompute(const GlmArgs& a, const double* sbeta, int lane) {
+  double f = 0.0;
+  for (int k = lane; k < a.K; k += 32) {
+    const double mu = a.prior_mu[k], sg = a.prior_sigma[k];
+    const double d = sbeta[k] - mu;
+    const double z = d / sg;
+    f += -0.5 * z * z;
+    a.prior_terms[1 + k] = d / (sg * sg);
+  }
+  f = warp_sum(f);
+  if (lane == 0) a.prior_terms[0] = f;
+}
+
 // Deterministic cross-CTA finish: CTA partial -> partials[blockIdx]; the last CTA to
 // arrive sums all partials in ascending CTA order (the reference's ascending-worker merge,
 // glm.py:243-250), adds the prior (sampler.py:55-58) and writes (f, g).
@@ -687,38 +723,48 @@ __device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& s
   // CTA, acquires every other CTA's; replaces two per-thread __threadfence() (MEMBAR +
   // L1 invalidation), measured ~4 us of a c0 launch.
   __syncthreads();
+  ab_stamp(a, 2);
   if (tid == 0) {
     unsigned t;
     asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(a.counter) : "memory");
     *sm.flag = (t == gridDim.x - 1) ? 1 : 0;
   }
   __syncthreads();
+  ab_stamp(a, 3);
   if (*sm.flag == 0) return;
   const int G = gridDim.x;
   const int lane = tid & 31, nwarps = blockDim.x >> 5;
-  if (a.with_prior) {  // -0.5 z_k^2 (sampler.py:55-58) computed in parallel into the free wg scratch
-    for (int k = tid; k < K; k += blockDim.x) {
-      const double z = (sm.sbeta[k] - a.prior_mu[k]) / a.prior_sigma[k];
-      sm.wg[k] = -0.5 * z * z;
-    }
-    __syncthreads();
-  }
   // column totals in a fixed order: one warp per column, lane l folds CTAs l, l+32, ...,
-  // then the fixed butterfly.  A warp takes CU of its columns at once so their L2 loads are
-  // all in flight together (one round trip instead of CU; this finish is on the critical
+  // then the fixed butterfly.  A warp takes CU of its columns at once, and the CTA loop is
+  // unrolled 8 deep, so all of a lane's L2 loads (<= 8 x CU for <= 256 CTAs) are in flight
+  // together: one round trip instead of one per 32 CTAs (this finish is on the critical
   // path of every launch).  The per-column summation order is unchanged.
   constexpr int CU = 4;
   const int ncols = grad ? K + 1 : 1;
   for (int c0 = tid >> 5; c0 < ncols; c0 += nwarps * CU) {
-    double part[CU];
+    double part[CU], pr[CU];
 #pragma unroll
-    for (int u = 0; u < CU; ++u) part[u] = 0.0;
-    for (int b = lane; b < G; b += 32) {
+    for (int u = 0; u < CU; ++u) {
+      part[u] = 0.0;
+      const int c = c0 + u * nwarps;
+      pr[u] = (a.with_prior && c < ncols) ? __ldcg(a.prior_terms + c) : 0.0;  // in flight with the partials
+    }
+    for (int b0 = 0; b0 < G; b0 += 256) {
+      double v[8][CU];
 #pragma unroll
-      for (int u = 0; u < CU; ++u) {
-        const int c = c0 + u * nwarps;
-        if (c < ncols) part[u] += __ldcg(a.partials + size_t(b) * (K + 1) + c);
+      for (int i = 0; i < 8; ++i) {
+        const int b = b0 + 32 * i + lane;
+#pragma unroll
+        for (int u = 0; u < CU; ++u) {
+          const int c = c0 + u * nwarps;
+          v[i][u] = (b < G && c < ncols) ? __ldcg(a.partials + size_t(b) * (K + 1) + c) : 0.0;
+        }
       }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int u = 0; u < CU; ++u)
+          if (b0 + 32 * i + lane < G) part[u] += v[i][u];
     }
 #pragma unroll
     for (int u = 0; u < CU; ++u) {
@@ -726,20 +772,9 @@ __device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& s
       if (c >= ncols) break;
       const double tot = warp_sum(part[u]);
       if (lane != 0) continue;
-      double v;
-      if (c == 0) {
-        v = tot;  // partials already hold -sum(nll) = L
-        if (a.with_prior) {
-          for (int k = 0; k < K; ++k) v += sm.wg[k];  // prior terms, ascending k
-        }
-      } else {
-        const int k = c - 1;
-        v = tot;
-        if (a.with_prior) {
-          const double sg = a.prior_sigma[k];
-          v -= (sm.sbeta[k] - a.prior_mu[k]) / (sg * sg);
-        }
-      }
+      // partials hold -sum(nll) = L and the gradient; + the prior terms of prior_precompute
+      double v = tot;
+      if (a.with_prior) v = c == 0 ? tot + pr[u] : tot - pr[u];
       if (a.xw == 0) {
         a.out[c] = v;
       } else if (a.xphase & 1) {  // deposit into slot [parity][xrank] of every rank's mailbox (P2P stores)
@@ -749,6 +784,10 @@ __device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& s
     }
   }
   if (tid == 0) *a.counter = 0u;  // re-arm for the next launch (kernel boundary orders it)
+#ifdef PM_AB_PHASES
+  __syncthreads();
+  ab_stamp(a, 4);
+#endif
   if (a.xw > 0) xchg_finish(a, ncols, sm.flag);
 }
 
@@ -761,6 +800,7 @@ template <typename XT, int KC, bool GRAD, int NCW, int R = SubRows<KC, GRAD>::va
 __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     glm_stream_kernel(GlmArgs a, BetaPack<KC> beta) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  ab_stamp(a, 0);
 #ifdef PM_AB_EMPTY  // A/B timing experiment only: launch + exit of the same grid / smem footprint
   if (threadIdx.x == 0 && blockIdx.x == 0) a.out[0] = 0.0;
   return;
@@ -779,6 +819,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   }
   for (int k = threadIdx.x; k < K; k += blockDim.x) sm.sbeta[k] = beta.v[k];
   __syncthreads();
+  if (blockIdx.x == 0 && a.with_prior && warp == NCW) prior_precompute(a, sm.sbeta, lane);
+  ab_stamp(a, 1);
 
   double breg[KC], g[KC];
 #pragma unroll
@@ -820,6 +862,7 @@ __global__ void __launch_bounds__(256) glm_wide_kernel(GlmArgs a) {
   double* ga = sm.wg + size_t(warp) * K;
   for (int k = lane; k < K; k += 32) ga[k] = 0.0;
   __syncthreads();
+  if (blockIdx.x == 0 && a.with_prior && warp == nw - 1) prior_precompute(a, sm.sbeta, lane);
   const XT* X = static_cast<const XT*>(a.X);
   double nll = 0.0;
   const int64_t total_warps = int64_t(gridDim.x) * nw;

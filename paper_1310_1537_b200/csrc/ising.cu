@@ -183,6 +183,7 @@ struct PackedArgs {
   int64_t n0;                 // global sites of colour 0
   uint64_t sweep;
   uint64_t seed;
+  Philox32Keys rk;            // key schedule of seed (host-computed)
   unsigned long long thr[9];  // Ising: ceil(P(+1 | nsum) * 2^32), nsum = -4..4
   // strip decomposition: own rows are global rows row0 .. row0+rows-1, stored at array rows
   // halo .. halo+rows-1; with halo = 1 the arrays carry one halo row above and below
@@ -265,14 +266,21 @@ struct GibbsTables {
 };
 
 // Thread = NG consecutive 16-site groups of one packed row (setup amortised over 16*NG sites).
+// sm != null (STAGE): the other colour's rows r-1, r, r+1 come from the CTA's shared-memory
+// stage (sm = this thread's first byte of row r there, rows `pitch` bytes apart, >= 16
+// staged bytes on either side for the edge neighbours) instead of three L2 loads each.
 template <int MODEL, bool T32, int NG, bool XCHG>
 __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const GibbsTables<MODEL, T32>& tb, int r,
-                                                 int q0);
+                                                 int q0, const int8_t* sm = nullptr, int pitch = 0);
 
 __device__ inline void lat_xchg_publish(const PackedArgs& a);
 
-// XCHG: the strip peer-memory halo exchange (PackedArgs xmb ...) is compiled in
-template <int MODEL, bool T32, int NG, bool XCHG>
+// XCHG: the strip peer-memory halo exchange (PackedArgs xmb ...) is compiled in.
+// STAGE (A/B, tune gibbs_smem=1; periodic whole lattices only): each CTA covers blockDim.y
+// rows and stages the other colour's rows above / below / inside (+ 16 edge bytes either
+// side) in shared memory once, so every row is read from L2 (blockDim.y + 2) / blockDim.y
+// times instead of 3 -- the north-star's neighbour-sum staging.
+template <int MODEL, bool T32, int NG, bool XCHG, bool STAGE = false>
 __global__ void __launch_bounds__(256, NG == 1 ? 6 : MODEL == PM_MODEL_ISING ? PM_GIBBS_MINB_ISING : PM_GIBBS_MINB_POTTS)
     gibbs_packed_kernel(PackedArgs a, const unsigned long long* __restrict__ pthr, const uint32_t* __restrict__ pcomp) {
   __shared__ GibbsTables<MODEL, T32> tb;
@@ -302,7 +310,30 @@ __global__ void __launch_bounds__(256, NG == 1 ? 6 : MODEL == PM_MODEL_ISING ? P
   // 2-D grid of 2-D blocks: x = (16*NG)-site column groups of a row, y = rows
   const int per_row = a.W2 / (16 * NG);
   const int cgrp = blockIdx.x * blockDim.x + threadIdx.x;
-  if (cgrp < per_row) {
+  if constexpr (STAGE) {
+    extern __shared__ __align__(16) int8_t stage[];
+    const int span = blockDim.x * 16 * NG;  // packed bytes of a row covered by the CTA
+    const int pitch = span + 32;
+    const int nchunk = pitch / 16, nrow = blockDim.y + 2;
+    const int cbase = blockIdx.x * span;
+    const int nthr = blockDim.x * blockDim.y;
+    for (int rb = blockIdx.y * blockDim.y; rb < a.rows; rb += gridDim.y * blockDim.y) {
+      for (int t = tid; t < nrow * nchunk; t += nthr) {
+        const int rr = t / nchunk, cc = t - rr * nchunk;
+        int gr = rb - 1 + rr;
+        gr = gr < 0 ? gr + a.rows : (gr >= a.rows ? gr - a.rows : gr);
+        int gc = cbase - 16 + cc * 16;
+        gc = gc < 0 ? gc + a.W2 : (gc >= a.W2 ? gc - a.W2 : gc);
+        *reinterpret_cast<uint4*>(stage + rr * pitch + cc * 16) = ld16(a.other + int64_t(gr) * a.W2 + gc);
+      }
+      __syncthreads();
+      const int r = rb + threadIdx.y;
+      if (r < a.rows && cgrp < per_row)
+        gibbs_packed_row<MODEL, T32, NG, XCHG>(a, tb, r, cgrp * 16 * NG,
+                                               stage + (threadIdx.y + 1) * pitch + 16 + threadIdx.x * 16 * NG, pitch);
+      __syncthreads();
+    }
+  } else if (cgrp < per_row) {
     for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < a.rows; r += gridDim.y * blockDim.y) {
       gibbs_packed_row<MODEL, T32, NG, XCHG>(a, tb, r, cgrp * 16 * NG);
     }
@@ -312,7 +343,7 @@ __global__ void __launch_bounds__(256, NG == 1 ? 6 : MODEL == PM_MODEL_ISING ? P
 
 template <int MODEL, bool T32, int NG, bool XCHG>
 __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const GibbsTables<MODEL, T32>& tb, int r,
-                                                 int q0) {
+                                                 int q0, const int8_t* sm, int pitch) {
   constexpr int NW = 4 * NG;   // 32-bit words (4 sites each) handled by this thread
   const int li = r + a.halo;   // array row
   const int i = a.row0 + r;    // global row: colour parity and RNG site index
@@ -336,7 +367,14 @@ __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const Gibb
   uint32_t U[NW], D[NW], M[NW];
 #pragma unroll
   for (int g = 0; g < NG; ++g) {
-    const uint4 u4 = ld16(urow + q0 + 16 * g), d4 = ld16(drow + q0 + 16 * g), m4 = ld16(orow + q0 + 16 * g);
+    uint4 u4, d4, m4;
+    if (sm) {
+      u4 = *reinterpret_cast<const uint4*>(sm - pitch + 16 * g);
+      d4 = *reinterpret_cast<const uint4*>(sm + pitch + 16 * g);
+      m4 = *reinterpret_cast<const uint4*>(sm + 16 * g);
+    } else {
+      u4 = ld16(urow + q0 + 16 * g), d4 = ld16(drow + q0 + 16 * g), m4 = ld16(orow + q0 + 16 * g);
+    }
     U[4 * g] = u4.x, U[4 * g + 1] = u4.y, U[4 * g + 2] = u4.z, U[4 * g + 3] = u4.w;
     D[4 * g] = d4.x, D[4 * g + 1] = d4.y, D[4 * g + 2] = d4.z, D[4 * g + 3] = d4.w;
     M[4 * g] = m4.x, M[4 * g + 1] = m4.y, M[4 * g + 2] = m4.z, M[4 * g + 3] = m4.w;
@@ -344,7 +382,7 @@ __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const Gibb
   // o = 0: horizontal neighbours of packed site q are q-1 and q; o = 1: q and q+1
   const int o = (i + a.colour) & 1;
   const int qe = o ? ((q0 + 16 * NG == a.W2) ? 0 : q0 + 16 * NG) : ((q0 == 0) ? a.W2 - 1 : q0 - 1);
-  const uint32_t edge = uint32_t(uint8_t(__ldg(orow + qe)));
+  const uint32_t edge = sm ? uint32_t(uint8_t(o ? sm[16 * NG] : sm[-1])) : uint32_t(uint8_t(__ldg(orow + qe)));
   // Philox block of the first word.  The packed path only runs on lattices with fewer than
   // 2^34 - 256 sites (packed_blocks_fit), so every block index of the half-sweep fits 32 bits:
   // the counter's high word is 0 and g0 + m is a 32-bit add (no carry chain per word)
@@ -356,7 +394,7 @@ __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const Gibb
     // byte b of `sh` = the other horizontal neighbour of site 4m+b (funnel shift across words)
     const uint32_t sh = o == 0 ? __funnelshift_l(m == 0 ? (edge << 24) : M[m - 1], cur, 8)
                                : __funnelshift_r(cur, m == NW - 1 ? edge : M[m + 1], 8);
-    const U32x4 blk = site_philox_block(uint64_t(g0 + uint32_t(m)), a.sweep, a.seed);
+    const U32x4 blk = site_philox_block_rk(g0 + uint32_t(m), a.sweep, a.rk);
     uint32_t out = 0;
     if constexpr (MODEL == PM_MODEL_ISING) {
       // packed bytes are 1 - s (0x02 for -1, 0x00 for +1), so the plain 4-way byte sum is
@@ -862,6 +900,7 @@ static cudaError_t launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t se
   pa.n0 = int64_t(Hg) * (h->W / 2);
   pa.sweep = sweep;
   pa.seed = seed;
+  pa.rk = philox4x32_keys(seed);
   for (int k = 0; k < 9; ++k) pa.thr[k] = h->thr[k];
   pa.row0 = h->row0;
   pa.rows = h->H;
@@ -899,6 +938,19 @@ static cudaError_t launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t se
   const dim3 grid((per_row + bx - 1) / bx, std::min((h->H + by - 1) / by, 65535));
   const bool ising = h->model == PM_MODEL_ISING;
   cudaError_t e = cudaSuccess;  // a failed launch is also the thread's last error (callers check it)
+  // A/B (tune gibbs_smem=1): shared-memory staging of the other colour's rows, 8-row CTAs
+  if (tune("gibbs_smem", 0) == 1 && !pa.xmb && !h->strip && h->t32 &&
+      ((ising && ng == 2) || (!ising && ng == 4))) {
+    const int sbx = std::min(32, per_row), sby = 8;
+    const dim3 sblock(sbx, sby);
+    const dim3 sgrid((per_row + sbx - 1) / sbx, std::min((h->H + sby - 1) / sby, 65535));
+    const size_t smem = size_t(sby + 2) * (sbx * 16 * ng + 32);
+    e = ising ? launch_pdl(h->pdl, gibbs_packed_kernel<PM_MODEL_ISING, true, 2, false, true>, sgrid, sblock, smem, st,
+                           pa, (const unsigned long long*)h->pthr, (const uint32_t*)h->pthr32)
+              : launch_pdl(h->pdl, gibbs_packed_kernel<PM_MODEL_POTTS4, true, 4, false, true>, sgrid, sblock, smem,
+                           st, pa, (const unsigned long long*)h->pthr, (const uint32_t*)h->pthr32);
+    return e;
+  }
 #define PM_LAUNCH_PACKED(M, T, N)                                                                      \
   e = pa.xmb ? launch_pdl(h->pdl, gibbs_packed_kernel<M, T, N, true>, grid, block, 0, st, pa,          \
                           (const unsigned long long*)h->pthr, (const uint32_t*)h->pthr32)                 \

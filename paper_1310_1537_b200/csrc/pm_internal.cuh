@@ -48,6 +48,11 @@ int sm_count(int device);
 // C ABI (pm_tune_set), never read from the environment, so the shipped library's dispatch
 // is fixed unless a caller explicitly asks otherwise.  Returns `dflt` when `name` is unset.
 int tune(const char* name, int dflt);
+
+// Evict every line of the 126 MB L2 on `st` (timing of cold-cache launches): a 512 MiB
+// memset, then a 256 MiB read of a second, clean buffer, so the next launch neither hits in
+// L2 nor pays the write-back of dirty scrub lines.  Buffers are allocated once per device.
+cudaError_t l2_scrub(int device, cudaStream_t st);
 void retain_pool(int device);
 
 }  // namespace pm
@@ -197,6 +202,26 @@ __device__ __forceinline__ double shfl_d(double v, int src) {
 }
 __device__ __forceinline__ double shfl_xor_d(double v, int m) {
   return __shfl_xor_sync(0xffffffffu, v, m);
+}
+
+// This lane's share of a cross-CTA fold: sum of p[b * stride] for b = lane, lane + 32, ... < n,
+// ascending (fixed order), with the loads of up to 8 strides issued together before the adds
+// (a plain strided loop waits one L2 round trip per 32 partials: ~0.3 us each on the critical
+// path of every launch).  Callers finish with warp_sum.
+__device__ __forceinline__ double fold_lane(const double* p, size_t stride, int n, int lane) {
+  double acc = 0.0;
+  for (int b0 = 0; b0 < n; b0 += 256) {
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int b = b0 + 32 * i + lane;
+      v[i] = b < n ? __ldcg(p + size_t(b) * stride) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (b0 + 32 * i + lane < n) acc += v[i];
+  }
+  return acc;
 }
 
 // Fixed-order butterfly sum across a warp (every lane gets the same bits).

@@ -152,6 +152,16 @@ class GlmDevice:
                       int(want_grad), ctypes.byref(ms))
         return float(ms.value)
 
+    def time_cold(self, betas: np.ndarray, with_prior: bool, want_grad: bool) -> float:
+        """Device milliseconds summed over len(betas) launches, each after an L2 scrub on the
+        handle stream (pm_glm_time_cold: cold inputs, no host launch latency)."""
+        betas = np.ascontiguousarray(betas, dtype=np.float64)
+        ms = ctypes.c_float()
+        with self.lock:
+            _lib.call("pm_glm_time_cold", self._h, _lib.dptr(betas), int(betas.shape[0]), int(with_prior),
+                      int(want_grad), ctypes.byref(ms))
+        return float(ms.value)
+
     def eval(self, beta: np.ndarray, with_prior: bool, want_grad: bool):
         with self.lock:
             self.launch(beta, with_prior, want_grad)
@@ -489,7 +499,8 @@ def diff_loglike_multi(ws: GlmWorkspace, data: DesignMatrix, k: int, deltas,
     counters.add_flops(ws.n_rows * _DIFF_FLOPS * d.size)
     out = np.empty(d.size)
     _lib.call("pm_ws_diff_eval", ws._ws, int(k), _lib.dptr(d), int(d.size), _lib.dptr(out))
-    _account(ExecPlan(workers=plan.workers), calls=d.size)  # glm.py:520-522: one region per call
+    counters.add_region(d.size)  # glm.py:520-522: one PLF region and one merge per worker per call
+    counters.add_merges(plan.workers * d.size)
     counters.add_launches(1)
     return out
 

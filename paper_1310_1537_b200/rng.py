@@ -96,14 +96,11 @@ class DeviateBuffer:
         self._gen_pos = 0                     # stream index of the generator's next output
         self._block_start = -self.capacity    # stream index of data[0] (no block yet)
         self._seek_to: int | None = None      # pending generator reposition (skip)
-        self._virtual_refills = 0             # refills skip() already counted (see refill)
 
     def refill(self) -> None:
         """Fill data[0:capacity] with the next block of the base stream."""
         if self._seek_to is not None:
             self._apply_seek()
-        counted = self._virtual_refills > 0
-        self._virtual_refills = 0
         self._block_start = self._gen_pos
         if self.kind is BufferKind.UNIFORM01:
             self.data[:] = self._gen.random(self.capacity)
@@ -124,8 +121,7 @@ class DeviateBuffer:
                     self._carry = float(block[remaining])
                 self._gen_pos += 2 * n_pairs
         self.cursor = 0
-        if not counted:
-            self.refills += 1
+        self.refills += 1
 
     def next(self) -> float:
         if self.cursor == self.capacity:
@@ -150,7 +146,10 @@ class DeviateBuffer:
 
     @property
     def generated(self) -> int:
-        return self.refills * self.capacity
+        """Deviates generated as the reference counts them (rng.py:129-138): a host consumer
+        refills one block whenever it runs dry, so after `consumed` deviates it has filled
+        ceil(consumed / capacity) blocks -- also when the device consumed them (skip)."""
+        return max(self.refills, -(-self.consumed // self.capacity)) * self.capacity
 
     @property
     def waste_fraction(self) -> float:
@@ -181,10 +180,6 @@ class DeviateBuffer:
         if n <= self.capacity - self.cursor:
             self.cursor += n
         else:
-            # the blocks a host consumer would have refilled to get there (the reference's
-            # generated / waste_fraction accounting, rng.py:129-138)
-            self.refills += -(-(n - (self.capacity - self.cursor)) // self.capacity)
-            self._virtual_refills += 1  # the lazy refill below re-fills the last of them
             # the generator is repositioned lazily, at the next refill (device paths skip
             # thousands of streams per call and most are never read on the host)
             target = self.position + n

@@ -327,3 +327,21 @@ def test_coupling_change_between_sweeps_is_used(gpu, model):
             ref = go.potts_sweeps(ref, 1.3, periodic, 5, go.RNG_PHILOX4X32, 99, 0, 4)
         gibbs_sweeps(lat, part, rng, 5)
         np.testing.assert_array_equal(lat.s, ref, err_msg=bnd)
+
+
+@pytest.mark.parametrize("model", ["ising", "potts"])
+def test_smem_staged_half_sweep_bit_exact(gpu, tune, model):
+    """The shared-memory neighbour-staging A/B variant (tune gibbs_smem=1: 8-row CTAs stage
+    the other colour's rows once) gives the same spins as the oracle, incl. the periodic
+    wrap of the staged rows / edge bytes and a row count that is not a multiple of 8."""
+    tune(gibbs_smem=1)
+    for shape in ((68, 256), (64, 2048)):
+        s0 = ising_spins(*shape, seed=6) if model == "ising" else potts_states(*shape, seed=6)
+        lat = (IsingLattice(s0, np.zeros(shape), 0.8814, boundary="periodic") if model == "ising"
+               else PottsLattice(s0, 0.4407))
+        part = color_lattice(lat)
+        assert part.device.fast_path()
+        gibbs_sweeps(lat, part, SitePhilox(13), 6)
+        ref = (go.ising_sweeps(s0, None, 0.8814, True, 6, go.RNG_PHILOX4X32, 13, 0, 0) if model == "ising"
+               else go.potts_sweeps(s0, 0.4407, True, 6, go.RNG_PHILOX4X32, 13, 0, 0))
+        np.testing.assert_array_equal(lat.s, ref, err_msg=str(shape))

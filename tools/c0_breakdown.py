@@ -43,7 +43,8 @@ for n in (32, 4096, 100_000, 1_000_000):
         clean.max()
         torch.cuda.synchronize()
         cold.append(dev.time_launches(betas[i:i + 1], True, True))
+    cold_dev = dev.time_cold(betas[:20], True, True) / 20  # scrub on the launching stream
     res[str(n)] = {"warm_us": round(min(warm) * 1e3, 2), "cold_us_median": round(float(np.median(cold)) * 1e3, 2),
-                   "geometry": dev.geometry()}
+                   "cold_dev_us": round(cold_dev * 1e3, 2), "geometry": dev.geometry()}
     d.release_device()
 print(json.dumps(res))
