@@ -276,6 +276,7 @@ int choose_geometry(pm_glm_s* h) {
   const int budget = std::min(max_optin_smem(h->device), 232448) - 1024;
   h->kind = KIND_NONE;
   h->pairs = 0;
+  h->tps = 1;
   const int t_rows = tune("glm_rows", -1);
   // row-per-lane kernel: fp64, even K <= 30, and enough tiles to fill the machine (measured on
   // B200, tools/ab_rows_k.py: 1.3-2x faster than the column kernel at N = 1e7 for K <= 30; at
@@ -314,17 +315,30 @@ int choose_geometry(pm_glm_s* h) {
     }
   }
   if (kc <= kMaxKC) {
-    const size_t fixed = stream_smem_bytes(h->K, xs, 0, kNCW);
-    const size_t per_stage = stream_smem_bytes(h->K, xs, 1, 0) - stream_smem_bytes(h->K, xs, 0, 0);
+    // Tiles per stage U (one bulk copy each): a 32-row tile of a narrow design is small (8 KB
+    // at K = 32 fp64) and the single producer thread's ~200 ns per copy then bounds the
+    // pipeline, so stages of ~24 KB hold U consecutive tiles of a contiguous per-CTA tile
+    // range (tune stream_tps=1 restores single interleaved tiles; r02 c0 breakdown).
+    const size_t tile_b = size_t(kTileRows) * h->K * xs;
+    int U = int(std::min<size_t>(8, std::max<size_t>(1, (24 * 1024) / tile_b)));
+    const int t_u = tune("stream_tps", -1);
+    if (t_u >= 1) U = std::min(t_u, 16);
+    // no more tiles per stage than the busiest CTA's share per consumer warp
+    const int64_t per_cta = (h->n_tiles + h->sms - 1) / std::max(1, h->sms);
+    U = int(std::max<int64_t>(1, std::min<int64_t>(U, (per_cta + kNCW - 1) / kNCW)));
+    const int tr = U * kTileRows;
+    const size_t fixed = stream_smem_bytes(h->K, xs, 0, kNCW, tr);
+    const size_t per_stage = stream_smem_bytes(h->K, xs, 1, 0, tr) - stream_smem_bytes(h->K, xs, 0, 0, tr);
     int S = int((budget - (long)fixed) / (long)per_stage);
     S = std::min(S, kMaxStages);
     if (S >= 1) S -= S % std::min(S, kNCW);  // each stage owned by one consumer warp
     if (S >= 2) {
       h->kind = KIND_STREAM;
       h->stages = S;
+      h->tps = U;
       h->threads = kStreamThreads;
       h->ncw = kNCW;
-      h->smem = stream_smem_bytes(h->K, xs, S, kNCW);
+      h->smem = stream_smem_bytes(h->K, xs, S, kNCW, tr);
       h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, h->n_tiles));
     }
     // fp32-X, even K with an even register count: the pairs consumer layout
@@ -346,10 +360,12 @@ int choose_geometry(pm_glm_s* h) {
     if (h->kind == KIND_STREAM && h->xtype == PM_X_F32 && kc <= 4 && h->pairs == 0 &&
         tune("stream_ncw", 15) != 7) {
       const size_t fixed15 = stream_smem_bytes(h->K, xs, 0, kNCW15);
-      int S15 = int((budget - (long)fixed15) / (long)per_stage);
+      const size_t per_stage1 = stream_smem_bytes(h->K, xs, 1, 0) - stream_smem_bytes(h->K, xs, 0, 0);
+      int S15 = int((budget - (long)fixed15) / (long)per_stage1);
       S15 -= S15 % kNCW15;
       if (S15 >= kNCW15) {
         h->stages = std::min(S15, 2 * kNCW15);
+        h->tps = 1;  // single interleaved tiles
         h->ncw = kNCW15;
         h->threads = (kNCW15 + 1) * 32;
         h->smem = stream_smem_bytes(h->K, xs, h->stages, kNCW15);
@@ -380,6 +396,7 @@ GlmArgs make_args(pm_glm_s* h, bool with_prior, double* out) {
   a.n_tiles = h->n_tiles;
   a.K = h->K;
   a.stages = h->stages;
+  a.tps = h->kind == KIND_STREAM ? h->tps : 1;
   a.with_prior = with_prior ? 1 : 0;
   a.evict_first = 1;
   a.prior_mu = h->prior_mu;

@@ -133,7 +133,9 @@ __device__ __forceinline__ void consume_tile(const XT* xs, const double* ys, int
 #pragma unroll
       for (int j = 0; j < KC; ++j) {
         x[r][j] = (j < KC - 1 || lane + 32 * j < K) ? ld_x_stream(xb + r * K + 32 * j) : 0.0;
-        acc = fma(x[r][j], breg[j], acc);
+        // first term as a product: rn(x*b) == fma(x, b, 0) up to the sign of a zero (which
+        // cannot change f or g), and it saves zeroing the accumulator pair (CS2R) per row
+        acc = j == 0 ? __dmul_rn(x[r][0], breg[0]) : fma(x[r][j], breg[j], acc);
       }
       v[r] = acc;
     }
@@ -144,7 +146,7 @@ __device__ __forceinline__ void consume_tile(const XT* xs, const double* ys, int
       double dep = yv;
 #pragma unroll
       for (int r = 0; r < R; ++r) dep += v[r];
-      mbar_arrive_after(empty, dep, lane, const_cast<XT*>(xs));
+      if (empty) mbar_arrive_after(empty, dep, lane, const_cast<XT*>(xs));
     }
     const double t = transpose_reduce<R>(v, lane);
     double nll, w;
@@ -217,7 +219,7 @@ __device__ __forceinline__ void consume_tile_pairs(const XT* xs, const double* y
           if (c < KP - 1 || last_ok) u = pr[32 * c];
           x[r][2 * c] = u.x;
           x[r][2 * c + 1] = u.y;
-          acc = fma(x[r][2 * c], breg[2 * c], acc);
+          acc = c == 0 ? __dmul_rn(x[r][0], breg[0]) : fma(x[r][2 * c], breg[2 * c], acc);
           acc = fma(x[r][2 * c + 1], breg[2 * c + 1], acc);
         }
         v[r] = acc;
@@ -235,7 +237,7 @@ __device__ __forceinline__ void consume_tile_pairs(const XT* xs, const double* y
         x[r][2 * c] = ld_x_scaled(reinterpret_cast<const float*>(&u.x));
         x[r][2 * c + 1] = ld_x_scaled(reinterpret_cast<const float*>(&u.y));
 #endif
-        acc = fma(x[r][2 * c], breg[2 * c], acc);
+        acc = c == 0 ? __dmul_rn(x[r][0], breg[0]) : fma(x[r][2 * c], breg[2 * c], acc);
         acc = fma(x[r][2 * c + 1], breg[2 * c + 1], acc);
       }
       v[r] = acc;
@@ -246,7 +248,7 @@ __device__ __forceinline__ void consume_tile_pairs(const XT* xs, const double* y
       double dep = yv;
 #pragma unroll
       for (int r = 0; r < R; ++r) dep += v[r];
-      mbar_arrive_after(empty, dep, lane, const_cast<XT*>(xs));
+      if (empty) mbar_arrive_after(empty, dep, lane, const_cast<XT*>(xs));
     }
 #pragma unroll
     for (int st = R / 2; st >= 1; st >>= 1) {
@@ -350,7 +352,7 @@ __device__ __forceinline__ void consume_tile_f32full(const float* xs, const doub
     }
     vs[s] = v[0];  // block s, row 8s + b, summed over the 8 lanes sharing lane bits 3-4
   }
-  if (HOLD || !GRAD) mbar_arrive_after(empty, dep, lane, const_cast<float*>(xs));  // all words consumed
+  if ((HOLD || !GRAD) && empty) mbar_arrive_after(empty, dep, lane, const_cast<float*>(xs));  // all words consumed
   // across lane bits 4 then 3: lane l keeps block (l >> 3), i.e. tile row l
   {
     const bool up = (lane & 16) != 0;
@@ -413,7 +415,7 @@ __device__ __forceinline__ void consume_tile_f32full(const float* xs, const doub
       double dg = 0.0;
 #pragma unroll
       for (int j = 0; j < KC; ++j) dg += g[j];  // depends on every re-read word
-      mbar_arrive_after(empty, dg, lane, const_cast<float*>(xs));
+      if (empty) mbar_arrive_after(empty, dg, lane, const_cast<float*>(xs));
     }
   }
 }
@@ -473,24 +475,37 @@ __device__ inline StreamSmem carve_stream_smem(unsigned char* base, int K, int x
   return s;
 }
 
-// Producer/consumer ring over the tiles tile_begin, tile_begin+stride, ... < tile_end
-// (a "tile" here is one stage: TR consecutive rows).
-// Warp 0 lane 0 issues TMA bulk copies; warps 1..NCW consume tiles round-robin.
-// Rows with global (padded) index >= row_limit are masked (padding).
+// Producer/consumer ring over "units" of tiles (a tile = TR consecutive rows).
+//   U == 1: unit i is the single tile tile_begin + i*stride (< tile_end): tiles interleaved
+//           across CTAs (stride = grid) or a contiguous range (stride = 1).
+//   U  > 1: the caller's range [tile_begin, tile_end) is contiguous (stride must be 1) and
+//           unit i is the U consecutive tiles from tile_begin + i*U (the last unit may be
+//           shorter): ONE bulk copy of X and one of y per unit.  For small tiles (K <= ~64
+//           fp64) the single producer thread's ~200 ns per copy bounds the pipeline
+//           otherwise (profiles/r02_c0_breakdown.txt).
+// A stage holds one unit; warp 0 lane 0 issues the TMA bulk copies; warps 1..NCW consume
+// units round-robin.  Rows with global (padded) index >= row_limit are masked (padding).
+// SYNC: the CTA barrier that publishes the mbarrier initialisation is taken INSIDE, after
+// the producer has issued its first round of copies (they need no `empty` wait), so the
+// first HBM round trip overlaps the rest of the CTA's prologue.  With SYNC the PRODUCER warp
+// takes that barrier in here; every other warp of the CTA executes its own __syncthreads()
+// before calling (and every warp of the CTA must call, even with no tiles).
 template <typename XT, int KC, bool GRAD, int NCW, int R = SubRows<KC, GRAD>::value, int TR = kTileRows,
-          int PAIRS = 0>
+          int PAIRS = 0, bool SYNC = false>
 __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const double* __restrict__ y, int K,
                                              int64_t tile_begin, int64_t tile_end, int64_t stride,
                                              int64_t row_limit, int S, const StreamSmem& sm,
                                              const double (&breg)[KC], double (&g)[KC], double& nll_acc,
-                                             bool evict_first) {
+                                             bool evict_first, int U_arg = 1) {
+  // 16-warp (128-register) instantiations always run single tiles: keep U out of their registers
+  const int U = NCW > 8 ? 1 : U_arg;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t tile_elems = uint32_t(TR) * K;
   const uint32_t tile_bytes = tile_elems * sizeof(XT);
-  const size_t tile_pitch = align_up(tile_bytes, 128);
-  if (tile_begin >= tile_end) return;
-  const int64_t n_mine = (tile_end - tile_begin + stride - 1) / stride;
+  const size_t tile_pitch = align_up(size_t(U) * tile_bytes, 128);  // stage pitch
+  const int64_t n_tiles_mine = tile_end > tile_begin ? (tile_end - tile_begin + stride - 1) / stride : 0;
+  const int64_t n_mine = (n_tiles_mine + U - 1) / U;  // units
   // Every stage must belong to exactly one consumer warp, which uses it in order: an
   // mbarrier parity wait cannot tell phase n from phase n+2, so a stage shared by two
   // warps could let one of them run a phase ahead.  nact consumers, Se = multiple of nact.
@@ -498,27 +513,39 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
   const int Se = S - S % nact;
 
   if (warp == 0) {
-    if (lane == 0) {
-      const uint64_t pol = l2_policy_evict_first();
-      int s = 0;        // stage = i % Se
-      uint32_t n = 0;   // use count of the stage = i / Se
-      for (int64_t i = 0; i < n_mine; ++i) {
+    const uint64_t pol = l2_policy_evict_first();
+    int s = 0;        // stage = i % Se
+    uint32_t n = 0;   // use count of the stage = i / Se
+    int64_t tile = tile_begin;
+    int64_t left = n_tiles_mine;
+    auto issue = [&](int64_t i_end) {  // lane 0 only
+      for (int64_t i = int64_t(n) * Se + s; i < i_end; ++i) {
         if (n > 0) mbar_wait(&sm.empty[s], (n - 1) & 1);
-        const int64_t tile = tile_begin + i * stride;
-        mbar_arrive_expect_tx(&sm.full[s], tile_bytes + TR * sizeof(double));
+        const uint32_t cnt = uint32_t(left < U ? left : U);
+        mbar_arrive_expect_tx(&sm.full[s], cnt * (tile_bytes + TR * uint32_t(sizeof(double))));
         const XT* src = X + tile * int64_t(tile_elems);
         if (evict_first) {
-          bulk_g2s_hint(sm.xs + size_t(s) * tile_pitch, src, tile_bytes, &sm.full[s], pol);
+          bulk_g2s_hint(sm.xs + size_t(s) * tile_pitch, src, cnt * tile_bytes, &sm.full[s], pol);
         } else {
-          bulk_g2s(sm.xs + size_t(s) * tile_pitch, src, tile_bytes, &sm.full[s]);
+          bulk_g2s(sm.xs + size_t(s) * tile_pitch, src, cnt * tile_bytes, &sm.full[s]);
         }
-        bulk_g2s(sm.ys + size_t(s) * TR, y + tile * TR, TR * sizeof(double), &sm.full[s]);
+        bulk_g2s(sm.ys + size_t(s) * U * TR, y + tile * TR, cnt * TR * uint32_t(sizeof(double)), &sm.full[s]);
+        tile += U * stride;
+        left -= U;
         if (++s == Se) {
           s = 0;
           ++n;
         }
       }
+    };
+    if constexpr (SYNC) {
+      // first round (no `empty` waits: the stages are fresh), then the CTA barrier that lets
+      // the consumers see the initialised mbarriers -- taken by the whole warp, converged
+      if (lane == 0) issue(n_mine < Se ? n_mine : Se);
+      __syncwarp();
+      __syncthreads();
     }
+    if (lane == 0) issue(n_mine);
     return;
   }
   const int cw = warp - 1;
@@ -533,12 +560,16 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
   }
   for (int64_t i = cw; i < n_mine; i += nact) {
     mbar_wait(&sm.full[s], n & 1);
-    const int64_t tile = tile_begin + i * stride;
+    const int64_t tile0 = tile_begin + i * U * stride;
+    const int64_t left = n_tiles_mine - i * U;
+    const int cnt = int(left < U ? left : U);
+    const unsigned char* xstage = sm.xs + size_t(s) * tile_pitch;
+    const double* ystage = sm.ys + size_t(s) * U * TR;
 #ifdef PM_AB_NO_COMPUTE  // A/B timing experiment only: the TMA pipeline without the consumers' math
     {
-      const double dep = sm.ys[size_t(s) * TR + lane];
+      const double dep = ystage[lane];
       nll_acc += dep;
-      mbar_arrive_after(&sm.empty[s], dep, lane, sm.xs + size_t(s) * tile_pitch);
+      mbar_arrive_after(&sm.empty[s], dep, lane, const_cast<unsigned char*>(xstage));
       s += nact;
       if (s >= Se) {
         s = cw;
@@ -547,18 +578,21 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
       continue;
     }
 #endif
-    if constexpr (PAIRS == 2) {
-      consume_tile_f32full<KC, GRAD>(reinterpret_cast<const float*>(sm.xs + size_t(s) * tile_pitch),
-                                     sm.ys + size_t(s) * TR, K, lane, tile * TR, row_limit, breg, g, nll_acc,
-                                     &sm.empty[s], roff);
-    } else if constexpr (PAIRS == 1) {
-      consume_tile_pairs<XT, KC, GRAD, R, TR>(reinterpret_cast<const XT*>(sm.xs + size_t(s) * tile_pitch),
-                                          sm.ys + size_t(s) * TR, K, lane, tile * TR, row_limit, breg, g,
-                                          nll_acc, &sm.empty[s], roff);
-    } else {
-      consume_tile<XT, KC, GRAD, R, TR>(reinterpret_cast<const XT*>(sm.xs + size_t(s) * tile_pitch),
-                                        sm.ys + size_t(s) * TR, K, lane, tile * TR, row_limit, breg, g, nll_acc,
-                                        &sm.empty[s]);
+    for (int j = 0; j < cnt; ++j) {
+      const unsigned char* xt = xstage + size_t(j) * tile_bytes;
+      const double* yt = ystage + j * TR;
+      uint64_t* rel = (j == cnt - 1) ? &sm.empty[s] : nullptr;  // release with the unit's last tile
+      const int64_t row0 = (tile0 + j) * TR;
+      if constexpr (PAIRS == 2) {
+        consume_tile_f32full<KC, GRAD>(reinterpret_cast<const float*>(xt), yt, K, lane, row0, row_limit, breg, g,
+                                       nll_acc, rel, roff);
+      } else if constexpr (PAIRS == 1) {
+        consume_tile_pairs<XT, KC, GRAD, R, TR>(reinterpret_cast<const XT*>(xt), yt, K, lane, row0, row_limit,
+                                                breg, g, nll_acc, rel, roff);
+      } else {
+        consume_tile<XT, KC, GRAD, R, TR>(reinterpret_cast<const XT*>(xt), yt, K, lane, row0, row_limit, breg, g,
+                                          nll_acc, rel);
+      }
     }
     s += nact;
     if (s >= Se) {
@@ -588,6 +622,7 @@ struct GlmArgs {
   int64_t n_tiles;
   int K;
   int stages;
+  int tps;                    // stream kernel: tiles per stage (1 = interleaved single tiles)
   int with_prior;
   int evict_first;
   const double* prior_mu;     // device [K]
@@ -610,9 +645,9 @@ struct GlmArgs {
 #endif
 };
 
-__device__ __forceinline__ void ab_stamp(const GlmArgs& a, int slot) {
+__device__ __forceinline__ void ab_stamp(const GlmArgs& a, int slot, int tid = 0) {
 #ifdef PM_AB_PHASES
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == tid) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.stamps[blockIdx.x * 8 + slot] = t;
@@ -685,11 +720,12 @@ __device__ inline void xchg_finish(const GlmArgs& a, int ncols, int* flag) {
 // the fixed butterfly), terms[1+k] = (beta_k - mu_k) / sigma_k^2.  Ordered before CTA 0's
 // release ticket in cta_reduce_finalize, so the finishing CTA (acquire) reads them from L2;
 // in the tail they cost two loads instead of K dependent divisions (~2 us of a c0 launch).
-__device__ inline void prior_precompute(const GlmArgs& a, const double* sbeta, int lane) {
+template <class BetaAt>
+__device__ __forceinline__ void prior_precompute_from(const GlmArgs& a, BetaAt beta_at, int lane) {
   double f = 0.0;
   for (int k = lane; k < a.K; k += 32) {
     const double mu = a.prior_mu[k], sg = a.prior_sigma[k];
-    const double d = sbeta[k] - mu;
+    const double d = beta_at(k) - mu;
     const double z = d / sg;
     f += -0.5 * z * z;
     a.prior_terms[1 + k] = d / (sg * sg);
@@ -697,10 +733,14 @@ __device__ inline void prior_precompute(const GlmArgs& a, const double* sbeta, i
   f = warp_sum(f);
   if (lane == 0) a.prior_terms[0] = f;
 }
+__device__ inline void prior_precompute(const GlmArgs& a, const double* sbeta, int lane) {
+  prior_precompute_from(a, [sbeta](int k) { return sbeta[k]; }, lane);
+}
 
 // Deterministic cross-CTA finish: CTA partial -> partials[blockIdx]; the last CTA to
 // arrive sums all partials in ascending CTA order (the reference's ascending-worker merge,
 // glm.py:243-250), adds the prior (sampler.py:55-58) and writes (f, g).
+template <int CU = 5>
 __device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& sm, int nw, bool grad) {
   const int K = a.K;
   const int tid = threadIdx.x;
@@ -735,11 +775,13 @@ __device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& s
   const int G = gridDim.x;
   const int lane = tid & 31, nwarps = blockDim.x >> 5;
   // column totals in a fixed order: one warp per column, lane l folds CTAs l, l+32, ...,
-  // then the fixed butterfly.  A warp takes CU of its columns at once, and the CTA loop is
-  // unrolled 8 deep, so all of a lane's L2 loads (<= 8 x CU for <= 256 CTAs) are in flight
-  // together: one round trip instead of one per 32 CTAs (this finish is on the critical
-  // path of every launch).  The per-column summation order is unchanged.
-  constexpr int CU = 4;
+  // then the fixed butterfly.  A warp takes CU of its columns at once and the CTA loop is
+  // unrolled BU deep, so all of a lane's L2 loads (BU x CU <= 25, covering 160 CTAs x
+  // 5*nwarps columns: the whole fold of a <= 40-column evaluation on 148 SMs) are in
+  // flight together: ONE L2 round trip on the critical path of every launch (r02 phase
+  // stamps: the two-pass form with 32 columns per pass took 4.8 us at K = 32, two passes
+  // for 33 columns).  The per-column summation order is unchanged.
+  constexpr int BU = 5;  // CU: 5 for 8-warp CTAs, 3 for the 16-warp (128-register) kernels
   const int ncols = grad ? K + 1 : 1;
   for (int c0 = tid >> 5; c0 < ncols; c0 += nwarps * CU) {
     double part[CU], pr[CU];
@@ -749,10 +791,10 @@ __device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& s
       const int c = c0 + u * nwarps;
       pr[u] = (a.with_prior && c < ncols) ? __ldcg(a.prior_terms + c) : 0.0;  // in flight with the partials
     }
-    for (int b0 = 0; b0 < G; b0 += 256) {
-      double v[8][CU];
+    for (int b0 = 0; b0 < G; b0 += 32 * BU) {
+      double v[BU][CU];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < BU; ++i) {
         const int b = b0 + 32 * i + lane;
 #pragma unroll
         for (int u = 0; u < CU; ++u) {
@@ -761,16 +803,22 @@ __device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& s
         }
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < BU; ++i)
 #pragma unroll
         for (int u = 0; u < CU; ++u)
           if (b0 + 32 * i + lane < G) part[u] += v[i][u];
+    }
+    // the CU butterflies interleaved level by level (independent chains)
+#pragma unroll
+    for (int sft = 16; sft >= 1; sft >>= 1) {
+#pragma unroll
+      for (int u = 0; u < CU; ++u) part[u] += shfl_xor_d(part[u], sft);
     }
 #pragma unroll
     for (int u = 0; u < CU; ++u) {
       const int c = c0 + u * nwarps;
       if (c >= ncols) break;
-      const double tot = warp_sum(part[u]);
+      const double tot = part[u];
       if (lane != 0) continue;
       // partials hold -sum(nll) = L and the gradient; + the prior terms of prior_precompute
       double v = tot;
@@ -807,9 +855,14 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
 #endif
   const int K = a.K;
   const int S = a.stages;
-  const StreamSmem sm = carve_stream_smem(smem_raw, K, sizeof(XT), S, NCW, TR);
+  const int U = a.tps;  // tiles per stage (> 1: contiguous tile range per CTA, one copy per unit)
+  const StreamSmem sm = carve_stream_smem(smem_raw, K, sizeof(XT), S, NCW, TR * U);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // The producer thread initialises the mbarriers and issues its first round of copies
+  // before the CTA barrier (inside stream_tiles), so the first HBM round trip overlaps the
+  // other warps' prologue: beta from the parameter bank (first touch misses the constant
+  // cache) and, in CTA 0, the prior terms.
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&sm.full[s], 1);
@@ -817,22 +870,33 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     }
     fence_mbar_init();
   }
-  for (int k = threadIdx.x; k < K; k += blockDim.x) sm.sbeta[k] = beta.v[k];
-  __syncthreads();
-  if (blockIdx.x == 0 && a.with_prior && warp == NCW) prior_precompute(a, sm.sbeta, lane);
-  ab_stamp(a, 1);
-
   double breg[KC], g[KC];
 #pragma unroll
   for (int j = 0; j < KC; ++j) {
     const int c = lane_col<PAIRS != 0>(lane, j);
-    breg[j] = (c < K) ? beta.v[c] * XScale<XT>::value : 0.0;  // exact (power of two)
+    breg[j] = (warp > 0 && c < K) ? beta.v[c] * XScale<XT>::value : 0.0;  // exact (power of two)
     g[j] = 0.0;
   }
+  if (warp > 0) {
+    __syncthreads();  // pairs with the producer warp's barrier inside stream_tiles
+    ab_stamp(a, 1, 32);
+    if (blockIdx.x == 0 && a.with_prior && warp == NCW)
+      prior_precompute_from(a, [&beta](int k) { return beta.v[k]; }, lane);
+  }
   double nll = 0.0;
-  stream_tiles<XT, KC, GRAD, NCW, R, TR, PAIRS>(static_cast<const XT*>(a.X), a.y, K, blockIdx.x,
-                                         a.n_tiles * (kTileRows / TR), gridDim.x,
-                                     a.n_rows, S, sm, breg, g, nll, a.evict_first != 0);
+  int64_t tb, te, stride;
+  const int64_t nt = a.n_tiles * (kTileRows / TR);
+  if (U > 1) {  // contiguous, near-equal tile ranges
+    tb = nt * blockIdx.x / gridDim.x;
+    te = nt * (blockIdx.x + 1) / gridDim.x;
+    stride = 1;
+  } else {  // tiles interleaved across the CTAs
+    tb = blockIdx.x;
+    te = nt;
+    stride = gridDim.x;
+  }
+  stream_tiles<XT, KC, GRAD, NCW, R, TR, PAIRS, true>(static_cast<const XT*>(a.X), a.y, K, tb, te, stride, a.n_rows,
+                                                      S, sm, breg, g, nll, a.evict_first != 0, U);
   if (warp > 0) {
     const int cw = warp - 1;
     const double wsum = warp_sum(nll);
@@ -845,7 +909,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       }
     }
   }
-  cta_reduce_finalize(a, sm, NCW, GRAD);
+  cta_reduce_finalize<(NCW > 8 ? 3 : 5)>(a, sm, NCW, GRAD);
 }
 
 // Wide-K kernel (K > 256): one warp per row, lanes stride the columns, X read once from

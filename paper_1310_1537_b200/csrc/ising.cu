@@ -945,6 +945,11 @@ static cudaError_t launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t se
     const dim3 sblock(sbx, sby);
     const dim3 sgrid((per_row + sbx - 1) / sbx, std::min((h->H + sby - 1) / sby, 65535));
     const size_t smem = size_t(sby + 2) * (sbx * 16 * ng + 32);
+    if (!ising) {  // 32.6 KB static table + the stage exceed the 48 KB default
+      e = cudaFuncSetAttribute(gibbs_packed_kernel<PM_MODEL_POTTS4, true, 4, false, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+    }
     e = ising ? launch_pdl(h->pdl, gibbs_packed_kernel<PM_MODEL_ISING, true, 2, false, true>, sgrid, sblock, smem, st,
                            pa, (const unsigned long long*)h->pthr, (const uint32_t*)h->pthr32)
               : launch_pdl(h->pdl, gibbs_packed_kernel<PM_MODEL_POTTS4, true, 4, false, true>, sgrid, sblock, smem,

@@ -78,6 +78,7 @@ static const char* const kTuneNames[] = {
     "f32_pairs",         // fp32-X consumer: 0 columns, 1 sub-tile pairs (default), 2 whole tile
     "f64_pairs",         // fp64 consumer: 0 columns, 1 pairs (default)
     "stream_ncw",        // fp32-X column consumer: 15 warps (default) or 7
+    "stream_tps",        // stream kernel 32-row tiles per stage / bulk copy (default: ~24 KB stages)
     "hb_rows",           // HB row-per-lane kernel: 0 off, 1 on (default)
     "hb_rows_ncw",       // 7 (default) or 15
     "hb_rows_tps",       // tiles per stage (default 2)
