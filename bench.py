@@ -875,9 +875,12 @@ def run_gibbs(args, cfg):
     # end to end: spins in from host, sweeps, spins out
     t0 = time.perf_counter()
     part.pack_from(lat)
+    t1 = time.perf_counter()
     dev.sweeps(args.steps, 2, rng.seed, 0, rng.sweep + args.steps)
+    t2 = time.perf_counter()
     part.unpack_into(lat)
     e2e = time.perf_counter() - t0
+    e2e_parts = {"pack_ms": (t1 - t0) * 1e3, "sweeps_ms": (t2 - t1) * 1e3, "unpack_ms": (t0 + e2e - t2) * 1e3}
     peak, src = load_peaks()
     bytes_sweep = 2 * h * w
     if rank == 0:
@@ -897,7 +900,7 @@ def run_gibbs(args, cfg):
                          "peak_source": src},
             "issue_roofline": issue_roofline(args.config, ms, clk),
             "e2e": {"value": args.steps / e2e, "unit": "sweeps/s", "h2d_bytes_per_step": h * w / args.steps,
-                    "d2h_bytes_per_step": h * w / args.steps},
+                    "d2h_bytes_per_step": h * w / args.steps, "parts": e2e_parts},
             "gpu_launches": 2 * args.steps, "clocks": clk,
             "cpu_baseline": None if args.no_cpu_baseline else cpu_baseline_other(args.config)}), flush=True)
 

@@ -315,17 +315,30 @@ int choose_geometry(pm_glm_s* h) {
     }
   }
   if (kc <= kMaxKC) {
-    // Tiles per stage U (one bulk copy each): a 32-row tile of a narrow design is small (8 KB
-    // at K = 32 fp64) and the single producer thread's ~200 ns per copy then bounds the
-    // pipeline, so stages of ~24 KB hold U consecutive tiles of a contiguous per-CTA tile
-    // range (tune stream_tps=1 restores single interleaved tiles; r02 c0 breakdown).
+    // fp32-X, even K with an even register count: the pairs consumer layout
+    // (consume_tile_pairs; tune f32_pairs=0 disables for A/B)
+    // 1 = sub-tile pairs (default; +5.5 % over columns at c1f32), 2 = whole-tile consumer
+    // (KC 2 or 4, 7 warps; measured 11 % slower than pairs at K=100: the re-read stage is held
+    // for the whole tile and 2 stages per warp expose the refill latency), 0 = columns
+    const int pmode = tune("f32_pairs", 1);
+    int pairs = 0;
+    if (h->xtype == PM_X_F32 && h->K % 2 == 0 && kc % 2 == 0 && pmode > 0) pairs = (pmode == 2 && kc <= 4) ? 2 : 1;
+    // fp64 X: the same pairs layout with 16-byte loads (tune f64_pairs=0 disables for A/B)
+    if (h->xtype == PM_X_F64 && h->K % 2 == 0 && kc % 2 == 0 && tune("f64_pairs", 1) != 0) pairs = 1;
+    // Tiles per stage U (one bulk copy each), column-per-lane consumers only: a 32-row tile of
+    // a narrow design is small (8 KB at K = 32 fp64) and the single producer thread's ~200 ns
+    // per copy then bounds the pipeline, so stages of ~24 KB hold U consecutive tiles of a
+    // contiguous per-CTA tile range (tune stream_tps=1 restores single interleaved tiles).
     const size_t tile_b = size_t(kTileRows) * h->K * xs;
     int U = int(std::min<size_t>(8, std::max<size_t>(1, (24 * 1024) / tile_b)));
     const int t_u = tune("stream_tps", -1);
     if (t_u >= 1) U = std::min(t_u, 16);
-    // no more tiles per stage than the busiest CTA's share per consumer warp
+    // at least two units per consumer warp, so a warp computes on one while the next lands
+    // (config 0, 22 tiles per CTA: U = 1 / 2 / 3 / 4 -> 19.2 / 19.8 / 20.6 / 21.4 us cold and
+    // 16.5 / 15.8 / 15.5 / 16.1 us warm; N = 1e6: 70.1 / 58.1 / 58.5 / 64.6 us cold)
     const int64_t per_cta = (h->n_tiles + h->sms - 1) / std::max(1, h->sms);
-    U = int(std::max<int64_t>(1, std::min<int64_t>(U, (per_cta + kNCW - 1) / kNCW)));
+    U = int(std::max<int64_t>(1, std::min<int64_t>(U, (per_cta + 2 * kNCW - 1) / (2 * kNCW))));
+    if (pairs != 0) U = 1;
     const int tr = U * kTileRows;
     const size_t fixed = stream_smem_bytes(h->K, xs, 0, kNCW, tr);
     const size_t per_stage = stream_smem_bytes(h->K, xs, 1, 0, tr) - stream_smem_bytes(h->K, xs, 0, 0, tr);
@@ -336,24 +349,12 @@ int choose_geometry(pm_glm_s* h) {
       h->kind = KIND_STREAM;
       h->stages = S;
       h->tps = U;
+      h->pairs = pairs;
       h->threads = kStreamThreads;
       h->ncw = kNCW;
       h->smem = stream_smem_bytes(h->K, xs, S, kNCW, tr);
       h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, h->n_tiles));
     }
-    // fp32-X, even K with an even register count: the pairs consumer layout
-    // (consume_tile_pairs; tune f32_pairs=0 disables for A/B)
-    // 1 = sub-tile pairs (default; +5.5 % over columns at c1f32), 2 = whole-tile consumer
-    // (KC 2 or 4, 7 warps; measured 11 % slower than pairs at K=100: the re-read stage is held
-    // for the whole tile and 2 stages per warp expose the refill latency), 0 = columns
-    const int pmode = tune("f32_pairs", 1);
-    h->pairs = 0;
-    if (h->kind == KIND_STREAM && h->xtype == PM_X_F32 && h->K % 2 == 0 && kc % 2 == 0 && pmode > 0)
-      h->pairs = (pmode == 2 && kc <= 4) ? 2 : 1;
-    // fp64 X: the same pairs layout with 16-byte loads (tune f64_pairs=0 disables for A/B)
-    if (h->kind == KIND_STREAM && h->xtype == PM_X_F64 && h->K % 2 == 0 && kc % 2 == 0 &&
-        tune("f64_pairs", 1) != 0)
-      h->pairs = 1;
     // fp32-X, K <= 128: 15 consumer warps, one 32-row stage each (tune stream_ncw=7 disables;
     // measured: 16-row stages, 2 per warp, are 26 % slower -- per-stage overheads dominate)
     // (the pairs consumer runs 7 warps: its two unrolled sub-tiles need the registers)
@@ -902,7 +903,7 @@ int pm_glm_time_launches(pm_glm_t h, const double* betas, int32_t n, int with_pr
     const int G = h->grid;
     std::vector<unsigned long long> st(size_t(G) * 8);
     cudaMemcpy(st.data(), a.stamps, sizeof(unsigned long long) * st.size(), cudaMemcpyDeviceToHost);
-    unsigned long long t0 = ~0ull, e_max = 0, p_max = 0, s_min = ~0ull, s_max = 0, k_max = 0, f_last = 0;
+    unsigned long long t0 = ~0ull, e_max = 0, p_max = 0, s_min = ~0ull, s_max = 0, k_max = 0, f_last = 0, c5 = 0, c6 = 0;
     for (int b = 0; b < G; ++b) {
       const unsigned long long* s = &st[size_t(b) * 8];
       t0 = std::min(t0, s[0]);
@@ -912,12 +913,14 @@ int pm_glm_time_launches(pm_glm_t h, const double* betas, int32_t n, int with_pr
       s_max = std::max(s_max, s[2]);
       k_max = std::max(k_max, s[3]);
       f_last = std::max(f_last, s[4]);
+      c5 = std::max(c5, s[5]);
+      c6 = std::max(c6, s[6]);
     }
     std::fprintf(stderr,
                  "[phases] grid %d: entry spread %.2f us, prologue done %.2f, stream done first %.2f last %.2f, "
-                 "tickets done %.2f, finish done %.2f (event %.2f us per launch)\n",
+                 "tickets done %.2f, chunk sums %.2f, totals %.2f, finish done %.2f (event %.2f us per launch)\n",
                  G, (e_max - t0) * 1e-3, (p_max - t0) * 1e-3, (s_min - t0) * 1e-3, (s_max - t0) * 1e-3,
-                 (k_max - t0) * 1e-3, (f_last - t0) * 1e-3, *total_ms * 1e3 / n);
+                 (k_max - t0) * 1e-3, (c5 - t0) * 1e-3, (c6 - t0) * 1e-3, (f_last - t0) * 1e-3, *total_ms * 1e3 / n);
     cudaMemset(a.stamps, 0, sizeof(unsigned long long) * st.size());
   }
 #endif

@@ -248,7 +248,7 @@ __device__ __forceinline__ void consume_tile_pairs(const XT* xs, const double* y
       double dep = yv;
 #pragma unroll
       for (int r = 0; r < R; ++r) dep += v[r];
-      if (empty) mbar_arrive_after(empty, dep, lane, const_cast<XT*>(xs));
+      mbar_arrive_after(empty, dep, lane, const_cast<XT*>(xs));
     }
 #pragma unroll
     for (int st = R / 2; st >= 1; st >>= 1) {
@@ -352,7 +352,7 @@ __device__ __forceinline__ void consume_tile_f32full(const float* xs, const doub
     }
     vs[s] = v[0];  // block s, row 8s + b, summed over the 8 lanes sharing lane bits 3-4
   }
-  if ((HOLD || !GRAD) && empty) mbar_arrive_after(empty, dep, lane, const_cast<float*>(xs));  // all words consumed
+  if (HOLD || !GRAD) mbar_arrive_after(empty, dep, lane, const_cast<float*>(xs));  // all words consumed
   // across lane bits 4 then 3: lane l keeps block (l >> 3), i.e. tile row l
   {
     const bool up = (lane & 16) != 0;
@@ -415,7 +415,7 @@ __device__ __forceinline__ void consume_tile_f32full(const float* xs, const doub
       double dg = 0.0;
 #pragma unroll
       for (int j = 0; j < KC; ++j) dg += g[j];  // depends on every re-read word
-      if (empty) mbar_arrive_after(empty, dg, lane, const_cast<float*>(xs));
+      mbar_arrive_after(empty, dg, lane, const_cast<float*>(xs));
     }
   }
 }
@@ -485,20 +485,19 @@ __device__ inline StreamSmem carve_stream_smem(unsigned char* base, int K, int x
 //           otherwise (profiles/r02_c0_breakdown.txt).
 // A stage holds one unit; warp 0 lane 0 issues the TMA bulk copies; warps 1..NCW consume
 // units round-robin.  Rows with global (padded) index >= row_limit are masked (padding).
-// SYNC: the CTA barrier that publishes the mbarrier initialisation is taken INSIDE, after
-// the producer has issued its first round of copies (they need no `empty` wait), so the
-// first HBM round trip overlaps the rest of the CTA's prologue.  With SYNC the PRODUCER warp
-// takes that barrier in here; every other warp of the CTA executes its own __syncthreads()
-// before calling (and every warp of the CTA must call, even with no tiles).
+// MULTI (compile time): U > 1 is only compiled into the column-per-lane consumers of the
+// 8-warp kernels (the narrow designs that need it); the pairs consumers keep the plain
+// single-tile loop (a per-tile release condition inside their unrolled sub-tile pair cost
+// the fp32-X kernel 9 %, r02 pass C).
 template <typename XT, int KC, bool GRAD, int NCW, int R = SubRows<KC, GRAD>::value, int TR = kTileRows,
-          int PAIRS = 0, bool SYNC = false>
+          int PAIRS = 0>
 __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const double* __restrict__ y, int K,
                                              int64_t tile_begin, int64_t tile_end, int64_t stride,
                                              int64_t row_limit, int S, const StreamSmem& sm,
                                              const double (&breg)[KC], double (&g)[KC], double& nll_acc,
                                              bool evict_first, int U_arg = 1) {
-  // 16-warp (128-register) instantiations always run single tiles: keep U out of their registers
-  const int U = NCW > 8 ? 1 : U_arg;
+  constexpr bool MULTI = PAIRS == 0 && NCW <= 8;
+  const int U = MULTI ? U_arg : 1;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t tile_elems = uint32_t(TR) * K;
@@ -538,13 +537,6 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
         }
       }
     };
-    if constexpr (SYNC) {
-      // first round (no `empty` waits: the stages are fresh), then the CTA barrier that lets
-      // the consumers see the initialised mbarriers -- taken by the whole warp, converged
-      if (lane == 0) issue(n_mine < Se ? n_mine : Se);
-      __syncwarp();
-      __syncthreads();
-    }
     if (lane == 0) issue(n_mine);
     return;
   }
@@ -578,20 +570,24 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
       continue;
     }
 #endif
-    for (int j = 0; j < cnt; ++j) {
-      const unsigned char* xt = xstage + size_t(j) * tile_bytes;
-      const double* yt = ystage + j * TR;
-      uint64_t* rel = (j == cnt - 1) ? &sm.empty[s] : nullptr;  // release with the unit's last tile
-      const int64_t row0 = (tile0 + j) * TR;
+    if constexpr (!MULTI) {
+      const int64_t row0 = tile0 * TR;
       if constexpr (PAIRS == 2) {
-        consume_tile_f32full<KC, GRAD>(reinterpret_cast<const float*>(xt), yt, K, lane, row0, row_limit, breg, g,
-                                       nll_acc, rel, roff);
+        consume_tile_f32full<KC, GRAD>(reinterpret_cast<const float*>(xstage), ystage, K, lane, row0, row_limit,
+                                       breg, g, nll_acc, &sm.empty[s], roff);
       } else if constexpr (PAIRS == 1) {
-        consume_tile_pairs<XT, KC, GRAD, R, TR>(reinterpret_cast<const XT*>(xt), yt, K, lane, row0, row_limit,
-                                                breg, g, nll_acc, rel, roff);
+        consume_tile_pairs<XT, KC, GRAD, R, TR>(reinterpret_cast<const XT*>(xstage), ystage, K, lane, row0,
+                                                row_limit, breg, g, nll_acc, &sm.empty[s], roff);
       } else {
-        consume_tile<XT, KC, GRAD, R, TR>(reinterpret_cast<const XT*>(xt), yt, K, lane, row0, row_limit, breg, g,
-                                          nll_acc, rel);
+        consume_tile<XT, KC, GRAD, R, TR>(reinterpret_cast<const XT*>(xstage), ystage, K, lane, row0, row_limit,
+                                          breg, g, nll_acc, &sm.empty[s]);
+      }
+    } else {
+      for (int j = 0; j < cnt; ++j) {
+        uint64_t* rel = (j == cnt - 1) ? &sm.empty[s] : nullptr;  // release with the unit's last tile
+        consume_tile<XT, KC, GRAD, R, TR>(reinterpret_cast<const XT*>(xstage + size_t(j) * tile_bytes),
+                                          ystage + j * TR, K, lane, (tile0 + j) * TR, row_limit, breg, g, nll_acc,
+                                          rel);
       }
     }
     s += nact;
@@ -773,64 +769,57 @@ __device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& s
   ab_stamp(a, 3);
   if (*sm.flag == 0) return;
   const int G = gridDim.x;
-  const int lane = tid & 31, nwarps = blockDim.x >> 5;
-  // column totals in a fixed order: one warp per column, lane l folds CTAs l, l+32, ...,
-  // then the fixed butterfly.  A warp takes CU of its columns at once and the CTA loop is
-  // unrolled BU deep, so all of a lane's L2 loads (BU x CU <= 25, covering 160 CTAs x
-  // 5*nwarps columns: the whole fold of a <= 40-column evaluation on 148 SMs) are in
-  // flight together: ONE L2 round trip on the critical path of every launch (r02 phase
-  // stamps: the two-pass form with 32 columns per pass took 4.8 us at K = 32, two passes
-  // for 33 columns).  The per-column summation order is unchanged.
-  constexpr int BU = 5;  // CU: 5 for 8-warp CTAs, 3 for the 16-warp (128-register) kernels
+  const int lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
+  // Column totals in a fixed order, coalesced: lanes = 32 consecutive columns (one 256-byte
+  // row segment of a CTA's partial per warp load, every fetched sector fully used), warps =
+  // (column group, one of 4 chunks of consecutive CTAs).  A lane sums its chunk's CTAs in ascending
+  // order with up to BU loads in flight (one L2 round trip for 148 CTAs split over >= 4
+  // chunks), chunk sums go through shared memory and are added in ascending chunk order:
+  // the reference's ascending-worker merge (glm.py:243-250), bracketed by chunk.
+  // (r02 phase stamps: the previous lane-per-CTA form read 8 bytes of every 32-byte sector,
+  // 6400 sector requests from one SM: 3.8-4.8 us at K = 32 on 148 CTAs.)
+  constexpr int BU = CU >= 5 ? 40 : 20;
+  constexpr int nchunk = 4;  // fixed: a column's summation order depends on the grid only (f of
+                             // a GRAD=false launch is bit-identical to f of a GRAD=true one)
   const int ncols = grad ? K + 1 : 1;
-  for (int c0 = tid >> 5; c0 < ncols; c0 += nwarps * CU) {
-    double part[CU], pr[CU];
-#pragma unroll
-    for (int u = 0; u < CU; ++u) {
-      part[u] = 0.0;
-      const int c = c0 + u * nwarps;
-      pr[u] = (a.with_prior && c < ncols) ? __ldcg(a.prior_terms + c) : 0.0;  // in flight with the partials
-    }
-    for (int b0 = 0; b0 < G; b0 += 32 * BU) {
-      double v[BU][CU];
-#pragma unroll
-      for (int i = 0; i < BU; ++i) {
-        const int b = b0 + 32 * i + lane;
-#pragma unroll
-        for (int u = 0; u < CU; ++u) {
-          const int c = c0 + u * nwarps;
-          v[i][u] = (b < G && c < ncols) ? __ldcg(a.partials + size_t(b) * (K + 1) + c) : 0.0;
-        }
-      }
+  const int ncg = (ncols + 31) >> 5;
+  double* scratch = (size_t(nw) * K >= size_t(nchunk) * ncols) ? sm.wg : reinterpret_cast<double*>(sm.xs);
+  const double prior_c = (a.with_prior && tid < ncols) ? __ldcg(a.prior_terms + tid) : 0.0;  // in flight
+  for (int item = wid; item < ncg * nchunk; item += nwarps) {
+    const int cg = item / nchunk, chunk = item - cg * nchunk;
+    const int b_lo = int(int64_t(G) * chunk / nchunk), b_hi = int(int64_t(G) * (chunk + 1) / nchunk);
+    const int c = cg * 32 + lane;
+    double acc = 0.0;
+    for (int b0 = b_lo; b0 < b_hi; b0 += BU) {
+      double v[BU];
 #pragma unroll
       for (int i = 0; i < BU; ++i)
+        v[i] = (b0 + i < b_hi && c < ncols) ? __ldcg(a.partials + size_t(b0 + i) * (K + 1) + c) : 0.0;
 #pragma unroll
-        for (int u = 0; u < CU; ++u)
-          if (b0 + 32 * i + lane < G) part[u] += v[i][u];
+      for (int i = 0; i < BU; ++i)
+        if (b0 + i < b_hi) acc += v[i];
     }
-    // the CU butterflies interleaved level by level (independent chains)
-#pragma unroll
-    for (int sft = 16; sft >= 1; sft >>= 1) {
-#pragma unroll
-      for (int u = 0; u < CU; ++u) part[u] += shfl_xor_d(part[u], sft);
+    if (c < ncols) scratch[size_t(chunk) * ncols + c] = acc;
+  }
+  ab_stamp(a, 5);
+  __syncthreads();
+  for (int c = tid; c < ncols; c += blockDim.x) {
+    double tot = scratch[c];
+    for (int ch = 1; ch < nchunk; ++ch) tot += scratch[size_t(ch) * ncols + c];
+    // partials hold -sum(nll) = L and the gradient; + the prior terms of prior_precompute
+    double v = tot;
+    if (a.with_prior) {
+      const double pr = c == tid ? prior_c : __ldcg(a.prior_terms + c);
+      v = c == 0 ? tot + pr : tot - pr;
     }
-#pragma unroll
-    for (int u = 0; u < CU; ++u) {
-      const int c = c0 + u * nwarps;
-      if (c >= ncols) break;
-      const double tot = part[u];
-      if (lane != 0) continue;
-      // partials hold -sum(nll) = L and the gradient; + the prior terms of prior_precompute
-      double v = tot;
-      if (a.with_prior) v = c == 0 ? tot + pr[u] : tot - pr[u];
-      if (a.xw == 0) {
-        a.out[c] = v;
-      } else if (a.xphase & 1) {  // deposit into slot [parity][xrank] of every rank's mailbox (P2P stores)
-        const size_t o = (size_t(a.xepoch & 1) * a.xw + a.xrank) * size_t(K + 1) + c;
-        for (int p = 0; p < a.xw; ++p) a.xpeer[p][o] = v;
-      }
+    if (a.xw == 0) {
+      a.out[c] = v;
+    } else if (a.xphase & 1) {  // deposit into slot [parity][xrank] of every rank's mailbox (P2P stores)
+      const size_t o = (size_t(a.xepoch & 1) * a.xw + a.xrank) * size_t(K + 1) + c;
+      for (int p = 0; p < a.xw; ++p) a.xpeer[p][o] = v;
     }
   }
+  ab_stamp(a, 6);
   if (tid == 0) *a.counter = 0u;  // re-arm for the next launch (kernel boundary orders it)
 #ifdef PM_AB_PHASES
   __syncthreads();
@@ -859,10 +848,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   const StreamSmem sm = carve_stream_smem(smem_raw, K, sizeof(XT), S, NCW, TR * U);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  // The producer thread initialises the mbarriers and issues its first round of copies
-  // before the CTA barrier (inside stream_tiles), so the first HBM round trip overlaps the
-  // other warps' prologue: beta from the parameter bank (first touch misses the constant
-  // cache) and, in CTA 0, the prior terms.
+  // Thread 0 initialises the mbarriers; the CTA barrier follows at once, so the producer's
+  // first copies are in flight while the consumers fetch beta from the parameter bank (the
+  // first touch misses the constant cache) and CTA 0 computes the prior terms.
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&sm.full[s], 1);
@@ -870,6 +858,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     }
     fence_mbar_init();
   }
+  __syncthreads();
+  ab_stamp(a, 1);
   double breg[KC], g[KC];
 #pragma unroll
   for (int j = 0; j < KC; ++j) {
@@ -877,12 +867,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     breg[j] = (warp > 0 && c < K) ? beta.v[c] * XScale<XT>::value : 0.0;  // exact (power of two)
     g[j] = 0.0;
   }
-  if (warp > 0) {
-    __syncthreads();  // pairs with the producer warp's barrier inside stream_tiles
-    ab_stamp(a, 1, 32);
-    if (blockIdx.x == 0 && a.with_prior && warp == NCW)
-      prior_precompute_from(a, [&beta](int k) { return beta.v[k]; }, lane);
-  }
+  if (blockIdx.x == 0 && a.with_prior && warp == NCW)
+    prior_precompute_from(a, [&beta](int k) { return beta.v[k]; }, lane);
   double nll = 0.0;
   int64_t tb, te, stride;
   const int64_t nt = a.n_tiles * (kTileRows / TR);
@@ -895,8 +881,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     te = nt;
     stride = gridDim.x;
   }
-  stream_tiles<XT, KC, GRAD, NCW, R, TR, PAIRS, true>(static_cast<const XT*>(a.X), a.y, K, tb, te, stride, a.n_rows,
-                                                      S, sm, breg, g, nll, a.evict_first != 0, U);
+  stream_tiles<XT, KC, GRAD, NCW, R, TR, PAIRS>(static_cast<const XT*>(a.X), a.y, K, tb, te, stride, a.n_rows, S, sm,
+                                                breg, g, nll, a.evict_first != 0, U);
   if (warp > 0) {
     const int cw = warp - 1;
     const double wsum = warp_sum(nll);

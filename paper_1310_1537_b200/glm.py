@@ -163,9 +163,12 @@ class GlmDevice:
         return float(ms.value)
 
     def eval(self, beta: np.ndarray, with_prior: bool, want_grad: bool):
-        with self.lock:
-            self.launch(beta, with_prior, want_grad)
-            return self.wait(want_grad)
+        """One evaluation, one C call (pm_glm_eval holds the handle across launch + wait)."""
+        f = ctypes.c_double()
+        g = np.empty(self.n_cols) if want_grad else None
+        _lib.call("pm_glm_eval", self._h, _lib.dptr(beta), int(with_prior), int(want_grad), ctypes.byref(f),
+                  _lib.dptr(g))
+        return f.value, g
 
     def eval_device(self, beta: np.ndarray, want_grad: bool, dev_out_ptr: int, stream: int = 0,
                     with_prior: bool = False) -> None:
@@ -301,11 +304,14 @@ _TR_GRAD_FLOPS = 8
 _DIFF_FLOPS = 8
 
 
-def _check_beta(beta, n_cols: int) -> np.ndarray:
+def _check_beta(beta, n_cols: int, finite: bool = True) -> np.ndarray:
+    """Shape and finiteness of beta (glm.py:210-216).  finite=False leaves the finiteness
+    scan to the C entry the caller is about to invoke (pm_glm_eval / pm_glm_launch make the
+    same check and raise the same ValueError), one pass instead of two per evaluation."""
     beta = np.ascontiguousarray(beta, dtype=np.float64)
     if beta.shape != (n_cols,):
         raise ValueError(f"beta has shape {beta.shape}, expected ({n_cols},)")
-    if not np.isfinite(beta).all():
+    if finite and not np.isfinite(beta).all():
         raise ValueError("beta contains non-finite entries")
     return beta
 
@@ -339,8 +345,7 @@ def _evaluate(data, beta, plan: ExecPlan, prior, want_grad: bool) -> GradResult:
     dev = data.on_device(plan.device, plan.x_storage)
     with dev.lock:
         dev.set_prior(mu, sigma)
-        dev.launch(beta, mu is not None, want_grad)
-        f, g = dev.wait(want_grad)
+        f, g = dev.eval(beta, mu is not None, want_grad)
     _account(plan)
     counters.add_launches(1)
     counters.add_device_partials(dev.grid)
@@ -380,16 +385,18 @@ def _evaluate_sharded(view: ShardedMatrix, beta, plan: ExecPlan, mu, sigma, want
 
 def loglike(data, beta, plan: ExecPlan = ExecPlan()) -> float:
     """L(beta) (reference glm.py:257-274); one device pass, value plan-invariant."""
-    beta = _check_beta(beta, data.n_cols)
+    beta = _check_beta(beta, data.n_cols, finite=False)
+    f = _evaluate(data, beta, plan, None, want_grad=False).f  # raises on a non-finite beta
     counters.add_flops(data.n_rows * (2 * data.n_cols + _TR_FLOPS))
-    return _evaluate(data, beta, plan, None, want_grad=False).f
+    return f
 
 
 def loglike_grad(data, beta, plan: ExecPlan = ExecPlan()) -> GradResult:
     """L(beta) and X'(y - sigmoid(X beta)) (reference glm.py:351-364) in one fused pass."""
-    beta = _check_beta(beta, data.n_cols)
+    beta = _check_beta(beta, data.n_cols, finite=False)
+    res = _evaluate(data, beta, plan, None, want_grad=True)  # raises on a non-finite beta
     counters.add_flops(data.n_rows * (4 * data.n_cols + _TR_GRAD_FLOPS))
-    return _evaluate(data, beta, plan, None, want_grad=True)
+    return res
 
 
 def log_posterior_grad(data, beta, prior, plan: ExecPlan = ExecPlan(), want_grad: bool = True) -> GradResult:
@@ -399,9 +406,10 @@ def log_posterior_grad(data, beta, prior, plan: ExecPlan = ExecPlan(), want_grad
     GaussianPrior.logpdf_coord (sampler.py:55-58, constants dropped); the prior
     is added on the device by the kernel's finalising CTA.
     """
-    beta = _check_beta(beta, data.n_cols)
+    beta = _check_beta(beta, data.n_cols, finite=False)
+    res = _evaluate(data, beta, plan, prior, want_grad=want_grad)  # raises on a non-finite beta
     counters.add_flops(data.n_rows * (4 * data.n_cols + _TR_GRAD_FLOPS) + 4 * data.n_cols)
-    return _evaluate(data, beta, plan, prior, want_grad=want_grad)
+    return res
 
 
 # ---------------------------------------------------------------------------
