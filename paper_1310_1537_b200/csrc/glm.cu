@@ -164,6 +164,11 @@ StreamLaunch pick_stream_pairs(int kc, int pairs) {  // fp32-X, pairs layouts (e
     if (kc == 4) return launch_stream<float, 4, GRAD, 2>;
     return nullptr;
   }
+  if (pairs == 3) {
+    if (kc == 2) return launch_stream<float, 2, GRAD, 3>;
+    if (kc == 4) return launch_stream<float, 4, GRAD, 3>;
+    return nullptr;
+  }
   switch (kc) {
     case 2: return launch_stream<float, 2, GRAD, 1>;
     case 4: return launch_stream<float, 4, GRAD, 1>;
@@ -197,6 +202,11 @@ cudaError_t launch_stream15(const GlmArgs& a, const double* beta, int grid, size
 }
 
 StreamLaunch pick_stream15(int kc, bool grad, int pairs) {  // fp32-X only
+  if (pairs == 3) {
+    if (kc == 2) return grad ? launch_stream15<float, 2, true, 3> : launch_stream15<float, 2, false, 3>;
+    if (kc == 4) return grad ? launch_stream15<float, 4, true, 3> : launch_stream15<float, 4, false, 3>;
+    return nullptr;
+  }
   if (pairs) {
     if (kc == 2) return grad ? launch_stream15<float, 2, true, 1> : launch_stream15<float, 2, false, 1>;
     if (kc == 4) return grad ? launch_stream15<float, 4, true, 1> : launch_stream15<float, 4, false, 1>;
@@ -209,6 +219,21 @@ StreamLaunch pick_stream15(int kc, bool grad, int pairs) {  // fp32-X only
     case 4: return grad ? launch_stream15<float, 4, true, 0> : launch_stream15<float, 4, false, 0>;
   }
   return nullptr;
+}
+
+// fp32-X row-dot consumer with a PAIR of warps per tile (consume_tile_rowdot2): 14 consumer
+// warps = 7 pairs, 480 threads, <= 136 registers.
+constexpr int kNCW14 = 14;
+template <bool GRAD>
+cudaError_t launch_stream14(const GlmArgs& a, const double* beta, int grid, size_t smem, cudaStream_t st) {
+  static std::atomic<uint64_t> attr{0};
+  auto kern = glm_stream_kernel<float, 4, GRAD, kNCW14, 8, kTileRows, 4>;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), attr);
+  if (e != cudaSuccess) return e;
+  BetaPack<4> bp;
+  for (int k = 0; k < 128; ++k) bp.v[k] = (k < a.K) ? beta[k] : 0.0;
+  kern<<<grid, (kNCW14 + 1) * 32, smem, st>>>(a, bp);
+  return cudaGetLastError();
 }
 
 template <typename XT, bool GRAD>
@@ -323,6 +348,11 @@ int choose_geometry(pm_glm_s* h) {
     const int pmode = tune("f32_pairs", 1);
     int pairs = 0;
     if (h->xtype == PM_X_F32 && h->K % 2 == 0 && kc % 2 == 0 && pmode > 0) pairs = (pmode == 2 && kc <= 4) ? 2 : 1;
+    // 3 = row-dot consumer (consume_tile_rowdot): K % 4 == 0 with K/4 odd (conflict-free
+    // 16-byte row loads), KC 2 or 4; 7 consumer warps, or 15 with tune stream_ncw=15
+    if (h->xtype == PM_X_F32 && pmode == 3 && h->K % 4 == 0 && (h->K / 4) % 2 == 1 && (kc == 2 || kc == 4)) pairs = 3;
+    // 4 = row-dot consumer, two warps per tile (consume_tile_rowdot2): KC == 4 only
+    if (h->xtype == PM_X_F32 && pmode == 4 && h->K % 4 == 0 && (h->K / 4) % 2 == 1 && kc == 4) pairs = 4;
     // fp64 X: the same pairs layout with 16-byte loads (tune f64_pairs=0 disables for A/B)
     if (h->xtype == PM_X_F64 && h->K % 2 == 0 && kc % 2 == 0 && tune("f64_pairs", 1) != 0) pairs = 1;
     // Tiles per stage U (one bulk copy each), column-per-lane consumers only: a 32-row tile of
@@ -358,8 +388,8 @@ int choose_geometry(pm_glm_s* h) {
     // fp32-X, K <= 128: 15 consumer warps, one 32-row stage each (tune stream_ncw=7 disables;
     // measured: 16-row stages, 2 per warp, are 26 % slower -- per-stage overheads dominate)
     // (the pairs consumer runs 7 warps: its two unrolled sub-tiles need the registers)
-    if (h->kind == KIND_STREAM && h->xtype == PM_X_F32 && kc <= 4 && h->pairs == 0 &&
-        tune("stream_ncw", 15) != 7) {
+    if (h->kind == KIND_STREAM && h->xtype == PM_X_F32 && kc <= 4 &&
+        ((h->pairs == 0 && tune("stream_ncw", 15) != 7) || (h->pairs == 3 && tune("stream_ncw", 7) == 15))) {
       const size_t fixed15 = stream_smem_bytes(h->K, xs, 0, kNCW15);
       const size_t per_stage1 = stream_smem_bytes(h->K, xs, 1, 0) - stream_smem_bytes(h->K, xs, 0, 0);
       int S15 = int((budget - (long)fixed15) / (long)per_stage1);
@@ -371,6 +401,20 @@ int choose_geometry(pm_glm_s* h) {
         h->threads = (kNCW15 + 1) * 32;
         h->smem = stream_smem_bytes(h->K, xs, h->stages, kNCW15);
       }
+    }
+  }
+  if (h->kind == KIND_STREAM && h->pairs == 4) {
+    // 7 warp pairs, two stages each when they fit (else one)
+    int S14 = 14;
+    if (stream_smem_bytes(h->K, xs, S14, kNCW14) > size_t(budget)) S14 = 7;
+    if (stream_smem_bytes(h->K, xs, S14, kNCW14) <= size_t(budget)) {
+      h->stages = S14;
+      h->tps = 1;
+      h->ncw = kNCW14;
+      h->threads = (kNCW14 + 1) * 32;
+      h->smem = stream_smem_bytes(h->K, xs, S14, kNCW14);
+    } else {
+      h->pairs = 1;  // does not fit: the sub-tile pairs consumer
     }
   }
   if (h->kind == KIND_NONE) {
@@ -398,6 +442,7 @@ GlmArgs make_args(pm_glm_s* h, bool with_prior, double* out) {
   a.K = h->K;
   a.stages = h->stages;
   a.tps = h->kind == KIND_STREAM ? h->tps : 1;
+  a.selfprod = (h->kind == KIND_STREAM && h->pairs == 3 && tune("f32_selfprod", 1) != 0) ? 1 : 0;
   a.with_prior = with_prior ? 1 : 0;
   a.evict_first = 1;
   a.prior_mu = h->prior_mu;
@@ -458,8 +503,9 @@ int enqueue_eval(pm_glm_s* h, const double* beta, bool with_prior, bool grad, do
     for (int k = 0; k < h->K; ++k) wide_fallback |= !(std::fabs(beta[k]) < 0x1p100);
   }
   if (h->kind == KIND_STREAM && !wide_fallback) {
-    StreamLaunch fn = h->ncw == kNCW15 ? pick_stream15((h->K + 31) / 32, grad, h->pairs)
-                                       : pick_stream_any(h->xtype, (h->K + 31) / 32, grad, h->pairs);
+    StreamLaunch fn = h->ncw == kNCW14 ? (grad ? launch_stream14<true> : launch_stream14<false>)
+                      : h->ncw == kNCW15 ? pick_stream15((h->K + 31) / 32, grad, h->pairs)
+                                         : pick_stream_any(h->xtype, (h->K + 31) / 32, grad, h->pairs);
     e = fn(a, beta, h->grid, h->smem, st);
   } else if (h->kind == KIND_ROWS) {
     RowsLaunch fn = grad ? pick_rows<true>(h->K) : pick_rows<false>(h->K);

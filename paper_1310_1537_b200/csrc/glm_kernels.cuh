@@ -420,6 +420,174 @@ __device__ __forceinline__ void consume_tile_f32full(const float* xs, const doub
   }
 }
 
+// fp32-X "row-dot" consumer (PAIRS == 3; K % 4 == 0 and K/4 odd, so the 16-byte row loads of
+// a quarter-warp fall in distinct bank groups).
+// Phase A: lane l owns ROW l of the 32-row tile: its dot product over all K columns with
+//   16-byte shared loads of the row, beta broadcast from shared memory (every lane reads the
+//   same address), 4 interleaved DFMA chains and F2F widening (XU pipe, otherwise idle) --
+//   no shuffles, no transpose -- then the logistic terms ONCE per row.
+// Phase B: the gradient in the pairs layout (lane l owns columns 64c + 2l, 64c + 2l + 1): the
+//   tile is re-read row by row with 8-byte loads, widened by integer ops (x * 2^-896 against
+//   w * 2^896, exact), w_r broadcast from lane r.
+// Against consume_tile_pairs at K = 100: ~33 instead of ~45 warp instructions per row, 64
+// instead of 124 shuffles per tile, and x never lives in registers across the two phases
+// (the pairs consumer keeps 16 x 4 doubles = 128 registers per sub-tile in flight).
+template <int KC, bool GRAD>
+__device__ __forceinline__ void consume_tile_rowdot(const float* xs, const double* ys, int K, int lane,
+                                                    int64_t row0, int64_t row_limit, const double* sbeta,
+                                                    double (&g)[KC], double& nll_acc, uint64_t* empty) {
+  static_assert(KC % 2 == 0, "row-dot consumer: pairs layout in the gradient phase");
+  constexpr int KP = KC / 2;
+  const float* xr = xs + size_t(lane) * K;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  const int nq = K >> 2;
+#pragma unroll 5
+  for (int q = 0; q < nq; ++q) {
+    const float4 xv = *reinterpret_cast<const float4*>(xr + 4 * q);
+    const double2 b01 = *reinterpret_cast<const double2*>(sbeta + 4 * q);
+    const double2 b23 = *reinterpret_cast<const double2*>(sbeta + 4 * q + 2);
+    a0 = fma(double(xv.x), b01.x, a0);
+    a1 = fma(double(xv.y), b01.y, a1);
+    a2 = fma(double(xv.z), b23.x, a2);
+    a3 = fma(double(xv.w), b23.y, a3);
+  }
+  const double t = (a0 + a1) + (a2 + a3);
+  const double yv = ys[lane];
+  double nll, w;
+  row_terms(t, yv, nll, w);
+  const bool valid = row0 + lane < row_limit;
+  nll_acc += valid ? nll : 0.0;
+  if constexpr (!GRAD) {
+    mbar_arrive_after(empty, t + yv, lane, const_cast<float*>(xs));
+    return;
+  }
+  w = valid ? w * kF32Unscale : 0.0;  // exact (power of two)
+  const bool last_ok = 64 * (KP - 1) + 2 * lane < K;
+  const char* xb = reinterpret_cast<const char*>(xs) + 2 * lane * sizeof(float);
+  const uint32_t row_bytes = uint32_t(K) * sizeof(float);
+  constexpr int NS = KC >= 8 ? 1 : 8 / KC;
+  double ga[NS > 1 ? NS - 1 : 1][KC];
+#pragma unroll
+  for (int s2 = 0; s2 + 1 < NS; ++s2)
+#pragma unroll
+    for (int j = 0; j < KC; ++j) ga[s2][j] = 0.0;
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    const double wr = __shfl_sync(0xffffffffu, w, r);
+#pragma unroll
+    for (int c = 0; c < KP; ++c) {
+      uint2 u = make_uint2(0u, 0u);
+      if (c < KP - 1 || last_ok) u = *reinterpret_cast<const uint2*>(xb + r * row_bytes + 256 * c);
+      const double x0 = ld_x_scaled(reinterpret_cast<const float*>(&u.x));
+      const double x1 = ld_x_scaled(reinterpret_cast<const float*>(&u.y));
+      if (r % NS == 0) {
+        g[2 * c] = fma(wr, x0, g[2 * c]);
+        g[2 * c + 1] = fma(wr, x1, g[2 * c + 1]);
+      } else {
+        ga[r % NS - 1][2 * c] = fma(wr, x0, ga[r % NS - 1][2 * c]);
+        ga[r % NS - 1][2 * c + 1] = fma(wr, x1, ga[r % NS - 1][2 * c + 1]);
+      }
+    }
+  }
+#pragma unroll
+  for (int s2 = 0; s2 + 1 < NS; ++s2)
+#pragma unroll
+    for (int j = 0; j < KC; ++j) g[j] += ga[s2][j];
+  double dg = 0.0;
+#pragma unroll
+  for (int j = 0; j < KC; ++j) dg += g[j];  // depends on every re-read word
+  mbar_arrive_after(empty, dg, lane, const_cast<float*>(xs));
+}
+
+// fp32-X row-dot consumer run by a PAIR of warps per tile (PAIRS == 4; KC == 4, K % 4 == 0,
+// K/4 odd).  A single warp per tile holds its stage for the whole two-phase tile time, and 15
+// such warps with one stage each left the consumers waiting on their refills for 42 % of the
+// samples (profiles/r02_ncu_rowdot15_*: by Little's law ~6 tiles must be in flight per SM on
+// top of the ones being computed, and 21 stages of 13 KB do not fit).  Two warps per tile
+// halve the hold time: 7 pairs x 2 stages = 14 stages, double-buffered, 14 consumer warps.
+//   phase A: warp `sub` of the pair takes the 16-byte column chunks [q_lo, q_hi) of ALL 32
+//     rows (lane = row); the two partial dot products meet through shared memory (`xch`,
+//     double-buffered by tile parity) at a 64-thread named barrier; both warps evaluate the
+//     logistic terms (each needs w for its rows below; only sub 0 counts f).
+//   phase B: warp `sub` adds rows [16 sub, 16 sub + 16) into its own gradient partial (pairs
+//     layout, integer widening), then both warps arrive on the stage's release barrier
+//     (initialised with count 2); each writes its dependency word into its OWN half of the
+//     stage (the partner may still be reading the other half).
+template <int KC, bool GRAD>
+__device__ __forceinline__ void consume_tile_rowdot2(const float* xs, const double* ys, int K, int lane, int sub,
+                                                     int pair, uint32_t parity, int64_t row0, int64_t row_limit,
+                                                     const double* sbeta, double* xch, double (&g)[KC],
+                                                     double& nll_acc, uint64_t* empty) {
+  static_assert(KC % 2 == 0, "row-dot consumer: pairs layout in the gradient phase");
+  constexpr int KP = KC / 2;
+  const float* xr = xs + size_t(lane) * K;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  const int nq = K >> 2, nh = (nq + 1) >> 1;
+  const int q_lo = sub ? nh : 0, q_hi = sub ? nq : nh;
+#pragma unroll 4
+  for (int q = q_lo; q < q_hi; ++q) {
+    const float4 xv = *reinterpret_cast<const float4*>(xr + 4 * q);
+    const double2 b01 = *reinterpret_cast<const double2*>(sbeta + 4 * q);
+    const double2 b23 = *reinterpret_cast<const double2*>(sbeta + 4 * q + 2);
+    a0 = fma(double(xv.x), b01.x, a0);
+    a1 = fma(double(xv.y), b01.y, a1);
+    a2 = fma(double(xv.z), b23.x, a2);
+    a3 = fma(double(xv.w), b23.y, a3);
+  }
+  const double tpart = (a0 + a1) + (a2 + a3);
+  double* box = xch + ((size_t(pair) * 2 + parity) * 2) * 32;  // [pair][parity][sub][lane]
+  box[sub * 32 + lane] = tpart;
+  asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
+  const double other = box[(sub ^ 1) * 32 + lane];
+  const double t = sub ? other + tpart : tpart + other;  // t_0 + t_1 in both warps
+  const double yv = ys[lane];
+  double nll, w;
+  row_terms(t, yv, nll, w);
+  const bool valid = row0 + lane < row_limit;
+  nll_acc += (valid && sub == 0) ? nll : 0.0;
+  float* mine = const_cast<float*>(xs) + size_t(16 * sub) * K;  // this warp's half of the stage
+  if constexpr (!GRAD) {
+    mbar_arrive_after(empty, t + yv, lane, mine);
+    return;
+  }
+  w = valid ? w * kF32Unscale : 0.0;  // exact (power of two)
+  const bool last_ok = 64 * (KP - 1) + 2 * lane < K;
+  const char* xb = reinterpret_cast<const char*>(mine) + 2 * lane * sizeof(float);
+  const uint32_t row_bytes = uint32_t(K) * sizeof(float);
+  constexpr int NS = KC >= 8 ? 1 : 8 / KC;
+  double ga[NS > 1 ? NS - 1 : 1][KC];
+#pragma unroll
+  for (int s2 = 0; s2 + 1 < NS; ++s2)
+#pragma unroll
+    for (int j = 0; j < KC; ++j) ga[s2][j] = 0.0;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const double wr = __shfl_sync(0xffffffffu, w, 16 * sub + r);
+#pragma unroll
+    for (int c = 0; c < KP; ++c) {
+      uint2 u = make_uint2(0u, 0u);
+      if (c < KP - 1 || last_ok) u = *reinterpret_cast<const uint2*>(xb + r * row_bytes + 256 * c);
+      const double x0 = ld_x_scaled(reinterpret_cast<const float*>(&u.x));
+      const double x1 = ld_x_scaled(reinterpret_cast<const float*>(&u.y));
+      if (r % NS == 0) {
+        g[2 * c] = fma(wr, x0, g[2 * c]);
+        g[2 * c + 1] = fma(wr, x1, g[2 * c + 1]);
+      } else {
+        ga[r % NS - 1][2 * c] = fma(wr, x0, ga[r % NS - 1][2 * c]);
+        ga[r % NS - 1][2 * c + 1] = fma(wr, x1, ga[r % NS - 1][2 * c + 1]);
+      }
+    }
+  }
+#pragma unroll
+  for (int s2 = 0; s2 + 1 < NS; ++s2)
+#pragma unroll
+    for (int j = 0; j < KC; ++j) g[j] += ga[s2][j];
+  double dg = 0.0;
+#pragma unroll
+  for (int j = 0; j < KC; ++j) dg += g[j];  // depends on every re-read word
+  mbar_arrive_after(empty, dg, lane, mine);
+}
+
 // Column owned by register j of `lane` in the two consumer layouts.
 template <bool PAIRS>
 __device__ __forceinline__ int lane_col(int lane, int j) {
@@ -495,7 +663,7 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
                                              int64_t tile_begin, int64_t tile_end, int64_t stride,
                                              int64_t row_limit, int S, const StreamSmem& sm,
                                              const double (&breg)[KC], double (&g)[KC], double& nll_acc,
-                                             bool evict_first, int U_arg = 1) {
+                                             bool evict_first, int U_arg = 1, bool selfprod = false) {
   constexpr bool MULTI = PAIRS == 0 && NCW <= 8;
   const int U = MULTI ? U_arg : 1;
   const int warp = threadIdx.x >> 5;
@@ -508,9 +676,58 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
   // Every stage must belong to exactly one consumer warp, which uses it in order: an
   // mbarrier parity wait cannot tell phase n from phase n+2, so a stage shared by two
   // warps could let one of them run a phase ahead.  nact consumers, Se = multiple of nact.
-  const int nact = S < NCW ? S : NCW;
+  constexpr int CW = PAIRS == 4 ? 2 : 1;  // warps per consumer unit (a stage's owner)
+  constexpr int NCU = NCW / CW;           // consumer units
+  const int nact = S < NCU ? S : NCU;
   const int Se = S - S % nact;
 
+  if constexpr (PAIRS == 3) {
+    // Self-producing consumers (row-dot consumer, runtime flag): every consumer warp issues
+    // the bulk copies of its OWN next tile into the stage it has just finished reading, so
+    // there is no producer thread to serialise on (~100 ns per copy, in stage order: with one
+    // stage per warp a warp that finishes out of order waits behind the producer's head of
+    // line) and no `empty` barrier: the refill starts the moment the stage is quiescent.
+    if (selfprod) {
+      if (warp == 0) return;
+      const int cw = warp - 1;
+      if (cw >= nact) return;
+      const int spw = Se / nact;  // stages per warp
+      const uint64_t pol = l2_policy_evict_first();
+      auto issue_one = [&](int64_t i, int s) {  // lane 0
+        const int64_t tile = tile_begin + i * stride;
+        mbar_arrive_expect_tx(&sm.full[s], tile_bytes + TR * uint32_t(sizeof(double)));
+        const XT* src = X + tile * int64_t(tile_elems);
+        if (evict_first) {
+          bulk_g2s_hint(sm.xs + size_t(s) * tile_pitch, src, tile_bytes, &sm.full[s], pol);
+        } else {
+          bulk_g2s(sm.xs + size_t(s) * tile_pitch, src, tile_bytes, &sm.full[s]);
+        }
+        bulk_g2s(sm.ys + size_t(s) * TR, y + tile * TR, TR * uint32_t(sizeof(double)), &sm.full[s]);
+      };
+      if (lane == 0) {
+        for (int m = 0; m < spw; ++m) {
+          const int64_t i = cw + int64_t(m) * nact;
+          if (i < n_mine) issue_one(i, cw + m * nact);
+        }
+      }
+      int m = 0;        // stage slot of this warp
+      uint32_t n = 0;   // use count of the slot
+      for (int64_t i = cw; i < n_mine; i += nact) {
+        const int s = cw + m * nact;
+        mbar_wait(&sm.full[s], n & 1);
+        consume_tile_rowdot<KC, GRAD>(reinterpret_cast<const float*>(sm.xs + size_t(s) * tile_pitch),
+                                      sm.ys + size_t(s) * TR, K, lane, (tile_begin + i * stride) * TR, row_limit,
+                                      sm.sbeta, g, nll_acc, nullptr);
+        const int64_t nxt = i + int64_t(spw) * nact;  // the stage is quiescent: refill it
+        if (lane == 0 && nxt < n_mine) issue_one(nxt, s);
+        if (++m == spw) {
+          m = 0;
+          ++n;
+        }
+      }
+      return;
+    }
+  }
   if (warp == 0) {
     const uint64_t pol = l2_policy_evict_first();
     int s = 0;        // stage = i % Se
@@ -540,13 +757,14 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
     if (lane == 0) issue(n_mine);
     return;
   }
-  const int cw = warp - 1;
+  const int cw = (warp - 1) / CW;
+  [[maybe_unused]] const int sub = (warp - 1) % CW;
   if (cw >= nact) return;
   int s = cw;       // i % Se for i = cw + m*nact (Se is a multiple of nact)
   uint32_t n = 0;   // i / Se
-  constexpr int RO = PAIRS == 2 ? 8 : (PAIRS ? R : 1);
+  constexpr int RO = PAIRS == 2 ? 8 : (PAIRS == 1 ? R : 1);
   uint32_t roff[RO];  // pairs layouts: byte offset of slot r's row + this lane's pair
-  if constexpr (PAIRS != 0) {
+  if constexpr (PAIRS == 1 || PAIRS == 2) {
 #pragma unroll
     for (int r = 0; r < RO; ++r) roff[r] = uint32_t(((r ^ (lane & (RO - 1))) * K + 2 * lane) * sizeof(XT));
   }
@@ -572,7 +790,15 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
 #endif
     if constexpr (!MULTI) {
       const int64_t row0 = tile0 * TR;
-      if constexpr (PAIRS == 2) {
+      if constexpr (PAIRS == 4) {
+        // xch: the pair's exchange boxes live in the (still unused) per-warp gradient area
+        consume_tile_rowdot2<KC, GRAD>(reinterpret_cast<const float*>(xstage), ystage, K, lane, sub, cw,
+                                       uint32_t((i / nact) & 1), row0, row_limit, sm.sbeta, sm.wg, g, nll_acc,
+                                       &sm.empty[s]);
+      } else if constexpr (PAIRS == 3) {
+        consume_tile_rowdot<KC, GRAD>(reinterpret_cast<const float*>(xstage), ystage, K, lane, row0, row_limit,
+                                      sm.sbeta, g, nll_acc, &sm.empty[s]);
+      } else if constexpr (PAIRS == 2) {
         consume_tile_f32full<KC, GRAD>(reinterpret_cast<const float*>(xstage), ystage, K, lane, row0, row_limit,
                                        breg, g, nll_acc, &sm.empty[s], roff);
       } else if constexpr (PAIRS == 1) {
@@ -619,6 +845,7 @@ struct GlmArgs {
   int K;
   int stages;
   int tps;                    // stream kernel: tiles per stage (1 = interleaved single tiles)
+  int selfprod;               // row-dot consumer: consumer warps issue their own bulk copies
   int with_prior;
   int evict_first;
   const double* prior_mu;     // device [K]
@@ -854,9 +1081,12 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], 1);
+      mbar_init(&sm.empty[s], PAIRS == 4 ? 2 : 1);  // released by every warp of the owning unit
     }
     fence_mbar_init();
+  }
+  if constexpr (PAIRS >= 3) {  // the row-dot consumers read all of beta from shared memory
+    for (int k = threadIdx.x; k < K; k += blockDim.x) sm.sbeta[k] = beta.v[k];
   }
   __syncthreads();
   ab_stamp(a, 1);
@@ -882,7 +1112,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     stride = gridDim.x;
   }
   stream_tiles<XT, KC, GRAD, NCW, R, TR, PAIRS>(static_cast<const XT*>(a.X), a.y, K, tb, te, stride, a.n_rows, S, sm,
-                                                breg, g, nll, a.evict_first != 0, U);
+                                                breg, g, nll, a.evict_first != 0, U, a.selfprod != 0);
+  if constexpr (PAIRS == 4) __syncthreads();  // the pairs' exchange boxes share sm.wg: all tiles done first
   if (warp > 0) {
     const int cw = warp - 1;
     const double wsum = warp_sum(nll);

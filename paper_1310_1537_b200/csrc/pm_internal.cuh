@@ -131,7 +131,9 @@ __device__ __forceinline__ void mbar_arrive_after(uint64_t* bar, double dep, int
   reinterpret_cast<volatile uint32_t*>(stage)[lane] = __double2loint(dep);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncwarp();
-  if (lane == 0)
+  // bar == nullptr: the caller refills the stage itself (self-producing consumers) and only
+  // needs the quiesce above
+  if (lane == 0 && bar)
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
                  : "memory");
 }

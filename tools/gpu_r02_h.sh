@@ -1,0 +1,35 @@
+# r02 pass H: fp32-X row-dot consumer by warp pairs (tune f32_pairs=4): parity, repeats, bench
+O=gpurun_out/r02h
+mkdir -p $O
+cat > /tmp/rowdot2_check.py <<'PY'
+import sys, numpy as np
+sys.path.insert(0, '.')
+from oracle import glm_oracle as gl
+from paper_1310_1537_b200 import _lib, glm
+from paper_1310_1537_b200.glm import DesignMatrix, ExecPlan
+from paper_1310_1537_b200.sampler import GaussianPrior
+from paper_1310_1537_b200.synthetic import baseline_design
+for k, n in [(100, 40_001), (100, 1_000_003), (108, 5_000), (116, 33), (124, 200_000)]:
+    with _lib.tuned(f32_pairs=4):
+        x, y, _, betas = baseline_design(n, k, seed=k, n_eval=2)
+        d = DesignMatrix(x, y); prior = GaussianPrior.isotropic(k, 0.0, 10.0)
+        plan = ExecPlan(x_storage="f32")
+        r = glm.log_posterior_grad(d, betas[0], prior, plan)
+        xr = x.astype(np.float32).astype(np.float64)
+        f, g = gl.log_posterior_grad(xr, y, betas[0], prior.mu, prior.sigma)
+        ef = abs(r.f - f) / max(abs(f), 1.0); eg = float(np.max(np.abs(r.g - g) / np.maximum(np.abs(g), 1.0)))
+        fl = glm.loglike(d, betas[0], plan); f0 = gl.loglike_grad(xr, y, betas[0])[0]
+        print(k, n, d.on_device(0, "f32").geometry(), "rel f", ef, "rel g", eg, "loglike rel", abs(fl - f0) / abs(f0), flush=True)
+        assert ef < 1e-10 and eg < 1e-10 and abs(fl - f0) / abs(f0) < 1e-10
+        for i in range(40):
+            o = glm.log_posterior_grad(d, betas[1], prior, plan)
+            a = glm.log_posterior_grad(d, betas[0], prior, plan)
+            assert a.f == r.f and np.array_equal(a.g, r.g), i
+        d.release_device()
+print("ok")
+PY
+timeout 900 python /tmp/rowdot2_check.py > $O/rowdot2_check.log 2>&1; echo "rowdot2 check rc=$?" > $O/summary.txt
+timeout 600 python bench.py --config c1f32 --no-cpu-baseline --steps 300 > $O/c1f32_pairs1.log 2>&1
+timeout 600 python bench.py --config c1f32 --no-cpu-baseline --steps 300 --tune f32_pairs=4 > $O/c1f32_rowdot2.log 2>&1
+timeout 600 python bench.py --config c1f32 --no-cpu-baseline --steps 300 --tune f32_pairs=3 --tune stream_ncw=15 > $O/c1f32_rowdot15.log 2>&1
+cat $O/summary.txt

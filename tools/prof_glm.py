@@ -17,7 +17,11 @@ p.add_argument("--n", type=int, default=10_000_000)
 p.add_argument("--k", type=int, default=100)
 p.add_argument("--f32", action="store_true")
 p.add_argument("--launches", type=int, default=5)
+p.add_argument("--tune", action="append", default=[])
 a = p.parse_args()
+from paper_1310_1537_b200 import _lib  # noqa: E402
+for kv in a.tune:
+    _lib.set_tune(kv.split("=")[0], int(kv.split("=")[1]))
 x, y, _, betas = baseline_design(a.n, a.k, seed=1, n_eval=a.launches + 1)
 d = glm.DesignMatrix(x, y)
 prior = GaussianPrior.isotropic(a.k, 0.0, 10.0)
