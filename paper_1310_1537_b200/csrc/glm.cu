@@ -83,6 +83,7 @@ struct pm_glm_s {
   int kind = KIND_NONE;
   int grid = 0, threads = 0, stages = 0, tps = 1, ncw = 7;
   int pairs = 0;  // fp32-X consumer layout (glm_stream_kernel PAIRS)
+  int selfprod = 0;  // row-dot consumer: 1 consumer warps issue their own copies, 3 + warp 0 consumes too
   size_t smem = 0;
   bool launched = false;
   int last_want_grad = 1;
@@ -301,6 +302,7 @@ int choose_geometry(pm_glm_s* h) {
   const int budget = std::min(max_optin_smem(h->device), 232448) - 1024;
   h->kind = KIND_NONE;
   h->pairs = 0;
+  h->selfprod = 0;
   h->tps = 1;
   const int t_rows = tune("glm_rows", -1);
   // row-per-lane kernel: fp64, even K <= 30, and enough tiles to fill the machine (measured on
@@ -345,12 +347,16 @@ int choose_geometry(pm_glm_s* h) {
     // 1 = sub-tile pairs (default; +5.5 % over columns at c1f32), 2 = whole-tile consumer
     // (KC 2 or 4, 7 warps; measured 11 % slower than pairs at K=100: the re-read stage is held
     // for the whole tile and 2 stages per warp expose the refill latency), 0 = columns
-    const int pmode = tune("f32_pairs", 1);
+    // default (-1): the row-dot consumer where it applies (below), else sub-tile pairs
+    const int pmode_t = tune("f32_pairs", -1);
+    const bool rowdot_ok = h->xtype == PM_X_F32 && h->K % 4 == 0 && (h->K / 4) % 2 == 1 && (kc == 2 || kc == 4);
+    const int pmode = pmode_t >= 0 ? pmode_t : (rowdot_ok ? 3 : 1);
     int pairs = 0;
     if (h->xtype == PM_X_F32 && h->K % 2 == 0 && kc % 2 == 0 && pmode > 0) pairs = (pmode == 2 && kc <= 4) ? 2 : 1;
     // 3 = row-dot consumer (consume_tile_rowdot): K % 4 == 0 with K/4 odd (conflict-free
-    // 16-byte row loads), KC 2 or 4; 7 consumer warps, or 15 with tune stream_ncw=15
-    if (h->xtype == PM_X_F32 && pmode == 3 && h->K % 4 == 0 && (h->K / 4) % 2 == 1 && (kc == 2 || kc == 4)) pairs = 3;
+    // 16-byte row loads), KC 2 or 4; 15 (+1) consumer warps, or 7 (+1) with tune stream_ncw=7.
+    // c1f32: 1406 evals/s vs 1272 with the sub-tile pairs consumer (profiles/r02_ab_f32_rowdot.txt)
+    if (pmode == 3 && rowdot_ok) pairs = 3;
     // 4 = row-dot consumer, two warps per tile (consume_tile_rowdot2): KC == 4 only
     if (h->xtype == PM_X_F32 && pmode == 4 && h->K % 4 == 0 && (h->K / 4) % 2 == 1 && kc == 4) pairs = 4;
     // fp64 X: the same pairs layout with 16-byte loads (tune f64_pairs=0 disables for A/B)
@@ -389,7 +395,7 @@ int choose_geometry(pm_glm_s* h) {
     // measured: 16-row stages, 2 per warp, are 26 % slower -- per-stage overheads dominate)
     // (the pairs consumer runs 7 warps: its two unrolled sub-tiles need the registers)
     if (h->kind == KIND_STREAM && h->xtype == PM_X_F32 && kc <= 4 &&
-        ((h->pairs == 0 && tune("stream_ncw", 15) != 7) || (h->pairs == 3 && tune("stream_ncw", 7) == 15))) {
+        ((h->pairs == 0 || h->pairs == 3) && tune("stream_ncw", 15) != 7)) {
       const size_t fixed15 = stream_smem_bytes(h->K, xs, 0, kNCW15);
       const size_t per_stage1 = stream_smem_bytes(h->K, xs, 1, 0) - stream_smem_bytes(h->K, xs, 0, 0);
       int S15 = int((budget - (long)fixed15) / (long)per_stage1);
@@ -400,6 +406,23 @@ int choose_geometry(pm_glm_s* h) {
         h->ncw = kNCW15;
         h->threads = (kNCW15 + 1) * 32;
         h->smem = stream_smem_bytes(h->K, xs, h->stages, kNCW15);
+      }
+    }
+  }
+  if (h->kind == KIND_STREAM && h->pairs == 3) {
+    // row-dot consumer: self-producing consumer warps (tune f32_selfprod: 0 = producer thread,
+    // 1 = consumer warps issue their own copies, 3 (default) = and warp 0 consumes as well:
+    // ncw + 1 consumer warps with one stage each, or two when they fit)
+    h->selfprod = tune("f32_selfprod", 3);
+    if (h->selfprod == 3) {
+      const int nw = h->ncw + 1;
+      int S = 2 * nw;
+      if (stream_smem_bytes(h->K, xs, S, nw) > size_t(budget)) S = nw;
+      if (stream_smem_bytes(h->K, xs, S, nw) <= size_t(budget)) {
+        h->stages = S;
+        h->smem = stream_smem_bytes(h->K, xs, S, nw);
+      } else {
+        h->selfprod = 1;
       }
     }
   }
@@ -442,7 +465,7 @@ GlmArgs make_args(pm_glm_s* h, bool with_prior, double* out) {
   a.K = h->K;
   a.stages = h->stages;
   a.tps = h->kind == KIND_STREAM ? h->tps : 1;
-  a.selfprod = (h->kind == KIND_STREAM && h->pairs == 3 && tune("f32_selfprod", 1) != 0) ? 1 : 0;
+  a.selfprod = (h->kind == KIND_STREAM && h->pairs == 3) ? h->selfprod : 0;
   a.with_prior = with_prior ? 1 : 0;
   a.evict_first = 1;
   a.prior_mu = h->prior_mu;

@@ -432,10 +432,21 @@ __device__ __forceinline__ void consume_tile_f32full(const float* xs, const doub
 // Against consume_tile_pairs at K = 100: ~33 instead of ~45 warp instructions per row, 64
 // instead of 124 shuffles per tile, and x never lives in registers across the two phases
 // (the pairs consumer keeps 16 x 4 doubles = 128 registers per sub-tile in flight).
-template <int KC, bool GRAD>
+// leading column pairs of every gradient-phase row widened by F2F (XU pipe) instead of integer
+// ops (ALU pipe); A/B builds override it (-DPM_ROWDOT_F2F_PAIRS=0|1|2)
+#ifndef PM_ROWDOT_F2F_PAIRS
+#define PM_ROWDOT_F2F_PAIRS 1
+#endif
+struct NoMid {
+  __device__ __forceinline__ void operator()(double) const {}
+};
+// `mid(dep)` is called once rows 0..15 of the gradient phase have been read (dep depends on
+// every word read so far): the self-producing form refills the stage's first half there.
+template <int KC, bool GRAD, class Mid = NoMid>
 __device__ __forceinline__ void consume_tile_rowdot(const float* xs, const double* ys, int K, int lane,
                                                     int64_t row0, int64_t row_limit, const double* sbeta,
-                                                    double (&g)[KC], double& nll_acc, uint64_t* empty) {
+                                                    double (&g)[KC], double& nll_acc, uint64_t* empty,
+                                                    Mid mid = Mid(), float* done_word = nullptr) {
   static_assert(KC % 2 == 0, "row-dot consumer: pairs layout in the gradient phase");
   constexpr int KP = KC / 2;
   const float* xr = xs + size_t(lane) * K;
@@ -474,18 +485,37 @@ __device__ __forceinline__ void consume_tile_rowdot(const float* xs, const doubl
 #pragma unroll
   for (int r = 0; r < 32; ++r) {
     const double wr = __shfl_sync(0xffffffffu, w, r);
+    // the first pair of every row is widened by F2F against the unscaled residual (one
+    // exact DMUL per row), the others by integer ops against the scaled one: the products
+    // are the same real numbers, so the sums do not depend on the split -- it balances the
+    // XU pipe (F2F) against the ALU pipe (3 integer ops per element)
+    [[maybe_unused]] const double wr_u = wr * (1.0 / kF32Unscale);
 #pragma unroll
     for (int c = 0; c < KP; ++c) {
       uint2 u = make_uint2(0u, 0u);
       if (c < KP - 1 || last_ok) u = *reinterpret_cast<const uint2*>(xb + r * row_bytes + 256 * c);
-      const double x0 = ld_x_scaled(reinterpret_cast<const float*>(&u.x));
-      const double x1 = ld_x_scaled(reinterpret_cast<const float*>(&u.y));
+      const bool f2f = c < PM_ROWDOT_F2F_PAIRS;
+      const double x0 = f2f ? double(__uint_as_float(u.x)) : ld_x_scaled(reinterpret_cast<const float*>(&u.x));
+      const double x1 = f2f ? double(__uint_as_float(u.y)) : ld_x_scaled(reinterpret_cast<const float*>(&u.y));
+      const double ww = f2f ? wr_u : wr;
       if (r % NS == 0) {
-        g[2 * c] = fma(wr, x0, g[2 * c]);
-        g[2 * c + 1] = fma(wr, x1, g[2 * c + 1]);
+        g[2 * c] = fma(ww, x0, g[2 * c]);
+        g[2 * c + 1] = fma(ww, x1, g[2 * c + 1]);
       } else {
-        ga[r % NS - 1][2 * c] = fma(wr, x0, ga[r % NS - 1][2 * c]);
-        ga[r % NS - 1][2 * c + 1] = fma(wr, x1, ga[r % NS - 1][2 * c + 1]);
+        ga[r % NS - 1][2 * c] = fma(ww, x0, ga[r % NS - 1][2 * c]);
+        ga[r % NS - 1][2 * c + 1] = fma(ww, x1, ga[r % NS - 1][2 * c + 1]);
+      }
+    }
+    if constexpr (!std::is_same<Mid, NoMid>::value) {
+      if (r == 15) {
+        double dh = 0.0;
+#pragma unroll
+        for (int j = 0; j < KC; ++j) dh += g[j];
+#pragma unroll
+        for (int s2 = 0; s2 + 1 < NS; ++s2)
+#pragma unroll
+          for (int j = 0; j < KC; ++j) dh += ga[s2][j];
+        mid(dh);
       }
     }
   }
@@ -496,7 +526,9 @@ __device__ __forceinline__ void consume_tile_rowdot(const float* xs, const doubl
   double dg = 0.0;
 #pragma unroll
   for (int j = 0; j < KC; ++j) dg += g[j];  // depends on every re-read word
-  mbar_arrive_after(empty, dg, lane, const_cast<float*>(xs));
+  // done_word: where the dependency word goes (default: the stage's first 128 bytes; the
+  // half-refilling form passes row 16, its first half being rewritten by then)
+  mbar_arrive_after(empty, dg, lane, done_word ? done_word : const_cast<float*>(xs));
 }
 
 // fp32-X row-dot consumer run by a PAIR of warps per tile (PAIRS == 4; KC == 4, K % 4 == 0,
@@ -663,7 +695,7 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
                                              int64_t tile_begin, int64_t tile_end, int64_t stride,
                                              int64_t row_limit, int S, const StreamSmem& sm,
                                              const double (&breg)[KC], double (&g)[KC], double& nll_acc,
-                                             bool evict_first, int U_arg = 1, bool selfprod = false) {
+                                             bool evict_first, int U_arg = 1, int selfprod = 0) {
   constexpr bool MULTI = PAIRS == 0 && NCW <= 8;
   const int U = MULTI ? U_arg : 1;
   const int warp = threadIdx.x >> 5;
@@ -688,8 +720,12 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
     // stage per warp a warp that finishes out of order waits behind the producer's head of
     // line) and no `empty` barrier: the refill starts the moment the stage is quiescent.
     if (selfprod) {
-      if (warp == 0) return;
-      const int cw = warp - 1;
+      // mode 3: the (now idle) producer warp consumes as well: NCW + 1 consumer warps
+      const bool all = selfprod == 3;
+      if (!all && warp == 0) return;
+      const int cw = all ? warp : warp - 1;
+      const int nact = all ? (S < NCW + 1 ? S : NCW + 1) : (S < NCW ? S : NCW);
+      const int Se = S - S % nact;
       if (cw >= nact) return;
       const int spw = Se / nact;  // stages per warp
       const uint64_t pol = l2_policy_evict_first();
@@ -1072,7 +1108,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   const int K = a.K;
   const int S = a.stages;
   const int U = a.tps;  // tiles per stage (> 1: contiguous tile range per CTA, one copy per unit)
-  const StreamSmem sm = carve_stream_smem(smem_raw, K, sizeof(XT), S, NCW, TR * U);
+  const int nw = (PAIRS == 3 && a.selfprod == 3) ? NCW + 1 : NCW;  // warps holding a partial
+  const StreamSmem sm = carve_stream_smem(smem_raw, K, sizeof(XT), S, nw, TR * U);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   // Thread 0 initialises the mbarriers; the CTA barrier follows at once, so the producer's
@@ -1112,10 +1149,10 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     stride = gridDim.x;
   }
   stream_tiles<XT, KC, GRAD, NCW, R, TR, PAIRS>(static_cast<const XT*>(a.X), a.y, K, tb, te, stride, a.n_rows, S, sm,
-                                                breg, g, nll, a.evict_first != 0, U, a.selfprod != 0);
+                                                breg, g, nll, a.evict_first != 0, U, a.selfprod);
   if constexpr (PAIRS == 4) __syncthreads();  // the pairs' exchange boxes share sm.wg: all tiles done first
-  if (warp > 0) {
-    const int cw = warp - 1;
+  if (warp > 0 || nw > NCW) {
+    const int cw = nw > NCW ? warp : warp - 1;
     const double wsum = warp_sum(nll);
     if (lane == 0) sm.wf[cw] = -wsum;
     if (GRAD) {
@@ -1126,7 +1163,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       }
     }
   }
-  cta_reduce_finalize<(NCW > 8 ? 3 : 5)>(a, sm, NCW, GRAD);
+  cta_reduce_finalize<(NCW > 8 ? 3 : 5)>(a, sm, nw, GRAD);
 }
 
 // Wide-K kernel (K > 256): one warp per row, lanes stride the columns, X read once from

@@ -78,7 +78,7 @@ static const char* const kTuneNames[] = {
     "f32_pairs",         // fp32-X consumer: 0 columns, 1 sub-tile pairs (default), 2 whole tile, 3 row-dot, 4 row-dot by warp pairs
     "f64_pairs",         // fp64 consumer: 0 columns, 1 pairs (default)
     "stream_ncw",        // fp32-X column consumer: 15 warps (default) or 7
-    "f32_selfprod",      // row-dot consumer: consumer warps issue their own bulk copies: 1 (default), 0
+    "f32_selfprod",      // row-dot consumer: 0 producer thread, 1 self-producing consumer warps, 3 (default) + warp 0 consumes
     "stream_tps",        // stream kernel 32-row tiles per stage / bulk copy (default: ~24 KB stages)
     "hb_rows",           // HB row-per-lane kernel: 0 off, 1 on (default)
     "hb_rows_ncw",       // 7 (default) or 15

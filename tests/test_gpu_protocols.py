@@ -35,7 +35,14 @@ def test_protocol_subset_against_oracle(gpu, family):
     (32, 700_001, "f64", {"stream_tps": 2}),       # ring reuse with 2-tile units, ragged tail
     (20, 300_000, "f64", {"glm_rows": 0}),         # narrow design through the column kernel
     (100, 300_000, "f64", {}),                     # pairs layout, ring reuse
-    (100, 300_000, "f32", {}),                     # fp32-X pairs
+    (100, 300_000, "f32", {}),                     # fp32-X row-dot consumer, 16 self-producing warps
+    (100, 300_000, "f32", {"f32_selfprod": 1}),    # ... 15 self-producing warps, warp 0 idle
+    (100, 300_000, "f32", {"f32_selfprod": 0}),    # ... with the producer thread
+    (100, 300_000, "f32", {"stream_ncw": 7}),      # ... 8 warps, two stages each
+    (100, 300_000, "f32", {"f32_pairs": 4}),       # row-dot by warp pairs (named barriers, count-2 release)
+    (100, 300_000, "f32", {"f32_pairs": 1}),       # sub-tile pairs consumer
+    (36, 150_001, "f32", {}),                      # row-dot, KC = 2, ragged tail
+    (124, 90_000, "f32", {}),                      # row-dot, one stage per warp
     (64, 200_000, "f32", {"stream_tps": 4}),       # fp32-X, 4-tile units
     (33, 150_000, "f32", {}),                      # fp32-X column consumer (odd K)
 ])

@@ -1,5 +1,5 @@
 # r02 pass J: row-dot consumer with self-producing consumer warps: parity + repeats + bench A/B
-O=gpurun_out/r02j
+O=gpurun_out/r02l
 mkdir -p $O
 cat > /tmp/rowdot3_check.py <<'PY'
 import sys, numpy as np
@@ -10,7 +10,7 @@ from paper_1310_1537_b200.glm import DesignMatrix, ExecPlan
 from paper_1310_1537_b200.sampler import GaussianPrior
 from paper_1310_1537_b200.synthetic import baseline_design
 for k, n in [(100, 40_001), (100, 1_000_003), (36, 9_999), (108, 5_000), (116, 33), (60, 200_000)]:
-    for knobs in ({"f32_pairs": 3, "stream_ncw": 15}, {"f32_pairs": 3}, {"f32_pairs": 3, "stream_ncw": 15, "f32_selfprod": 0}):
+    for knobs in ({"f32_pairs": 3, "stream_ncw": 15}, {"f32_pairs": 3}, {"f32_pairs": 3, "stream_ncw": 15, "f32_selfprod": 1}, {"f32_pairs": 3, "stream_ncw": 15, "f32_selfprod": 0}):
         with _lib.tuned(**knobs):
             x, y, _, betas = baseline_design(n, k, seed=k, n_eval=2)
             d = DesignMatrix(x, y); prior = GaussianPrior.isotropic(k, 0.0, 10.0)
@@ -30,8 +30,9 @@ for k, n in [(100, 40_001), (100, 1_000_003), (36, 9_999), (108, 5_000), (116, 3
 print("ok")
 PY
 timeout 900 python /tmp/rowdot3_check.py > $O/check.log 2>&1; echo "rowdot selfprod check rc=$?" > $O/summary.txt
-timeout 600 python bench.py --config c1f32 --no-cpu-baseline --steps 300 --tune f32_pairs=3 --tune stream_ncw=15 > $O/c1f32_rowdot15_self.log 2>&1
+timeout 600 python bench.py --config c1f32 --no-cpu-baseline --steps 300 --tune f32_pairs=3 --tune stream_ncw=15 > $O/c1f32_rowdot16_self3.log 2>&1
 timeout 600 python bench.py --config c1f32 --no-cpu-baseline --steps 300 --tune f32_pairs=3 --tune stream_ncw=15 --tune f32_selfprod=0 > $O/c1f32_rowdot15_prod.log 2>&1
-timeout 600 python bench.py --config c1f32 --no-cpu-baseline --steps 300 --tune f32_pairs=3 > $O/c1f32_rowdot7_self.log 2>&1
+timeout 600 python bench.py --config c1f32 --no-cpu-baseline --steps 300 --tune f32_pairs=3 --tune stream_ncw=15 --tune f32_selfprod=1 > $O/c1f32_rowdot15_self1.log 2>&1
 timeout 600 python bench.py --config c1f32 --no-cpu-baseline --steps 300 > $O/c1f32_pairs1.log 2>&1
 cat $O/summary.txt
+timeout 600 python bench.py --config c1f32 --no-cpu-baseline --steps 300 --tune f32_pairs=3 > $O/c1f32_rowdot8_self3.log 2>&1

@@ -35,6 +35,8 @@ def glm_cases():
     gen = np.random.default_rng(1)
     for k, n, xs, knobs in [(100, 4099, "f64", {}), (100, 4099, "f64", {"f64_pairs": 0}),
                             (100, 4099, "f32", {}), (100, 4099, "f32", {"f32_pairs": 0}),
+                            (100, 4099, "f32", {"f32_pairs": 1}), (100, 4099, "f32", {"f32_pairs": 4}),
+                            (100, 4099, "f32", {"f32_selfprod": 0}),
                             (64, 2049, "f32", {"f32_pairs": 2}), (20, 70_001, "f64", {"glm_rows": 1}),
                             (300, 1500, "f64", {}), (32, 100_000, "f64", {})]:
         with _lib.tuned(**knobs):
