@@ -1361,6 +1361,7 @@ cudaError_t launch_hb_rows_n(const pm_hb_s* h, const HbArgs& a, cudaStream_t st)
   r.stages = h->rows_stages;
   r.tps = h->rows_tps;
   r.contig = h->rows_contig;
+  r.selfprod = tune("hb_selfprod", 1) != 0 ? 1 : 0;
   r.fused = h->rows_fused;
   r.n_tiles = h->n_tiles;
   r.betas = a.betas;

@@ -247,6 +247,7 @@ struct HbRowsArgs {
   int G, K, stages, tps;
   int contig;            // 1: contiguous unit range per consumer warp; 0: round-robin
   int fused;             // 1: fold in the same launch (per-group tickets); 0: hb_fold_kernel
+  int selfprod;          // 1: every consumer warp issues the bulk copies of its own units (no producer thread)
   int64_t n_tiles;       // poff[G] / 32
   const double* betas;   // [G][K]
   double* part;          // [nseg][NCW][K+1]
@@ -429,7 +430,28 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a
   const int64_t q = n_units / nact;
   const int rr = int(n_units - q * nact);
   const int cw = warp - 1;
-  if (warp == 0) {
+  // this consumer warp's units (pure arithmetic on the arguments: no global loads, so a
+  // self-producing warp can start its first copies before the PDL wait)
+  const int64_t u_first = a.contig ? int64_t(cw) * q + (int64_t(cw) * rr) / nact : cw;
+  const int64_t n_w = a.contig ? int64_t(cw + 1) * q + (int64_t(cw + 1) * rr) / nact - u_first
+                               : q + (cw < rr ? 1 : 0);
+  const int64_t u_step = a.contig ? 1 : nact;
+  // Self-producing consumers (a.selfprod): warp w refills its own stages, unit m + spw into
+  // the stage unit m has just left -- no producer thread to serialise on (~100 ns per copy,
+  // 2 copies per 10 KB unit: ~44 us of one thread's time per config-3 launch) and no `empty`
+  // barriers.
+  auto issue_unit = [&](int64_t m, int s) {  // lane 0 of consumer warp cw
+    const int64_t tile = t0 + (u_first + m * u_step) * TPS;
+    const uint32_t nt = uint32_t(t1 - tile < TPS ? t1 - tile : TPS);
+    mbar_arrive_expect_tx(&sm.full[s], nt * (tile_bytes + 32 * sizeof(double)));
+    bulk_g2s(sm.xs + size_t(s) * stage_pitch, a.X + tile * int64_t(kTileRows) * K, nt * tile_bytes, &sm.full[s]);
+    bulk_g2s(sm.ys + size_t(s) * 32 * TPS, a.y + tile * kTileRows, nt * 32 * sizeof(double), &sm.full[s]);
+  };
+  if (a.selfprod && warp > 0 && cw < nact && lane == 0) {
+    for (int m = 0; m < spw; ++m)
+      if (m < n_w) issue_unit(m, cw + nact * m);
+  }
+  if (warp == 0 && !a.selfprod) {
     if (lane == 0) {
       // the single producer thread is on the critical path: no divisions and no dependent
       // global loads before its first copy (the per-warp first unit / count are rebuilt
@@ -511,10 +533,6 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a
       double* dst = slot(grp);
       for (int k = lane; k <= K; k += 32) dst[k] = 0.0;
     };
-    const int64_t u_first = a.contig ? int64_t(cw) * q + (int64_t(cw) * rr) / nact : cw;
-    const int64_t n_w = a.contig ? int64_t(cw + 1) * q + (int64_t(cw + 1) * rr) / nact - u_first
-                                 : q + (cw < rr ? 1 : 0);
-    const int64_t u_step = a.contig ? 1 : nact;
     if (n_w <= 0) {
       for (int grp = g_first; grp <= g_last; ++grp) zero_fill(grp);
     } else {
@@ -543,7 +561,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a
           consume_tile_rows<KMAX, GRAD>(xst + size_t(j) * kTileRows * K, yst + 32 * j, K, q0, lane, row0,
                                         row_limit, b, g, nll, dep);
         }
-        mbar_arrive_after(&sm.empty[s], dep, lane, const_cast<double*>(xst));
+        mbar_arrive_after(a.selfprod ? nullptr : &sm.empty[s], dep, lane, const_cast<double*>(xst));
+        if (a.selfprod && lane == 0 && m + spw < n_w) issue_unit(m + spw, s);  // the stage is quiescent
         s += nact;
         if (s >= nact * spw) {
           s = cw;

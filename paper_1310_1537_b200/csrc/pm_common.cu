@@ -85,6 +85,7 @@ static const char* const kTuneNames[] = {
     "hb_rows_tps",       // tiles per stage (default 2)
     "hb_rows_stages",    // stages (default: auto)
     "hb_contig",         // contiguous per-warp tile ranges: 1 (default)
+    "hb_selfprod",       // HB rows kernel: consumer warps issue their own bulk copies: 1 (default), 0 producer thread
     "hb_fused",          // fold fused into the rows launch: 0 (default)
     "hb_mapped_out",     // pm_hb_eval results: 0 device + one D2H copy (default), 1 mapped host stores
     "pdl",               // programmatic dependent launch: 1 (default)
