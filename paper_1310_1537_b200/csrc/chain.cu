@@ -47,7 +47,7 @@ struct ChainArgs {
   uint64_t key0, key1, pos0;
   double* beta;          // [K] in/out
   double* draws;         // [n_iter - n_burnin][K]
-  double* partials;      // [2][grid][kChainMaxM]
+  double* partials;      // [2][kChainMaxM][grid] (coalesced fold: every CTA reads all of a delta's partials)
   unsigned long long* out_pos;
   long long* out_evals;
   int* status;           // [0] = 0 ok / 1 widen / 2 shrink, [1] = coordinate
@@ -160,12 +160,12 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
     if (tid < M) {
       double s = 0.0;
       for (int w = 0; w < kChainThreads / 32; ++w) s += red[w][tid];
-      a.partials[(size_t(parity) * G + blockIdx.x) * kChainMaxM + tid] = s;
+      a.partials[(size_t(parity) * kChainMaxM + tid) * G + blockIdx.x] = s;  // [parity][m][cta]: the fold reads rows
     }
     grid.sync();
     // every CTA folds all CTA partials in the same fixed order: warp w folds delta m = w, w+8..
     for (int m = warp; m < M; m += kChainThreads / 32) {
-      const double p = warp_sum(fold_lane(a.partials + size_t(parity) * G * kChainMaxM + m, kChainMaxM, G, lane));
+      const double p = warp_sum(fold_lane(a.partials + (size_t(parity) * kChainMaxM + m) * G, 1, G, lane));
       if (lane == 0) tot_s[m] = -p;
     }
     __syncthreads();

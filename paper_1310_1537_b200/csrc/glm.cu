@@ -1373,7 +1373,8 @@ cudaError_t launch_hb_rows_n(const pm_hb_s* h, const HbArgs& a, cudaStream_t st)
   r.sigma = a.sigma;
   r.out_f = a.out_f;
   r.out_g = a.out_g;
-  e = launch_pdl(h->rows_pdl != 0, kern, dim3(h->rows_grid), dim3((NCW + 1) * 32), h->rows_smem, st, r);
+  if (HbRowsThreads<NCW>::all) r.selfprod = 1;  // no producer warp in that geometry
+  e = launch_pdl(h->rows_pdl != 0, kern, dim3(h->rows_grid), dim3(HbRowsThreads<NCW>::value), h->rows_smem, st, r);
   if (e != cudaSuccess || h->rows_fused) return e;
   return launch_pdl(h->rows_pdl != 0, hb_fold_kernel<GRAD>, dim3(h->G), dim3(64), 0, st, (const double*)h->part,
                     (const int*)h->gseg, int(NCW), h->K, a.betas, a.mu, a.sigma, a.out_f, a.out_g);
@@ -1381,6 +1382,7 @@ cudaError_t launch_hb_rows_n(const pm_hb_s* h, const HbArgs& a, cudaStream_t st)
 
 template <int KMAX, bool GRAD>
 cudaError_t launch_hb_rows(const pm_hb_s* h, const HbArgs& a, cudaStream_t st) {
+  if (h->rows_ncw == 8) return launch_hb_rows_n<KMAX, GRAD, 8>(h, a, st);
   return h->rows_ncw == 7 ? launch_hb_rows_n<KMAX, GRAD, 7>(h, a, st) : launch_hb_rows_n<KMAX, GRAD, 15>(h, a, st);
 }
 
@@ -1557,7 +1559,10 @@ int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64_t* off
     gseg[G] = nseg;
     // consumer warps (7 or 15), tiles per stage, stages (a multiple of the consumer count,
     // at least two per warp when they fit): tune hb_rows_ncw / _tps / _stages for A/B
-    const int ncw = tune("hb_rows_ncw", 7) == 15 ? 15 : 7;
+    // (8: every warp consumes and issues its own bulk copies -- the default; 7 / 15: + a
+    // producer warp, which idles under hb_selfprod=1)
+    const int t_ncw = tune("hb_rows_ncw", tune("hb_selfprod", 1) != 0 ? 8 : 7);
+    const int ncw = t_ncw == 15 ? 15 : (t_ncw == 8 ? 8 : 7);
     int tps = std::max(1, std::min(8, tune("hb_rows_tps", 2)));
     const int t_st = tune("hb_rows_stages", -1);
     const size_t cap = 200 * 1024;

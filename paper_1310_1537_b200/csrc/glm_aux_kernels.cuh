@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(256) diff_eval_kernel(DiffArgs a, DeltaPack dp
   if (threadIdx.x < M) {
     double s = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w][threadIdx.x];
-    a.partials[size_t(blockIdx.x) * kMaxDeltas + threadIdx.x] = s;
+    a.partials[size_t(threadIdx.x) * gridDim.x + blockIdx.x] = s;  // [m][cta]: coalesced fold
   }
   __syncthreads();
   if (threadIdx.x == 0) {  // one acq_rel ticket publishes / acquires the CTA partials (see K1)
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256) diff_eval_kernel(DiffArgs a, DeltaPack dp
   // warp w folds delta m = w, w + 8, ...: lane-strided CTA partials (loads in flight
   // together), then the fixed butterfly -- the order does not depend on M
   for (int m = warp; m < M; m += blockDim.x >> 5) {
-    const double s = warp_sum(fold_lane(a.partials + m, kMaxDeltas, gridDim.x, lane));
+    const double s = warp_sum(fold_lane(a.partials + size_t(m) * gridDim.x, 1, gridDim.x, lane));
     if (lane == 0) a.out[m] = -s;
   }
   if (threadIdx.x == 0) *a.counter = 0u;
@@ -396,8 +396,16 @@ __device__ __forceinline__ int group_of_tile_in(const int64_t* poff, int lo, int
   return lo;
 }
 
+// NCW odd (7, 15): warp 0 is the producer (or idle when the consumers produce for themselves);
+// NCW even (8): every warp of the CTA consumes and produces for itself (a.selfprod required).
+template <int NCW>
+struct HbRowsThreads {
+  static constexpr bool all = NCW % 2 == 0;
+  static constexpr int value = (all ? NCW : NCW + 1) * 32;
+};
 template <int KMAX, bool GRAD, int NCW>
-__global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a) {
+__global__ void __launch_bounds__(HbRowsThreads<NCW>::value, 1) hb_rows_kernel(HbRowsArgs a) {
+  constexpr bool ALL = HbRowsThreads<NCW>::all;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int K = a.K;
   const int S = a.stages;
@@ -429,7 +437,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a
   // costs a partial flush and a beta reload); a.contig = 0: round-robin, unit w + m*nact.
   const int64_t q = n_units / nact;
   const int rr = int(n_units - q * nact);
-  const int cw = warp - 1;
+  const int cw = ALL ? warp : warp - 1;
   // this consumer warp's units (pure arithmetic on the arguments: no global loads, so a
   // self-producing warp can start its first copies before the PDL wait)
   const int64_t u_first = a.contig ? int64_t(cw) * q + (int64_t(cw) * rr) / nact : cw;
@@ -447,11 +455,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a
     bulk_g2s(sm.xs + size_t(s) * stage_pitch, a.X + tile * int64_t(kTileRows) * K, nt * tile_bytes, &sm.full[s]);
     bulk_g2s(sm.ys + size_t(s) * 32 * TPS, a.y + tile * kTileRows, nt * 32 * sizeof(double), &sm.full[s]);
   };
-  if (a.selfprod && warp > 0 && cw < nact && lane == 0) {
+  if (a.selfprod && (ALL || warp > 0) && cw < nact && lane == 0) {
     for (int m = 0; m < spw; ++m)
       if (m < n_w) issue_unit(m, cw + nact * m);
   }
-  if (warp == 0 && !a.selfprod) {
+  if (!ALL && warp == 0 && !a.selfprod) {
     if (lane == 0) {
       // the single producer thread is on the critical path: no divisions and no dependent
       // global loads before its first copy (the per-warp first unit / count are rebuilt
@@ -500,12 +508,12 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) hb_rows_kernel(HbRowsArgs a
   // PDL: the copies above only read X and y (never written by a kernel); the consumers and
   // the fold below read beta and write the partials / tickets the previous launch uses
   if (threadIdx.x == 0) pdl_trigger();
-  if (warp > 0) pdl_wait();
+  if (ALL || warp > 0) pdl_wait();
   // the CTA's groups and segments (host-computed; loaded after the producer started)
   const int g_first = a.cta_g0[c];
   const int seg0 = a.seg_base[c];
   const int g_last = g_first + (a.seg_base[c + 1] - seg0) - 1;
-  if (warp > 0 && cw < nact) {
+  if ((ALL || warp > 0) && cw < nact) {
     double* b = sm.wg + size_t(cw) * K;
     double g[KMAX];
     double nll = 0.0;

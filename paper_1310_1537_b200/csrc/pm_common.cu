@@ -81,7 +81,7 @@ static const char* const kTuneNames[] = {
     "f32_selfprod",      // row-dot consumer: 0 producer thread, 1 self-producing consumer warps, 3 (default) + warp 0 consumes
     "stream_tps",        // stream kernel 32-row tiles per stage / bulk copy (default: ~24 KB stages)
     "hb_rows",           // HB row-per-lane kernel: 0 off, 1 on (default)
-    "hb_rows_ncw",       // 7 (default) or 15
+    "hb_rows_ncw",       // 8 (default: all warps consume, self-producing), 7 or 15 (+ a producer warp)
     "hb_rows_tps",       // tiles per stage (default 2)
     "hb_rows_stages",    // stages (default: auto)
     "hb_contig",         // contiguous per-warp tile ranges: 1 (default)
