@@ -141,8 +141,8 @@ def issue_roofline(config: str, ms_per_sweep: float, clk: dict):
     achieved = 2 * n / (ms_per_sweep * 1e-3)
     peak = 148 * 4 * clk["sm_mhz"] * 1e6
     return {"achieved": achieved, "peak": peak, "unit": "warp instructions/s", "frac": achieved / peak,
-            "source": "ncu smsp__inst_executed.sum per half-sweep (profiles/r01_ncu_gibbs_%s_raw.csv)"
-            % ("packed" if config == "c4" else "potts")}
+            "source": "ncu smsp__inst_executed.sum per half-sweep (%s)"
+            % ("profiles/r02_ncu_ising_raw.csv" if config == "c4" else "profiles/r01_ncu_gibbs_potts_raw.csv")}
 
 
 # ---------------------------------------------------------------------------- clocks

@@ -47,6 +47,7 @@ struct ChainArgs {
   uint64_t key0, key1, pos0;
   double* beta;          // [K] in/out
   double* draws;         // [n_iter - n_burnin][K]
+  unsigned long long* bar;  // grid barrier arrival count (zero at launch); null: cg grid sync
   double* partials;      // [2][kChainMaxM][grid] (coalesced fold: every CTA reads all of a delta's partials)
   unsigned long long* out_pos;
   long long* out_evals;
@@ -77,6 +78,7 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
   __shared__ uint64_t ubase_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x;
+  unsigned long long bar_target = 0;  // thread 0: arrivals expected after this CTA's next barrier
   for (int k = tid; k < a.K; k += blockDim.x) sbeta[k] = a.beta[k];
   if (tid == 0) ubase_s = ~0ull;
   __syncthreads();
@@ -162,7 +164,25 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ChainArgs a) {
       for (int w = 0; w < kChainThreads / 32; ++w) s += red[w][tid];
       a.partials[(size_t(parity) * kChainMaxM + tid) * G + blockIdx.x] = s;  // [parity][m][cta]: the fold reads rows
     }
-    grid.sync();
+    // grid-wide barrier (the launch is cooperative: all CTAs are resident).  One release
+    // add by thread 0 after the CTA barrier publishes this CTA's partials (PTX fences are
+    // cumulative over writes ordered before them by bar.sync); the acquire spin on the
+    // monotonic arrival count orders every other CTA's before the fold's loads.  Replaces
+    // cg::grid_group::sync (two extra fences and CTA barriers per pass).
+    if (a.bar) {
+      __syncthreads();
+      if (tid == 0) {
+        bar_target += G;
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.bar) : "memory");
+        unsigned long long seen;
+        do {
+          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(seen) : "l"(a.bar) : "memory");
+        } while (seen < bar_target);
+      }
+      __syncthreads();
+    } else {
+      grid.sync();
+    }
     // every CTA folds all CTA partials in the same fixed order: warp w folds delta m = w, w+8..
     for (int m = warp; m < M; m += kChainThreads / 32) {
       const double p = warp_sum(fold_lane(a.partials + (size_t(parity) * kChainMaxM + m) * G, 1, G, lane));
@@ -407,6 +427,8 @@ int pm_ws_run_chain(pm_ws_t ws, const double* mu, const double* sigma, int32_t n
   a.beta = d_beta;
   a.draws = d_draws;
   a.partials = d_part;
+  a.bar = tune("chain_own_barrier", 0) != 0 ? d_pos + 4 : nullptr;  // inside the 64 trailing bytes
+  PM_CUDA(cudaMemsetAsync(d_pos + 4, 0, sizeof(unsigned long long), st));
   a.out_pos = d_pos;
   a.out_evals = d_evals;
   a.status = d_status;

@@ -91,6 +91,7 @@ static const char* const kTuneNames[] = {
     "pdl",               // programmatic dependent launch: 1 (default)
     "chain_unroll",      // chain kernel rows per ILP batch (default 2)
     "chain_blocks_per_sm",  // chain kernel CTAs per SM (default 2)
+    "chain_own_barrier", // chain kernel grid barrier: 0 cg grid sync (default), 1 own release/acquire counter (measured equal)
     "chain_spec",        // speculative shrink candidates (default 4)
     "hbs_spec",          // hb_sweep speculation (default 1)
     "hbs_minb",          // hb_sweep CTAs per SM register budget (default 8)
