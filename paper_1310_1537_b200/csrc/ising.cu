@@ -280,7 +280,13 @@ __device__ inline void lat_xchg_publish(const PackedArgs& a);
 // rows and stages the other colour's rows above / below / inside (+ 16 edge bytes either
 // side) in shared memory once, so every row is read from L2 (blockDim.y + 2) / blockDim.y
 // times instead of 3 -- the north-star's neighbour-sum staging.
-template <int MODEL, bool T32, int NG, bool XCHG, bool STAGE = false>
+template <int MODEL, bool T32, int NG, int RPT>
+__device__ __forceinline__ void gibbs_packed_rows(const PackedArgs& a, const GibbsTables<MODEL, T32>& tb, int r0,
+                                                  int q0);
+
+// RPT: consecutive rows per thread (gibbs_packed_rows; 1 = one row per thread, the only form
+// of the peer-exchanging and staged kernels)
+template <int MODEL, bool T32, int NG, bool XCHG, bool STAGE = false, int RPT = 1>
 __global__ void __launch_bounds__(256, NG == 1 ? 6 : MODEL == PM_MODEL_ISING ? PM_GIBBS_MINB_ISING : PM_GIBBS_MINB_POTTS)
     gibbs_packed_kernel(PackedArgs a, const unsigned long long* __restrict__ pthr, const uint32_t* __restrict__ pcomp) {
   __shared__ GibbsTables<MODEL, T32> tb;
@@ -334,60 +340,27 @@ __global__ void __launch_bounds__(256, NG == 1 ? 6 : MODEL == PM_MODEL_ISING ? P
       __syncthreads();
     }
   } else if (cgrp < per_row) {
-    for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < a.rows; r += gridDim.y * blockDim.y) {
-      gibbs_packed_row<MODEL, T32, NG, XCHG>(a, tb, r, cgrp * 16 * NG);
+    if constexpr (RPT > 1 && !XCHG) {
+      for (int rg = blockIdx.y * blockDim.y + threadIdx.y; rg * RPT < a.rows; rg += gridDim.y * blockDim.y)
+        gibbs_packed_rows<MODEL, T32, NG, RPT>(a, tb, rg * RPT, cgrp * 16 * NG);
+    } else {
+      for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < a.rows; r += gridDim.y * blockDim.y) {
+        gibbs_packed_row<MODEL, T32, NG, XCHG>(a, tb, r, cgrp * 16 * NG);
+      }
     }
   }
   if constexpr (XCHG) lat_xchg_publish(a);
 }
 
-template <int MODEL, bool T32, int NG, bool XCHG>
-__device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const GibbsTables<MODEL, T32>& tb, int r,
-                                                 int q0, const int8_t* sm, int pitch) {
-  constexpr int NW = 4 * NG;   // 32-bit words (4 sites each) handled by this thread
-  const int li = r + a.halo;   // array row
-  const int i = a.row0 + r;    // global row: colour parity and RNG site index
-  const int iu = a.halo ? li - 1 : (li == 0 ? a.rows - 1 : li - 1);
-  const int id = a.halo ? li + 1 : (li == a.rows - 1 ? 0 : li + 1);
-  const int8_t* orow = a.other + int64_t(li) * a.W2;
-  const int8_t* urow = a.other + int64_t(iu) * a.W2;
-  const int8_t* drow = a.other + int64_t(id) * a.W2;
-  if constexpr (XCHG) {  // halo rows of the other colour from the mailbox, once the neighbours delivered
-    const int oc = a.colour ^ 1;
-    const unsigned long long* fl = reinterpret_cast<const unsigned long long*>(a.xmb + lat_xchg_flags(a.W2));
-    if (r == 0) {
-      lat_wait_flag(fl + oc * 2 + 0, a.kread, a.status);
-      urow = a.xmb + lat_xchg_halo(a.rpar, oc, 0, a.W2);
-    }
-    if (r == a.rows - 1) {
-      lat_wait_flag(fl + oc * 2 + 1, a.kread, a.status);
-      drow = a.xmb + lat_xchg_halo(a.rpar, oc, 1, a.W2);
-    }
-  }
-  uint32_t U[NW], D[NW], M[NW];
-#pragma unroll
-  for (int g = 0; g < NG; ++g) {
-    uint4 u4, d4, m4;
-    if (sm) {
-      u4 = *reinterpret_cast<const uint4*>(sm - pitch + 16 * g);
-      d4 = *reinterpret_cast<const uint4*>(sm + pitch + 16 * g);
-      m4 = *reinterpret_cast<const uint4*>(sm + 16 * g);
-    } else {
-      u4 = ld16(urow + q0 + 16 * g), d4 = ld16(drow + q0 + 16 * g), m4 = ld16(orow + q0 + 16 * g);
-    }
-    U[4 * g] = u4.x, U[4 * g + 1] = u4.y, U[4 * g + 2] = u4.z, U[4 * g + 3] = u4.w;
-    D[4 * g] = d4.x, D[4 * g + 1] = d4.y, D[4 * g + 2] = d4.z, D[4 * g + 3] = d4.w;
-    M[4 * g] = m4.x, M[4 * g + 1] = m4.y, M[4 * g + 2] = m4.z, M[4 * g + 3] = m4.w;
-  }
-  // o = 0: horizontal neighbours of packed site q are q-1 and q; o = 1: q and q+1
-  const int o = (i + a.colour) & 1;
-  const int qe = o ? ((q0 + 16 * NG == a.W2) ? 0 : q0 + 16 * NG) : ((q0 == 0) ? a.W2 - 1 : q0 - 1);
-  const uint32_t edge = sm ? uint32_t(uint8_t(o ? sm[16 * NG] : sm[-1])) : uint32_t(uint8_t(__ldg(orow + qe)));
-  // Philox block of the first word.  The packed path only runs on lattices with fewer than
-  // 2^34 - 256 sites (packed_blocks_fit), so every block index of the half-sweep fits 32 bits:
-  // the counter's high word is 0 and g0 + m is a 32-bit add (no carry chain per word)
-  const uint32_t g0 = uint32_t((uint64_t(a.colour) * uint64_t(a.n0) + uint64_t(i) * a.W2 + q0) >> 2);
-  uint32_t res[NW];
+// New packed words of one row chunk: U / D / M = the other colour's rows above / below / at the
+// row, `edge` the one byte beyond the chunk on the side given by o, g0 the chunk's first
+// Philox block.
+template <int MODEL, bool T32, int NG>
+__device__ __forceinline__ void gibbs_packed_words(const PackedArgs& a, const GibbsTables<MODEL, T32>& tb,
+                                                   const uint32_t (&U)[4 * NG], const uint32_t (&D)[4 * NG],
+                                                   const uint32_t (&M)[4 * NG], uint32_t edge, int o, uint32_t g0,
+                                                   uint32_t (&res)[4 * NG]) {
+  constexpr int NW = 4 * NG;
 #pragma unroll
   for (int m = 0; m < NW; ++m) {
     const uint32_t cur = M[m];
@@ -445,6 +418,107 @@ __device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const Gibb
     }
     res[m] = out;
   }
+}
+
+// RPT consecutive rows of one column group per thread (whole lattices and NCCL-exchanged
+// strips; the peer-exchanging and staged forms keep one row per thread): row r + 1's rows
+// above / at are row r's rows at / below, so each further row costs ONE new 16-byte load per
+// group instead of three, and the per-thread set-up (parameters, addresses, table base) is
+// paid once per RPT rows.
+template <int MODEL, bool T32, int NG, int RPT>
+__device__ __forceinline__ void gibbs_packed_rows(const PackedArgs& a, const GibbsTables<MODEL, T32>& tb, int r0,
+                                                  int q0) {
+  constexpr int NW = 4 * NG;
+  auto load_row = [&](int arow, uint32_t (&w)[NW]) {
+    const int8_t* p = a.other + int64_t(arow) * a.W2 + q0;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const uint4 v = ld16(p + 16 * g);
+      w[4 * g] = v.x, w[4 * g + 1] = v.y, w[4 * g + 2] = v.z, w[4 * g + 3] = v.w;
+    }
+  };
+  const int li0 = r0 + a.halo;
+  const int iu0 = a.halo ? li0 - 1 : (li0 == 0 ? a.rows - 1 : li0 - 1);
+  uint32_t U[NW], M[NW], D[NW];
+  load_row(iu0, U);
+  load_row(li0, M);
+  // not unrolled: a fully unrolled RPT = 4 body needs more than the 64 (Ising) / 80 (Potts)
+  // registers of the occupancy these kernels run at (152 / 296 bytes of spills); rolled, the
+  // window advances by 2 x NW register moves per row
+#pragma unroll 1
+  for (int j = 0; j < RPT; ++j) {
+    const int r = r0 + j;
+    if (r >= a.rows) break;
+    const int li = r + a.halo;
+    const int i = a.row0 + r;
+    const int id = a.halo ? li + 1 : (li == a.rows - 1 ? 0 : li + 1);
+    load_row(id, D);
+    const int o = (i + a.colour) & 1;
+    const int qe = o ? ((q0 + 16 * NG == a.W2) ? 0 : q0 + 16 * NG) : ((q0 == 0) ? a.W2 - 1 : q0 - 1);
+    const uint32_t edge = uint32_t(uint8_t(__ldg(a.other + int64_t(li) * a.W2 + qe)));
+    const uint32_t g0 = uint32_t((uint64_t(a.colour) * uint64_t(a.n0) + uint64_t(i) * a.W2 + q0) >> 2);
+    uint32_t res[NW];
+    gibbs_packed_words<MODEL, T32, NG>(a, tb, U, D, M, edge, o, g0, res);
+#pragma unroll
+    for (int g = 0; g < NG; ++g)
+      *reinterpret_cast<uint4*>(a.mine + int64_t(li) * a.W2 + q0 + 16 * g) =
+          make_uint4(res[4 * g], res[4 * g + 1], res[4 * g + 2], res[4 * g + 3]);
+#pragma unroll
+    for (int m = 0; m < NW; ++m) {  // next row: above = this row, at = the row below
+      U[m] = M[m];
+      M[m] = D[m];
+    }
+  }
+}
+
+template <int MODEL, bool T32, int NG, bool XCHG>
+__device__ __forceinline__ void gibbs_packed_row(const PackedArgs& a, const GibbsTables<MODEL, T32>& tb, int r,
+                                                 int q0, const int8_t* sm, int pitch) {
+  constexpr int NW = 4 * NG;   // 32-bit words (4 sites each) handled by this thread
+  const int li = r + a.halo;   // array row
+  const int i = a.row0 + r;    // global row: colour parity and RNG site index
+  const int iu = a.halo ? li - 1 : (li == 0 ? a.rows - 1 : li - 1);
+  const int id = a.halo ? li + 1 : (li == a.rows - 1 ? 0 : li + 1);
+  const int8_t* orow = a.other + int64_t(li) * a.W2;
+  const int8_t* urow = a.other + int64_t(iu) * a.W2;
+  const int8_t* drow = a.other + int64_t(id) * a.W2;
+  if constexpr (XCHG) {  // halo rows of the other colour from the mailbox, once the neighbours delivered
+    const int oc = a.colour ^ 1;
+    const unsigned long long* fl = reinterpret_cast<const unsigned long long*>(a.xmb + lat_xchg_flags(a.W2));
+    if (r == 0) {
+      lat_wait_flag(fl + oc * 2 + 0, a.kread, a.status);
+      urow = a.xmb + lat_xchg_halo(a.rpar, oc, 0, a.W2);
+    }
+    if (r == a.rows - 1) {
+      lat_wait_flag(fl + oc * 2 + 1, a.kread, a.status);
+      drow = a.xmb + lat_xchg_halo(a.rpar, oc, 1, a.W2);
+    }
+  }
+  uint32_t U[NW], D[NW], M[NW];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    uint4 u4, d4, m4;
+    if (sm) {
+      u4 = *reinterpret_cast<const uint4*>(sm - pitch + 16 * g);
+      d4 = *reinterpret_cast<const uint4*>(sm + pitch + 16 * g);
+      m4 = *reinterpret_cast<const uint4*>(sm + 16 * g);
+    } else {
+      u4 = ld16(urow + q0 + 16 * g), d4 = ld16(drow + q0 + 16 * g), m4 = ld16(orow + q0 + 16 * g);
+    }
+    U[4 * g] = u4.x, U[4 * g + 1] = u4.y, U[4 * g + 2] = u4.z, U[4 * g + 3] = u4.w;
+    D[4 * g] = d4.x, D[4 * g + 1] = d4.y, D[4 * g + 2] = d4.z, D[4 * g + 3] = d4.w;
+    M[4 * g] = m4.x, M[4 * g + 1] = m4.y, M[4 * g + 2] = m4.z, M[4 * g + 3] = m4.w;
+  }
+  // o = 0: horizontal neighbours of packed site q are q-1 and q; o = 1: q and q+1
+  const int o = (i + a.colour) & 1;
+  const int qe = o ? ((q0 + 16 * NG == a.W2) ? 0 : q0 + 16 * NG) : ((q0 == 0) ? a.W2 - 1 : q0 - 1);
+  const uint32_t edge = sm ? uint32_t(uint8_t(o ? sm[16 * NG] : sm[-1])) : uint32_t(uint8_t(__ldg(orow + qe)));
+  // Philox block of the first word.  The packed path only runs on lattices with fewer than
+  // 2^34 - 256 sites (packed_blocks_fit), so every block index of the half-sweep fits 32 bits:
+  // the counter's high word is 0 and g0 + m is a 32-bit add (no carry chain per word)
+  const uint32_t g0 = uint32_t((uint64_t(a.colour) * uint64_t(a.n0) + uint64_t(i) * a.W2 + q0) >> 2);
+  uint32_t res[NW];
+  gibbs_packed_words<MODEL, T32, NG>(a, tb, U, D, M, edge, o, g0, res);
 #pragma unroll
   for (int g = 0; g < NG; ++g)
     *reinterpret_cast<uint4*>(a.mine + int64_t(li) * a.W2 + q0 + 16 * g) =
@@ -956,11 +1030,20 @@ static cudaError_t launch_packed(pm_lat_s* h, int c, uint64_t sweep, uint64_t se
                            st, pa, (const unsigned long long*)h->pthr, (const uint32_t*)h->pthr32);
     return e;
   }
+  // rows per thread without the in-kernel exchange (tune gibbs_rpt = 1 | 2 | 4; default 1: measured no gain, profiles/r02_ab_gibbs_rpt.txt):
+  // the grid's y extent shrinks accordingly
+  const int t_rpt = tune("gibbs_rpt", 1);
+  const int rpt = pa.xmb ? 1 : (t_rpt >= 4 ? 4 : (t_rpt >= 2 ? 2 : 1));
+  const dim3 grid_r(grid.x, std::min(((h->H + rpt - 1) / rpt + by - 1) / by, 65535));
 #define PM_LAUNCH_PACKED(M, T, N)                                                                      \
   e = pa.xmb ? launch_pdl(h->pdl, gibbs_packed_kernel<M, T, N, true>, grid, block, 0, st, pa,          \
                           (const unsigned long long*)h->pthr, (const uint32_t*)h->pthr32)                 \
-             : launch_pdl(h->pdl, gibbs_packed_kernel<M, T, N, false>, grid, block, 0, st, pa,         \
-                          (const unsigned long long*)h->pthr, (const uint32_t*)h->pthr32)
+      : rpt == 4 ? launch_pdl(h->pdl, gibbs_packed_kernel<M, T, N, false, false, 4>, grid_r, block, 0, st, pa, \
+                              (const unsigned long long*)h->pthr, (const uint32_t*)h->pthr32)             \
+      : rpt == 2 ? launch_pdl(h->pdl, gibbs_packed_kernel<M, T, N, false, false, 2>, grid_r, block, 0, st, pa, \
+                              (const unsigned long long*)h->pthr, (const uint32_t*)h->pthr32)             \
+                 : launch_pdl(h->pdl, gibbs_packed_kernel<M, T, N, false>, grid, block, 0, st, pa,     \
+                              (const unsigned long long*)h->pthr, (const uint32_t*)h->pthr32)
 #define PM_LAUNCH_NG(M, T)            \
   do {                                \
     if (ng == 4)                      \

@@ -96,6 +96,7 @@ static const char* const kTuneNames[] = {
     "hbs_spec",          // hb_sweep speculation (default 1)
     "hbs_minb",          // hb_sweep CTAs per SM register budget (default 8)
     "gibbs_ng",          // packed Gibbs 16-site groups per thread: 1, 2, 4 (default: per model)
+    "gibbs_rpt",         // packed Gibbs: consecutive rows per thread 1 (default) | 2 | 4 (A/B: register-level neighbour reuse, no gain)
     "gibbs_smem",        // packed Gibbs: 1 = stage the neighbour rows in shared memory (A/B; default 0)
 };
 
