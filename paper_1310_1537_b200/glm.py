@@ -326,15 +326,15 @@ def _prior_arrays(prior, n_cols: int):
     return mu, sigma
 
 
-def _account(plan: ExecPlan, calls: int = 1) -> None:
+def _account(plan: ExecPlan, calls: int = 1, launches: int = 0, partials: int = 0) -> None:
     """The reference's region / merge accounting for `calls` evaluations under `plan`
     (instrumentation contract, read by its tests: SOM opens two regions -- the matvec and
     the transcendental pass, glm.py:277-295 / 375-396 -- every other strategy one, and the
-    merge folds one partial per worker, glm.py:234-250).  The device work is counted
-    separately (kernel_launches, device_partials)."""
+    merge folds one partial per worker, glm.py:234-250), plus the device work of the call
+    (kernel launches, partials folded on the device) -- one counter update in all."""
     regions = 2 if plan.strategy is Strategy.SOM else 1
-    counters.add_region(regions * calls)
-    counters.add_merges(plan.workers * calls)
+    counters.account(parallel_regions=regions * calls, merge_events=plan.workers * calls,
+                     kernel_launches=launches, device_partials=partials)
 
 
 def _evaluate(data, beta, plan: ExecPlan, prior, want_grad: bool) -> GradResult:
@@ -346,9 +346,7 @@ def _evaluate(data, beta, plan: ExecPlan, prior, want_grad: bool) -> GradResult:
     with dev.lock:
         dev.set_prior(mu, sigma)
         f, g = dev.eval(beta, mu is not None, want_grad)
-    _account(plan)
-    counters.add_launches(1)
-    counters.add_device_partials(dev.grid)
+    _account(plan, launches=1, partials=dev.grid)
     return GradResult(f, g)
 
 
@@ -377,9 +375,7 @@ def _evaluate_sharded(view: ShardedMatrix, beta, plan: ExecPlan, mu, sigma, want
     finally:
         for d in devs:
             d.lock.release()
-    _account(plan)
-    counters.add_launches(len(devs))
-    counters.add_device_partials(len(devs))
+    _account(plan, launches=len(devs), partials=len(devs))
     return GradResult(f, g)
 
 
@@ -504,12 +500,11 @@ def diff_loglike_multi(ws: GlmWorkspace, data: DesignMatrix, k: int, deltas,
         raise ValueError("delta_beta_k must be finite")
     if data.n_rows != ws.n_rows or data.n_cols != ws.n_cols:
         raise ValueError("workspace/data shape mismatch")
-    counters.add_flops(ws.n_rows * _DIFF_FLOPS * d.size)
     out = np.empty(d.size)
     _lib.call("pm_ws_diff_eval", ws._ws, int(k), _lib.dptr(d), int(d.size), _lib.dptr(out))
-    counters.add_region(d.size)  # glm.py:520-522: one PLF region and one merge per worker per call
-    counters.add_merges(plan.workers * d.size)
-    counters.add_launches(1)
+    # glm.py:520-522: 8N flops, one PLF region and one merge per worker per evaluated delta
+    counters.account(flops=ws.n_rows * _DIFF_FLOPS * d.size, parallel_regions=d.size,
+                     merge_events=plan.workers * d.size, kernel_launches=1)
     return out
 
 
