@@ -100,7 +100,10 @@ PM_API int pm_glm_eval(pm_glm_t h, const double* beta, int with_prior, int want_
 
 /* Split form of pm_glm_eval for several handles in flight (the reference's
  * SHARDED strategy, glm.py:439-454, one shard per device): _launch enqueues the
- * kernel on the handle's stream, _wait synchronises and returns the result.
+ * kernel on the handle's stream, _wait returns the result as soon as the kernel's
+ * finishing CTA has published it (it polls a completion word the kernel stores, system
+ * scope, after (f, g) in mapped host memory; the stream itself drains a few microseconds
+ * later and every later call on the handle is ordered after it).
  * One evaluation may be in flight per handle: _launch returns PM_ESTATE until the
  * matching _wait.  pm_glm_eval holds the handle's mutex across both halves, so
  * threads sharing one handle each get their own (f, g). */

@@ -74,7 +74,8 @@ struct pm_glm_s {
   double* partials = nullptr;
   int partials_cap = 0;
   unsigned int* counter = nullptr;
-  double* out_host = nullptr;   // mapped pinned [K+1]
+  double* out_host = nullptr;   // mapped pinned [K+2]: (f, g[K]) and the completion word
+  unsigned long long seq = 0;   // evaluations launched through pm_glm_launch / pm_glm_eval
   double* out_dev = nullptr;    // device alias of out_host
   double* beta_dev = nullptr;   // [K] (wide kernel)
   double* beta_pinned = nullptr;
@@ -481,6 +482,8 @@ GlmArgs make_args(pm_glm_s* h, bool with_prior, double* out) {
   a.xepoch = 0;
   for (int p = 0; p < kMaxXchgRanks; ++p) a.xpeer[p] = nullptr;
   a.xstatus = nullptr;
+  a.done = nullptr;
+  a.done_seq = 0;
 #ifdef PM_AB_PHASES
   static unsigned long long* stamps = nullptr;
   if (!stamps) {
@@ -507,8 +510,12 @@ struct XchgLaunch {  // peer exchange fields of one evaluation (pm_glm_eval_xchg
 };
 
 int enqueue_eval(pm_glm_s* h, const double* beta, bool with_prior, bool grad, double* out, cudaStream_t st,
-                 const XchgLaunch* xl = nullptr) {
+                 const XchgLaunch* xl = nullptr, unsigned long long done_seq = 0) {
   GlmArgs a = make_args(h, with_prior, out);
+  if (done_seq) {  // results go to the handle's mapped buffer: completion word right after them
+    a.done = reinterpret_cast<unsigned long long*>(h->out_dev + h->K + 1);
+    a.done_seq = done_seq;
+  }
   if (xl) {
     a.xw = xl->world;
     a.xrank = xl->rank;
@@ -656,7 +663,9 @@ int pm_glm_upload(pm_glm_t h, const void* X, int x_dtype, const double* y, int64
   h->partials_cap = std::max(std::max(h->grid, 1), 2 * h->sms);  // the fp32 wide fallback uses 2 x SMs
   PM_CUDA(cudaMalloc(&h->partials, sizeof(double) * size_t(h->partials_cap) * (n_cols + 1)));
   PM_CUDA(cudaMalloc(&h->beta_dev, sizeof(double) * (n_cols + 1)));  // +1: PM_AB_OUT_DEVICE scratch
-  PM_CUDA(cudaHostAlloc(&h->out_host, sizeof(double) * (n_cols + 1), cudaHostAllocMapped | cudaHostAllocPortable));
+  PM_CUDA(cudaHostAlloc(&h->out_host, sizeof(double) * (n_cols + 2), cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(h->out_host, 0, sizeof(double) * (n_cols + 2));
+  h->seq = 0;
   PM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->out_dev), h->out_host, 0));
   PM_CUDA(cudaHostAlloc(&h->beta_pinned, sizeof(double) * n_cols, cudaHostAllocPortable));
   return PM_OK;
@@ -698,7 +707,7 @@ int glm_launch_locked(pm_glm_s* h, const double* beta, int with_prior, int want_
   int rc = check_beta(h, beta);
   if (rc) return rc;
   DeviceGuard g(h->device);
-  rc = enqueue_eval(h, beta, with_prior != 0, want_grad != 0, h->out_dev, h->stream);
+  rc = enqueue_eval(h, beta, with_prior != 0, want_grad != 0, h->out_dev, h->stream, nullptr, ++h->seq);
   if (rc) return rc;
   h->launched = true;
   h->last_want_grad = want_grad;
@@ -709,7 +718,24 @@ int glm_wait_locked(pm_glm_s* h, double* f_out, double* g_out) {
   if (!h->launched) return fail(PM_ESTATE, "pm_glm_wait without a launch");
   DeviceGuard g(h->device);
   h->launched = false;
-  PM_CUDA(cudaStreamSynchronize(h->stream));
+  // The finishing CTA stores (f, g), then the launch's sequence number (system-scope release)
+  // into the mapped buffer: poll that word instead of cudaStreamSynchronize -- the results
+  // are readable a few microseconds before the driver reports the stream idle (kernel
+  // teardown + completion processing).  The stream is queried now and then so that a failed
+  // launch ends the wait; tune glm_poll=0 restores the synchronise.
+  bool seen = false;
+  if (tune("glm_poll", 1) != 0) {
+    volatile unsigned long long* word = reinterpret_cast<volatile unsigned long long*>(h->out_host + h->K + 1);
+    for (unsigned spins = 1;; ++spins) {
+      if (*word == h->seq) {
+        seen = true;
+        break;
+      }
+      if ((spins & 0x3ff) == 0 && cudaStreamQuery(h->stream) != cudaErrorNotReady) break;
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+  }
+  if (!seen) PM_CUDA(cudaStreamSynchronize(h->stream));
   if (f_out) *f_out = h->out_host[0];
   if (g_out && h->last_want_grad) std::memcpy(g_out, h->out_host + 1, sizeof(double) * h->K);
   return PM_OK;

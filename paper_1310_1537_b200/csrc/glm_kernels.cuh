@@ -899,6 +899,10 @@ struct GlmArgs {
   unsigned long long xepoch;  // >= 1, +1 per evaluation, identical on every rank
   double* xpeer[kMaxXchgRanks];  // mailbox base of every rank, mapped into this process
   unsigned* xstatus;          // local: set to 1 on a wait timeout
+  // completion word (nullable): written with done_seq, system-scope release, after the
+  // results -- pm_glm_wait polls it in mapped host memory instead of synchronising the stream
+  unsigned long long* done;
+  unsigned long long done_seq;
 #ifdef PM_AB_PHASES  // A/B timing experiment only: %globaltimer stamps per CTA, 8 slots each
   unsigned long long* stamps;
 #endif
@@ -1084,6 +1088,13 @@ __device__ inline void cta_reduce_finalize(const GlmArgs& a, const StreamSmem& s
   }
   ab_stamp(a, 6);
   if (tid == 0) *a.counter = 0u;  // re-arm for the next launch (kernel boundary orders it)
+  if (a.done && a.xw == 0) {
+    __syncthreads();  // every thread's result stores, then one system-scope fence + release store
+    if (tid == 0) {
+      asm volatile("fence.sc.sys;" ::: "memory");
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.done), "l"(a.done_seq) : "memory");
+    }
+  }
 #ifdef PM_AB_PHASES
   __syncthreads();
   ab_stamp(a, 4);

@@ -79,6 +79,7 @@ static const char* const kTuneNames[] = {
     "f64_pairs",         // fp64 consumer: 0 columns, 1 pairs (default)
     "stream_ncw",        // fp32-X column consumer: 15 warps (default) or 7
     "f32_selfprod",      // row-dot consumer: 0 producer thread, 1 self-producing consumer warps, 3 (default) + warp 0 consumes
+    "glm_poll",          // pm_glm_wait: 1 poll the completion word in mapped memory (default), 0 cudaStreamSynchronize
     "stream_tps",        // stream kernel 32-row tiles per stage / bulk copy (default: ~24 KB stages)
     "hb_rows",           // HB row-per-lane kernel: 0 off, 1 on (default)
     "hb_rows_ncw",       // 8 (default: all warps consume, self-producing), 7 or 15 (+ a producer warp)
