@@ -103,6 +103,12 @@ class GlmDevice:
         self._prior_key = None
         self.lock = threading.Lock()
         self.grid = self.geometry()["grid"]
+        # hot call: pm_glm_eval through a prototype that takes raw addresses (no per-call
+        # POINTER objects) and a reusable result slot for f (guarded by self.lock)
+        self._eval_c = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_void_p, ctypes.c_void_p)(("pm_glm_eval", lib))
+        self._f_slot = ctypes.c_double()
+        self._f_addr = ctypes.addressof(self._f_slot)
 
     @property
     def handle(self):
@@ -127,8 +133,11 @@ class GlmDevice:
                 _lib.call("pm_glm_set_prior", self._h, None, None)
                 self._prior_key = None
             return
-        mu = np.ascontiguousarray(mu, dtype=np.float64)
-        sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+        ready = (isinstance(mu, np.ndarray) and isinstance(sigma, np.ndarray) and mu.dtype == np.float64
+                 and sigma.dtype == np.float64 and mu.flags.c_contiguous and sigma.flags.c_contiguous)
+        if not ready:  # _prior_arrays hands over validated contiguous float64 arrays
+            mu = np.ascontiguousarray(mu, dtype=np.float64)
+            sigma = np.ascontiguousarray(sigma, dtype=np.float64)
         key = (mu.tobytes(), sigma.tobytes())
         if key != self._prior_key:
             _lib.call("pm_glm_set_prior", self._h, _lib.dptr(mu), _lib.dptr(sigma))
@@ -164,11 +173,13 @@ class GlmDevice:
 
     def eval(self, beta: np.ndarray, with_prior: bool, want_grad: bool):
         """One evaluation, one C call (pm_glm_eval holds the handle across launch + wait)."""
-        f = ctypes.c_double()
         g = np.empty(self.n_cols) if want_grad else None
-        _lib.call("pm_glm_eval", self._h, _lib.dptr(beta), int(with_prior), int(want_grad), ctypes.byref(f),
-                  _lib.dptr(g))
-        return f.value, g
+        rc = self._eval_c(self._h, beta.__array_interface__["data"][0], 1 if with_prior else 0,
+                          1 if want_grad else 0, self._f_addr,
+                          g.__array_interface__["data"][0] if want_grad else None)
+        if rc:
+            _lib.check(rc, "pm_glm_eval")
+        return self._f_slot.value, g
 
     def eval_device(self, beta: np.ndarray, want_grad: bool, dev_out_ptr: int, stream: int = 0,
                     with_prior: bool = False) -> None:
@@ -326,7 +337,7 @@ def _prior_arrays(prior, n_cols: int):
     return mu, sigma
 
 
-def _account(plan: ExecPlan, calls: int = 1, launches: int = 0, partials: int = 0) -> None:
+def _account(plan: ExecPlan, calls: int = 1, launches: int = 0, partials: int = 0, flops: int = 0) -> None:
     """The reference's region / merge accounting for `calls` evaluations under `plan`
     (instrumentation contract, read by its tests: SOM opens two regions -- the matvec and
     the transcendental pass, glm.py:277-295 / 375-396 -- every other strategy one, and the
@@ -334,23 +345,25 @@ def _account(plan: ExecPlan, calls: int = 1, launches: int = 0, partials: int = 
     (kernel launches, partials folded on the device) -- one counter update in all."""
     regions = 2 if plan.strategy is Strategy.SOM else 1
     counters.account(parallel_regions=regions * calls, merge_events=plan.workers * calls,
-                     kernel_launches=launches, device_partials=partials)
+                     kernel_launches=launches, device_partials=partials, flops=flops)
 
 
-def _evaluate(data, beta, plan: ExecPlan, prior, want_grad: bool) -> GradResult:
-    """Dispatch one evaluation to the device(s)."""
+def _evaluate(data, beta, plan: ExecPlan, prior, want_grad: bool, flops: int = 0) -> GradResult:
+    """Dispatch one evaluation to the device(s); `flops` (the caller's analytic count,
+    glm.py:173-176) is accounted with the regions / merges once the evaluation succeeded."""
     mu, sigma = _prior_arrays(prior, data.n_cols)
     if isinstance(data, ShardedMatrix):
-        return _evaluate_sharded(data, beta, plan, mu, sigma, want_grad)
+        return _evaluate_sharded(data, beta, plan, mu, sigma, want_grad, flops)
     dev = data.on_device(plan.device, plan.x_storage)
     with dev.lock:
         dev.set_prior(mu, sigma)
         f, g = dev.eval(beta, mu is not None, want_grad)
-    _account(plan, launches=1, partials=dev.grid)
+    _account(plan, launches=1, partials=dev.grid, flops=flops)
     return GradResult(f, g)
 
 
-def _evaluate_sharded(view: ShardedMatrix, beta, plan: ExecPlan, mu, sigma, want_grad: bool) -> GradResult:
+def _evaluate_sharded(view: ShardedMatrix, beta, plan: ExecPlan, mu, sigma, want_grad: bool,
+                      flops: int = 0) -> GradResult:
     """One kernel per shard on device shard % n_devices, merged in ascending shard order."""
     n_dev = max(1, _lib.device_count())
     devs = []
@@ -375,24 +388,20 @@ def _evaluate_sharded(view: ShardedMatrix, beta, plan: ExecPlan, mu, sigma, want
     finally:
         for d in devs:
             d.lock.release()
-    _account(plan, launches=len(devs), partials=len(devs))
+    _account(plan, launches=len(devs), partials=len(devs), flops=flops)
     return GradResult(f, g)
 
 
 def loglike(data, beta, plan: ExecPlan = ExecPlan()) -> float:
     """L(beta) (reference glm.py:257-274); one device pass, value plan-invariant."""
     beta = _check_beta(beta, data.n_cols, finite=False)
-    f = _evaluate(data, beta, plan, None, want_grad=False).f  # raises on a non-finite beta
-    counters.add_flops(data.n_rows * (2 * data.n_cols + _TR_FLOPS))
-    return f
+    return _evaluate(data, beta, plan, None, False, data.n_rows * (2 * data.n_cols + _TR_FLOPS)).f
 
 
 def loglike_grad(data, beta, plan: ExecPlan = ExecPlan()) -> GradResult:
     """L(beta) and X'(y - sigmoid(X beta)) (reference glm.py:351-364) in one fused pass."""
     beta = _check_beta(beta, data.n_cols, finite=False)
-    res = _evaluate(data, beta, plan, None, want_grad=True)  # raises on a non-finite beta
-    counters.add_flops(data.n_rows * (4 * data.n_cols + _TR_GRAD_FLOPS))
-    return res
+    return _evaluate(data, beta, plan, None, True, data.n_rows * (4 * data.n_cols + _TR_GRAD_FLOPS))
 
 
 def log_posterior_grad(data, beta, prior, plan: ExecPlan = ExecPlan(), want_grad: bool = True) -> GradResult:
@@ -403,9 +412,8 @@ def log_posterior_grad(data, beta, prior, plan: ExecPlan = ExecPlan(), want_grad
     is added on the device by the kernel's finalising CTA.
     """
     beta = _check_beta(beta, data.n_cols, finite=False)
-    res = _evaluate(data, beta, plan, prior, want_grad=want_grad)  # raises on a non-finite beta
-    counters.add_flops(data.n_rows * (4 * data.n_cols + _TR_GRAD_FLOPS) + 4 * data.n_cols)
-    return res
+    return _evaluate(data, beta, plan, prior, want_grad,
+                     data.n_rows * (4 * data.n_cols + _TR_GRAD_FLOPS) + 4 * data.n_cols)
 
 
 # ---------------------------------------------------------------------------
