@@ -410,6 +410,18 @@ int choose_geometry(pm_glm_s* h) {
       }
     }
   }
+  if (h->kind == KIND_STREAM && h->pairs == 0 && h->ncw == kNCW && tune("stream_selfprod", 0) != 0) {
+    // column consumers: all 8 warps consume and issue their own bulk copies (no producer
+    // thread); stages a multiple of 8
+    const int nw = kNCW + 1, tr = h->tps * kTileRows;
+    int S = std::min(kMaxStages, 2 * nw);
+    while (S > nw && stream_smem_bytes(h->K, xs, S, nw, tr) > size_t(budget)) S -= nw;
+    if (stream_smem_bytes(h->K, xs, S, nw, tr) <= size_t(budget)) {
+      h->selfprod = 3;
+      h->stages = S;
+      h->smem = stream_smem_bytes(h->K, xs, S, nw, tr);
+    }
+  }
   if (h->kind == KIND_STREAM && h->pairs == 3) {
     // row-dot consumer: self-producing consumer warps (tune f32_selfprod: 0 = producer thread,
     // 1 = consumer warps issue their own copies, 3 (default) = and warp 0 consumes as well:
@@ -466,7 +478,7 @@ GlmArgs make_args(pm_glm_s* h, bool with_prior, double* out) {
   a.K = h->K;
   a.stages = h->stages;
   a.tps = h->kind == KIND_STREAM ? h->tps : 1;
-  a.selfprod = (h->kind == KIND_STREAM && h->pairs == 3) ? h->selfprod : 0;
+  a.selfprod = h->kind == KIND_STREAM ? h->selfprod : 0;
   a.with_prior = with_prior ? 1 : 0;
   a.evict_first = 1;
   a.prior_mu = h->prior_mu;

@@ -118,10 +118,19 @@ struct SubRows {
 // Each row's transcendental terms are computed by 32/R lanes; only lane < R counts f.
 // `empty` (the stage's release barrier) is arrived on as soon as the last sub-tile's values
 // are in registers, so the producer can refill the stage while this warp still computes.
-template <typename XT, int KC, bool GRAD, int R = SubRows<KC, GRAD>::value, int TR = kTileRows>
+// Self-producing consumers pass a RefillWhen: at the release point the warp quiesces its reads
+// of the stage and, when `active` (the unit's last tile), issues its own next copies (fn).
+struct NoRefill {};
+template <class F>
+struct RefillWhen {
+  bool active;
+  F fn;
+};
+template <typename XT, int KC, bool GRAD, int R = SubRows<KC, GRAD>::value, int TR = kTileRows,
+          class Refill = NoRefill>
 __device__ __forceinline__ void consume_tile(const XT* xs, const double* ys, int K, int lane, int64_t row0,
                                              int64_t row_limit, const double (&breg)[KC], double (&g)[KC],
-                                             double& nll_acc, uint64_t* empty) {
+                                             double& nll_acc, uint64_t* empty, Refill refill = Refill()) {
 #pragma unroll 1
   for (int sub = 0; sub < TR / R; ++sub) {
     const XT* xb = xs + (sub * R) * K + lane;
@@ -146,7 +155,14 @@ __device__ __forceinline__ void consume_tile(const XT* xs, const double* ys, int
       double dep = yv;
 #pragma unroll
       for (int r = 0; r < R; ++r) dep += v[r];
-      if (empty) mbar_arrive_after(empty, dep, lane, const_cast<XT*>(xs));
+      if constexpr (!std::is_same<Refill, NoRefill>::value) {
+        if (refill.active) {
+          mbar_arrive_after(nullptr, dep, lane, const_cast<XT*>(xs));  // quiesce only
+          refill.fn();
+        }
+      } else if (empty) {
+        mbar_arrive_after(empty, dep, lane, const_cast<XT*>(xs));
+      }
     }
     const double t = transpose_reduce<R>(v, lane);
     double nll, w;
@@ -764,6 +780,64 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
       return;
     }
   }
+  if constexpr (MULTI) {
+    // Self-producing column consumers (selfprod == 3: all NCW + 1 warps consume and issue the
+    // bulk copies of their own units; narrow / small designs, where the single producer
+    // thread's ~100 ns per copy delays the last warp's first data by more than a microsecond
+    // and an eighth consumer shortens the per-warp chain of tiles).
+    if (selfprod == 3) {
+      const int cw = warp;
+      const int nact = S < NCW + 1 ? S : NCW + 1;
+      const int Se = S - S % nact;
+      if (cw >= nact) return;
+      const int spw = Se / nact;
+      const uint64_t pol = l2_policy_evict_first();
+      auto issue_unit = [&](int64_t i, int s) {  // lane 0
+        const int64_t tile = tile_begin + i * U * stride;
+        const int64_t left = n_tiles_mine - i * U;
+        const uint32_t cnt = uint32_t(left < U ? left : U);
+        mbar_arrive_expect_tx(&sm.full[s], cnt * (tile_bytes + TR * uint32_t(sizeof(double))));
+        const XT* src = X + tile * int64_t(tile_elems);
+        if (evict_first) {
+          bulk_g2s_hint(sm.xs + size_t(s) * tile_pitch, src, cnt * tile_bytes, &sm.full[s], pol);
+        } else {
+          bulk_g2s(sm.xs + size_t(s) * tile_pitch, src, cnt * tile_bytes, &sm.full[s]);
+        }
+        bulk_g2s(sm.ys + size_t(s) * U * TR, y + tile * TR, cnt * TR * uint32_t(sizeof(double)), &sm.full[s]);
+      };
+      if (lane == 0) {
+        for (int m = 0; m < spw; ++m) {
+          const int64_t i = cw + int64_t(m) * nact;
+          if (i < n_mine) issue_unit(i, cw + m * nact);
+        }
+      }
+      int m = 0;
+      uint32_t n = 0;
+      for (int64_t i = cw; i < n_mine; i += nact) {
+        const int s = cw + m * nact;
+        mbar_wait(&sm.full[s], n & 1);
+        const int64_t tile0 = tile_begin + i * U * stride;
+        const int64_t left = n_tiles_mine - i * U;
+        const int cnt = int(left < U ? left : U);
+        const unsigned char* xstage = sm.xs + size_t(s) * tile_pitch;
+        const double* ystage = sm.ys + size_t(s) * U * TR;
+        const int64_t nxt = i + int64_t(spw) * nact;
+        auto refill = [&]() {
+          if (lane == 0 && nxt < n_mine) issue_unit(nxt, s);
+        };
+        for (int j = 0; j < cnt; ++j) {
+          consume_tile<XT, KC, GRAD, R, TR>(reinterpret_cast<const XT*>(xstage + size_t(j) * tile_bytes),
+                                            ystage + j * TR, K, lane, (tile0 + j) * TR, row_limit, breg, g, nll_acc,
+                                            nullptr, RefillWhen<decltype(refill)>{j == cnt - 1, refill});
+        }
+        if (++m == spw) {
+          m = 0;
+          ++n;
+        }
+      }
+      return;
+    }
+  }
   if (warp == 0) {
     const uint64_t pol = l2_policy_evict_first();
     int s = 0;        // stage = i % Se
@@ -1119,7 +1193,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   const int K = a.K;
   const int S = a.stages;
   const int U = a.tps;  // tiles per stage (> 1: contiguous tile range per CTA, one copy per unit)
-  const int nw = (PAIRS == 3 && a.selfprod == 3) ? NCW + 1 : NCW;  // warps holding a partial
+  const int nw = ((PAIRS == 3 || (PAIRS == 0 && NCW <= 8)) && a.selfprod == 3) ? NCW + 1 : NCW;  // warps holding a partial
   const StreamSmem sm = carve_stream_smem(smem_raw, K, sizeof(XT), S, nw, TR * U);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -1142,7 +1216,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
 #pragma unroll
   for (int j = 0; j < KC; ++j) {
     const int c = lane_col<PAIRS != 0>(lane, j);
-    breg[j] = (warp > 0 && c < K) ? beta.v[c] * XScale<XT>::value : 0.0;  // exact (power of two)
+    breg[j] = ((warp > 0 || nw > NCW) && c < K) ? beta.v[c] * XScale<XT>::value : 0.0;  // exact (power of two)
     g[j] = 0.0;
   }
   if (blockIdx.x == 0 && a.with_prior && warp == NCW)
