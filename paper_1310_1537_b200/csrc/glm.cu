@@ -410,6 +410,7 @@ int choose_geometry(pm_glm_s* h) {
       }
     }
   }
+#ifdef PM_AB_STREAM_SELFPROD
   if (h->kind == KIND_STREAM && h->pairs == 0 && h->ncw == kNCW && tune("stream_selfprod", 0) != 0) {
     // column consumers: all 8 warps consume and issue their own bulk copies (no producer
     // thread); stages a multiple of 8
@@ -422,6 +423,7 @@ int choose_geometry(pm_glm_s* h) {
       h->smem = stream_smem_bytes(h->K, xs, S, nw, tr);
     }
   }
+#endif
   if (h->kind == KIND_STREAM && h->pairs == 3) {
     // row-dot consumer: self-producing consumer warps (tune f32_selfprod: 0 = producer thread,
     // 1 = consumer warps issue their own copies, 3 (default) = and warp 0 consumes as well:

@@ -780,6 +780,8 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
       return;
     }
   }
+#ifdef PM_AB_STREAM_SELFPROD  // A/B build only (-DPM_AB_STREAM_SELFPROD + tune stream_selfprod=1): compiled into
+                              // the default library, the extra path cost the config-0 kernel ~1 us per launch
   if constexpr (MULTI) {
     // Self-producing column consumers (selfprod == 3: all NCW + 1 warps consume and issue the
     // bulk copies of their own units; narrow / small designs, where the single producer
@@ -838,6 +840,7 @@ __device__ __forceinline__ void stream_tiles(const XT* __restrict__ X, const dou
       return;
     }
   }
+#endif
   if (warp == 0) {
     const uint64_t pol = l2_policy_evict_first();
     int s = 0;        // stage = i % Se

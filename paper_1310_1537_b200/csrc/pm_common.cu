@@ -80,7 +80,7 @@ static const char* const kTuneNames[] = {
     "stream_ncw",        // fp32-X column consumer: 15 warps (default) or 7
     "f32_selfprod",      // row-dot consumer: 0 producer thread, 1 self-producing consumer warps, 3 (default) + warp 0 consumes
     "glm_poll",          // pm_glm_wait: 1 poll the completion word in mapped memory (default), 0 cudaStreamSynchronize
-    "stream_selfprod",   // column consumers of the stream kernel: 0 producer thread (default), 1 all 8 warps consume and produce for themselves (measured slower at config 0)
+    "stream_selfprod",   // column consumers of the stream kernel: 0 producer thread (default), 1 all 8 warps consume and produce for themselves (only in -DPM_AB_STREAM_SELFPROD builds; measured slower at config 0)
     "stream_tps",        // stream kernel 32-row tiles per stage / bulk copy (default: ~24 KB stages)
     "hb_rows",           // HB row-per-lane kernel: 0 off, 1 on (default)
     "hb_rows_ncw",       // 8 (default: all warps consume, self-producing), 7 or 15 (+ a producer warp)

@@ -31,7 +31,6 @@ def test_protocol_subset_against_oracle(gpu, family):
 
 @pytest.mark.parametrize("k,n,xs,knobs", [
     (32, 100_000, "f64", {}),                      # config 0: 2-tile units, producer thread
-    (32, 100_000, "f64", {"stream_selfprod": 1}),  # ... 8 self-producing column consumers (A/B form)
     (75, 260_000, "f64", {}),                      # odd K: column consumer, KC = 3, ring reuse
     (32, 100_000, "f64", {"stream_tps": 1}),       # single interleaved tiles
     (32, 700_001, "f64", {"stream_tps": 2}),       # ring reuse with 2-tile units, ragged tail
