@@ -35,10 +35,30 @@ int max_optin_smem(int device) {
   return v;
 }
 
+// finite <=> exponent field not all ones; branch-free so the host compiler vectorises it
+// (an early-exit isfinite loop costs ~7 us per 20,000 doubles: every HB evaluation)
 bool all_finite(const double* p, int64_t n) {
-  for (int64_t i = 0; i < n; ++i)
-    if (!std::isfinite(p[i])) return false;
-  return true;
+  constexpr uint64_t kExp = 0x7ff0000000000000ull;
+  uint64_t bad = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t b;
+    std::memcpy(&b, p + i, sizeof(b));
+    bad |= uint64_t((b & kExp) == kExp);
+  }
+  return bad == 0;
+}
+
+// dst[0..n) = src[0..n) and the same finiteness test in one pass over the data
+bool copy_check_finite(double* dst, const double* src, int64_t n) {
+  constexpr uint64_t kExp = 0x7ff0000000000000ull;
+  uint64_t bad = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t b;
+    std::memcpy(&b, src + i, sizeof(b));
+    bad |= uint64_t((b & kExp) == kExp);
+    std::memcpy(dst + i, &b, sizeof(b));
+  }
+  return bad == 0;
 }
 
 template <typename T>
@@ -1641,7 +1661,6 @@ int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64_t* off
 static int hb_stage(pm_hb_t h, const double* betas, const double* mu, const double* sigma, HbArgs& a) {
   if (h->G == 0) return fail(PM_ESTATE, "no data uploaded");
   const int G = h->G, K = h->K;
-  if (!all_finite(betas, int64_t(G) * K)) return fail(PM_EINVAL, "betas contain non-finite entries");
   const bool prior = mu != nullptr;
   if (prior != (sigma != nullptr)) return fail(PM_EINVAL, "mu and sigma must both be given");
   if (prior) {
@@ -1649,7 +1668,8 @@ static int hb_stage(pm_hb_t h, const double* betas, const double* mu, const doub
       if (!(sigma[k] > 0) || !std::isfinite(mu[k]) || !std::isfinite(sigma[k]))
         return fail(PM_EINVAL, "prior must be finite with sigma > 0");
   }
-  std::memcpy(h->pin_in, betas, sizeof(double) * size_t(G) * K);
+  // staged and validated in one pass (a rejected call leaves stale staging bytes, nothing else)
+  if (!copy_check_finite(h->pin_in, betas, int64_t(G) * K)) return fail(PM_EINVAL, "betas contain non-finite entries");
   if (prior) {
     std::memcpy(h->pin_in + size_t(G) * K, mu, sizeof(double) * K);
     std::memcpy(h->pin_in + size_t(G) * K + K, sigma, sizeof(double) * K);

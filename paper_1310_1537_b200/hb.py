@@ -112,6 +112,9 @@ class HbDevice:
         self.G, self.K = csr.m_groups, csr.n_cols
         _lib.check(lib.pm_hb_upload(h, _lib.dptr(csr.x), _lib.dptr(csr.y), _lib.i64ptr(csr.offsets),
                                     self.G, self.K), "pm_hb_upload")
+        # hot call through a prototype that takes raw addresses (no per-call POINTER objects)
+        vp = ctypes.c_void_p
+        self._eval_c = ctypes.CFUNCTYPE(ctypes.c_int, vp, vp, vp, vp, ctypes.c_int, vp, vp)(("pm_hb_eval", lib))
 
     def stream(self) -> int:
         p = ctypes.c_void_p()
@@ -128,8 +131,10 @@ class HbDevice:
         sigma = None if sigma is None else np.ascontiguousarray(sigma, dtype=np.float64)
         if mu is not None and (mu.shape != (self.K,) or sigma is None or sigma.shape != (self.K,)):
             raise ValueError("prior dimension does not match dataset")
-        _lib.call("pm_hb_eval", self._h, _lib.dptr(betas), _lib.dptr(mu), _lib.dptr(sigma),
-                  int(want_grad), _lib.dptr(f), _lib.dptr(g))
+        addr = lambda a: None if a is None else a.__array_interface__["data"][0]  # noqa: E731
+        rc = self._eval_c(self._h, addr(betas), addr(mu), addr(sigma), 1 if want_grad else 0, addr(f), addr(g))
+        if rc:
+            _lib.check(rc, "pm_hb_eval")
         return f, g
 
     def time_evals(self, betas, mu=None, sigma=None, n: int = 10, want_grad: bool = True) -> float:
