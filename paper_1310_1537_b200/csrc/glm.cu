@@ -1356,7 +1356,8 @@ struct pm_hb_s {
   double* sigma_dev = nullptr;
   double* out_f = nullptr;
   double* out_g = nullptr;
-  double* pin_in = nullptr;    // G*K + 2K
+  double* pin_in = nullptr;    // G*K + 2K (mapped: the kernels can read it in place, tune hb_mapped_in)
+  double* pin_in_dev = nullptr;  // device alias of pin_in
   double* pin_out = nullptr;   // G + G*K (mapped)
   double* pin_out_dev = nullptr;  // device alias of pin_out
   // small-K row-per-lane path (even K <= 32): balanced tile ranges + segment fold
@@ -1582,7 +1583,8 @@ int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64_t* off
   // f then g, contiguous: pm_hb_eval reads both back with one D2H copy
   PM_CUDA(cudaMalloc(&h->out_f, sizeof(double) * (size_t(G) + size_t(G) * K)));
   h->out_g = h->out_f + G;
-  PM_CUDA(cudaHostAlloc(&h->pin_in, sizeof(double) * (size_t(G) * K + 2 * K), cudaHostAllocPortable));
+  PM_CUDA(cudaHostAlloc(&h->pin_in, sizeof(double) * (size_t(G) * K + 2 * K), cudaHostAllocPortable | cudaHostAllocMapped));
+  PM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->pin_in_dev), h->pin_in, 0));
   // mapped, so the fold can also write (f, g) straight into host memory (tune hb_mapped_out=1)
   PM_CUDA(cudaHostAlloc(&h->pin_out, sizeof(double) * (size_t(G) + size_t(G) * K),
                         cudaHostAllocPortable | cudaHostAllocMapped));
@@ -1674,18 +1676,23 @@ static int hb_stage(pm_hb_t h, const double* betas, const double* mu, const doub
     std::memcpy(h->pin_in + size_t(G) * K, mu, sizeof(double) * K);
     std::memcpy(h->pin_in + size_t(G) * K + K, sigma, sizeof(double) * K);
   }
-  // one copy: betas, then mu and sigma right after them (contiguous on both sides)
-  PM_CUDA(cudaMemcpyAsync(h->betas, h->pin_in, sizeof(double) * (size_t(G) * K + (prior ? 2 * K : 0)),
-                          cudaMemcpyHostToDevice, h->stream));
+  // hb_mapped_in=1 (A/B): no H2D copy -- the kernels read betas / mu / sigma in place from the
+  // mapped staging buffer (one 8K-byte read per warp and group over PCIe instead of a DMA
+  // before the launch); default: one copy, betas then mu and sigma (contiguous on both sides)
+  const bool mapped_in = tune("hb_mapped_in", 0) == 1;
+  if (!mapped_in)
+    PM_CUDA(cudaMemcpyAsync(h->betas, h->pin_in, sizeof(double) * (size_t(G) * K + (prior ? 2 * K : 0)),
+                            cudaMemcpyHostToDevice, h->stream));
   a.X = h->X;
   a.y = h->y;
   a.poff = h->poff;
   a.nrows = h->nrows;
   a.K = K;
   a.stages = h->stages;
-  a.betas = h->betas;
-  a.mu = prior ? h->mu_dev : nullptr;
-  a.sigma = prior ? h->sigma_dev : nullptr;
+  const double* src = mapped_in ? h->pin_in_dev : h->betas;
+  a.betas = src;
+  a.mu = prior ? src + size_t(G) * K : nullptr;
+  a.sigma = prior ? src + size_t(G) * K + K : nullptr;
   a.out_f = h->out_f;
   a.out_g = h->out_g;
   return PM_OK;
@@ -1703,9 +1710,11 @@ int pm_hb_eval(pm_hb_t h, const double* betas, const double* mu, const double* s
   if (rc) return rc;
   const int G = h->G, K = h->K;
   const bool grad = want_grad != 0 && g_out != nullptr;
-  // default: the fold writes (f, g) to device memory and one DMA brings them back (168 KB at
-  // config 3); hb_mapped_out=1: the fold's stores go straight into mapped host memory
-  const bool mapped = tune("hb_mapped_out", 0) == 1;
+  // default (hb_mapped_out=1): the fold's stores go straight into mapped host memory;
+  // hb_mapped_out=0: the fold writes (f, g) to device memory and one DMA brings them back
+  // (168 KB at config 3).  Re-measured in r02 after the host path was trimmed: 110.1 vs 117.1 us
+  // per call end to end (profiles/r02_ab_hb_selfprod.txt); in r01 the copy had won.
+  const bool mapped = tune("hb_mapped_out", 1) == 1;
   if (mapped) {
     a.out_f = h->pin_out_dev;
     a.out_g = h->pin_out_dev + G;

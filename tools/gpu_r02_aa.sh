@@ -1,0 +1,15 @@
+# r02 pass AA: HB inputs read in place from mapped memory (tune hb_mapped_in) and mapped outputs: A/B
+O=gpurun_out/r02aa
+mkdir -p $O
+for t in "hb_mapped_in=0" "hb_mapped_in=1" "hb_mapped_out=1" "hb_mapped_in=1 --tune hb_mapped_out=1" "hb_mapped_in=0" "hb_mapped_in=1"; do
+  echo "== $t" >> $O/c3.log
+  timeout 600 python bench.py --config c3 --no-cpu-baseline --tune $t >> $O/c3.log 2>&1
+done
+python - <<'PY'
+import json
+tag=None
+for line in open('gpurun_out/r02aa/c3.log'):
+    if line.startswith('=='): tag=line.strip()
+    elif line.startswith('{'):
+        l=json.loads(line); print(tag, 'device', round(l['value'],1), 'us', round(l['ms_per_step']*1e3,2), 'e2e', round(l['e2e']['value'],1), round(1e6/l['e2e']['value'],1), 'us')
+PY
