@@ -872,7 +872,12 @@ def run_gibbs(args, cfg):
         flush()
         cold_ms += dev.time_sweeps(1, 2, rng.seed, 0, rng.sweep + args.steps + t)
     del flush
-    # end to end: spins in from host, sweeps, spins out
+    # end to end: spins in from host, sweeps, spins out (one untimed spin round trip first, as
+    # every other timed region here has its warm-up: the first one after the cold-L2 loop
+    # intermittently took ~50 ms on the pack step, whatever the model)
+    part.pack_from(lat)
+    part.unpack_into(lat)
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     part.pack_from(lat)
     t1 = time.perf_counter()
