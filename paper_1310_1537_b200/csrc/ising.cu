@@ -259,7 +259,11 @@ struct GibbsTables {
   // Potts T32: by the compact code sum e (0..84), threshold a of entry e replicated per lane at
   //   word (3e + a) * 32 + lane, so every lane reads its own bank (random e, no conflicts)
   // Potts 64-bit: by the compact code sum e, entry 3e + a (no lane replication: rare path)
+#ifdef PM_AB_GIBBS_BORROW
+  using IsingT = unsigned long long;  // 2^64 - T
+#else
   using IsingT = typename std::conditional<T32, uint32_t, unsigned long long>::type;
+#endif
   typename std::conditional<MODEL == PM_MODEL_ISING, IsingT[8],
                             typename std::conditional<T32, uint32_t[kPottsCodes * 3 * 32],
                                                       unsigned long long[kPottsCodes * 3]>::type>::type t;
@@ -295,7 +299,11 @@ __global__ void __launch_bounds__(256, NG == 1 ? 6 : MODEL == PM_MODEL_ISING ? P
     // static indices into the parameter array (a dynamic index would copy the params to local memory)
     if (tid == 0) {
 #pragma unroll
+#ifdef PM_AB_GIBBS_BORROW
+      for (int k = 0; k < 5; ++k) tb.t[k] = 0ull - a.thr[8 - 2 * k];
+#else
       for (int k = 0; k < 5; ++k) tb.t[k] = a.thr[8 - 2 * k];
+#endif
     }
   } else if constexpr (T32) {
     // replicate the compact table (85 x 3 words) across the 32 lanes: 4 lanes per 16-byte store
@@ -373,6 +381,23 @@ __device__ __forceinline__ void gibbs_packed_words(const PackedArgs& a, const Gi
       // packed bytes are 1 - s (0x02 for -1, 0x00 for +1), so the plain 4-way byte sum is
       // 2 x (number of -1 neighbours) <= 8 per byte (no carries, no masks); scaled to the
       // table's byte offset (x4 for u32 thresholds, x8 for u64) it is the LDS address offset
+#ifdef PM_AB_GIBBS_BORROW
+      // A/B build only: the compare on the FMA pipe.  tb.t holds 2^64 - T per entry (8 bytes);
+      // word + (2^64 - T) as one IMAD.WIDE: the high word is all ones iff word < T.  One
+      // IMAD.WIDE + one LOP3 per site instead of ISETP + a predicated add (both ALU).
+      const uint32_t off = (U[m] + D[m] + cur + sh) << 2;
+      const char* tbase = reinterpret_cast<const char*>(&tb.t[0]);
+      uint32_t plus_bits = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const uint32_t o = __byte_perm(off, 0u, 0x4440u + b);
+        const unsigned long long neg = *reinterpret_cast<const unsigned long long*>(tbase + o);
+        unsigned long long w;
+        asm("mad.wide.u32 %0, %1, 1, %2;" : "=l"(w) : "r"(blk.v[b]), "l"(neg));
+        plus_bits |= uint32_t(w >> 32) & (1u << (8 * b));
+      }
+      out = 0x02020202u - 2u * plus_bits;
+#else
       constexpr int SH = T32 ? 1 : 2;
       const uint32_t off = (U[m] + D[m] + cur + sh) << SH;
       const char* tbase = reinterpret_cast<const char*>(&tb.t[0]);
@@ -389,6 +414,7 @@ __device__ __forceinline__ void gibbs_packed_words(const PackedArgs& a, const Gi
         plus_bits |= plus ? (1u << (8 * b)) : 0u;
       }
       out = 0x02020202u - 2u * plus_bits;  // per byte: 0x00 (+1) or 0x02 (-1), no borrows
+#endif
     } else {
       if constexpr (T32) {
         // packed bytes hold the codes already (enc 2): code sums <= 84 per byte, no carries
