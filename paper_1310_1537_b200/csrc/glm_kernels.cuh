@@ -448,21 +448,15 @@ __device__ __forceinline__ void consume_tile_f32full(const float* xs, const doub
 // Against consume_tile_pairs at K = 100: ~33 instead of ~45 warp instructions per row, 64
 // instead of 124 shuffles per tile, and x never lives in registers across the two phases
 // (the pairs consumer keeps 16 x 4 doubles = 128 registers per sub-tile in flight).
-// leading column pairs of every gradient-phase row widened by F2F (XU pipe) instead of integer
-// ops (ALU pipe); A/B builds override it (-DPM_ROWDOT_F2F_PAIRS=0|1|2)
+// PM_ROWDOT_F2F_PAIRS: leading column pairs of every gradient-phase row widened by F2F (XU
+// pipe) instead of integer ops (ALU pipe); A/B builds override it (-DPM_ROWDOT_F2F_PAIRS=0|1|2)
 #ifndef PM_ROWDOT_F2F_PAIRS
 #define PM_ROWDOT_F2F_PAIRS 1
 #endif
-struct NoMid {
-  __device__ __forceinline__ void operator()(double) const {}
-};
-// `mid(dep)` is called once rows 0..15 of the gradient phase have been read (dep depends on
-// every word read so far): the self-producing form refills the stage's first half there.
-template <int KC, bool GRAD, class Mid = NoMid>
+template <int KC, bool GRAD>
 __device__ __forceinline__ void consume_tile_rowdot(const float* xs, const double* ys, int K, int lane,
                                                     int64_t row0, int64_t row_limit, const double* sbeta,
-                                                    double (&g)[KC], double& nll_acc, uint64_t* empty,
-                                                    Mid mid = Mid(), float* done_word = nullptr) {
+                                                    double (&g)[KC], double& nll_acc, uint64_t* empty) {
   static_assert(KC % 2 == 0, "row-dot consumer: pairs layout in the gradient phase");
   constexpr int KP = KC / 2;
   const float* xr = xs + size_t(lane) * K;
@@ -522,18 +516,6 @@ __device__ __forceinline__ void consume_tile_rowdot(const float* xs, const doubl
         ga[r % NS - 1][2 * c + 1] = fma(ww, x1, ga[r % NS - 1][2 * c + 1]);
       }
     }
-    if constexpr (!std::is_same<Mid, NoMid>::value) {
-      if (r == 15) {
-        double dh = 0.0;
-#pragma unroll
-        for (int j = 0; j < KC; ++j) dh += g[j];
-#pragma unroll
-        for (int s2 = 0; s2 + 1 < NS; ++s2)
-#pragma unroll
-          for (int j = 0; j < KC; ++j) dh += ga[s2][j];
-        mid(dh);
-      }
-    }
   }
 #pragma unroll
   for (int s2 = 0; s2 + 1 < NS; ++s2)
@@ -542,9 +524,7 @@ __device__ __forceinline__ void consume_tile_rowdot(const float* xs, const doubl
   double dg = 0.0;
 #pragma unroll
   for (int j = 0; j < KC; ++j) dg += g[j];  // depends on every re-read word
-  // done_word: where the dependency word goes (default: the stage's first 128 bytes; the
-  // half-refilling form passes row 16, its first half being rewritten by then)
-  mbar_arrive_after(empty, dg, lane, done_word ? done_word : const_cast<float*>(xs));
+  mbar_arrive_after(empty, dg, lane, const_cast<float*>(xs));
 }
 
 // fp32-X row-dot consumer run by a PAIR of warps per tile (PAIRS == 4; KC == 4, K % 4 == 0,
