@@ -1642,9 +1642,11 @@ int pm_hb_upload(pm_hb_t h, const double* X, const double* y, const int64_t* off
     PM_CUDA(cudaMalloc(&h->gcount, sizeof(unsigned) * G));
     PM_CUDA(cudaMemset(h->gcount, 0, sizeof(unsigned) * G));
     h->rows_contig = tune("hb_contig", 1) != 0 ? 1 : 0;
-    // measured (profiles/r01_ab_hb_pdl.txt): with PDL a separate fold launch overlapped with
-    // the next rows kernel beats the fused per-group-ticket fold (68.3 vs 71.2 us)
-    h->rows_fused = tune("hb_fused", 0) == 1 ? 1 : 0;
+    // fold fused into the rows launch (per-group tickets) by default: with the self-producing
+    // 8-warp kernel it beats the separate PDL-overlapped fold launch, 61.5 vs 64.4 us
+    // (profiles/r02_ab_hb_selfprod.txt); with the r01 producer-thread kernel it was the other
+    // way round (68.3 vs 71.2 us, profiles/r01_ab_hb_pdl.txt).  tune hb_fused=0 separates it.
+    h->rows_fused = tune("hb_fused", 1) == 1 ? 1 : 0;
     h->rows_pdl = tune("pdl", 1) != 0 ? 1 : 0;
     h->rows = true;
     h->rows_grid = C;

@@ -88,7 +88,7 @@ static const char* const kTuneNames[] = {
     "hb_rows_stages",    // stages (default: auto)
     "hb_contig",         // contiguous per-warp tile ranges: 1 (default)
     "hb_selfprod",       // HB rows kernel: consumer warps issue their own bulk copies: 1 (default), 0 producer thread
-    "hb_fused",          // fold fused into the rows launch: 0 (default)
+    "hb_fused",          // fold fused into the rows launch: 1 (default), 0 separate fold launch
     "hb_mapped_in",      // pm_hb_eval inputs: 0 one H2D copy (default), 1 kernels read the mapped staging buffer in place
     "hb_mapped_out",     // pm_hb_eval results: 1 mapped host stores (default), 0 device + one D2H copy
     "pdl",               // programmatic dependent launch: 1 (default)

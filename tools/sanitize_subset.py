@@ -53,7 +53,7 @@ def glm_cases():
 
 def hb_cases():
     from paper_1310_1537_b200.synthetic import hb_design
-    for knobs in ({}, {"hb_fused": 1}, {"hb_rows": 0}, {"hb_mapped_out": 0}, {"hb_selfprod": 0, "hb_rows_ncw": 7},
+    for knobs in ({}, {"hb_fused": 0}, {"hb_rows": 0}, {"hb_mapped_out": 0}, {"hb_selfprod": 0, "hb_rows_ncw": 7},
                   {"hb_rows_ncw": 15}, {"hb_mapped_in": 1}):
         with _lib.tuned(**knobs):
             x, y, off, betas, mu, tau = hb_design(40, 20, seed=3, mean_rows=300)
