@@ -1124,6 +1124,7 @@ struct pm_ws_s {
   unsigned long long* maxbits = nullptr;
   double* out_host = nullptr;
   double* out_dev = nullptr;
+  unsigned long long seq = 0;  // differential evaluations launched (completion word value)
   int grid = 0;
   std::mutex mu;
 };
@@ -1187,7 +1188,8 @@ int pm_ws_create(pm_glm_t h, const double* beta0, pm_ws_t* out) {
   chk(cudaMalloc(&w->partials, sizeof(double) * size_t(w->grid) * kMaxDeltas));
   chk(cudaMalloc(&w->counter, sizeof(unsigned int)));
   chk(cudaMalloc(&w->maxbits, sizeof(unsigned long long)));
-  chk(cudaHostAlloc(&w->out_host, sizeof(double) * kMaxDeltas, cudaHostAllocMapped | cudaHostAllocPortable));
+  chk(cudaHostAlloc(&w->out_host, sizeof(double) * (kMaxDeltas + 1), cudaHostAllocMapped | cudaHostAllocPortable));
+  if (w->out_host) std::memset(w->out_host, 0, sizeof(double) * (kMaxDeltas + 1));
   if (e != cudaSuccess) {
     free_ws(w);
     delete w;
@@ -1248,6 +1250,8 @@ int pm_ws_diff_eval(pm_ws_t w, int32_t k, const double* deltas, int32_t n_deltas
   a.partials = w->partials;
   a.counter = w->counter;
   a.out = w->out_dev;
+  a.done = reinterpret_cast<unsigned long long*>(w->out_dev + kMaxDeltas);
+  a.done_seq = ++w->seq;
   DeltaPack dp;
   for (int m = 0; m < kMaxDeltas; ++m) dp.d[m] = m < n_deltas ? deltas[m] : 0.0;
   cudaError_t e;
@@ -1257,7 +1261,20 @@ int pm_ws_diff_eval(pm_ws_t w, int32_t k, const double* deltas, int32_t n_deltas
   else if (n_deltas <= 8) e = launch_diff<8>(a, dp, w->grid, h->stream);
   else e = launch_diff<16>(a, dp, w->grid, h->stream);
   if (e != cudaSuccess) return cuda_fail(e, "diff_eval launch");
-  PM_CUDA(cudaStreamSynchronize(h->stream));
+  // completion: poll the word the finishing CTA stores after the results (as pm_glm_wait)
+  bool seen = false;
+  if (tune("glm_poll", 1) != 0) {
+    volatile unsigned long long* word = reinterpret_cast<volatile unsigned long long*>(w->out_host + kMaxDeltas);
+    for (unsigned spins = 1;; ++spins) {
+      if (*word == w->seq) {
+        seen = true;
+        break;
+      }
+      if ((spins & 0x3ff) == 0 && cudaStreamQuery(h->stream) != cudaErrorNotReady) break;
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+  }
+  if (!seen) PM_CUDA(cudaStreamSynchronize(h->stream));
   std::memcpy(f_out, w->out_host, sizeof(double) * n_deltas);
   return PM_OK;
 }

@@ -20,9 +20,11 @@ struct DiffArgs {
   const double* xk;   // xt + k*n_pad
   const double* y;
   int64_t n;
-  double* partials;   // [grid][kMaxDeltas]
+  double* partials;   // [kMaxDeltas][grid]
   unsigned int* counter;
   double* out;        // [M]
+  unsigned long long* done;     // completion word after `out` in mapped memory (see GlmArgs::done)
+  unsigned long long done_seq;
 };
 
 // Rounding identical to numpy's `xbeta + delta*xk` (glm.py:517): product rounded, then sum.
@@ -71,6 +73,13 @@ __global__ void __launch_bounds__(256) diff_eval_kernel(DiffArgs a, DeltaPack dp
     if (lane == 0) a.out[m] = -s;
   }
   if (threadIdx.x == 0) *a.counter = 0u;
+  if (a.done) {
+    __syncthreads();  // every warp's result store, then one system-scope fence + release store
+    if (threadIdx.x == 0) {
+      asm volatile("fence.sc.sys;" ::: "memory");
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.done), "l"(a.done_seq) : "memory");
+    }
+  }
 }
 
 __global__ void __launch_bounds__(256) commit_kernel(double* __restrict__ xbeta, const double* __restrict__ xk,

@@ -438,6 +438,10 @@ class GlmWorkspace:
         _lib.check(_lib.load().pm_ws_create(self._dev.handle, _lib.dptr(beta0), ctypes.byref(h)),
                    "pm_ws_create")
         self._ws = h
+        # hot call through a prototype that takes raw addresses (no per-call POINTER objects)
+        vp = ctypes.c_void_p
+        self._diff_c = ctypes.CFUNCTYPE(ctypes.c_int, vp, ctypes.c_int32, vp, ctypes.c_int32, vp)(
+            ("pm_ws_diff_eval", _lib.load()))
         counters.add_launches(2)
 
     @property
@@ -504,12 +508,14 @@ def diff_loglike_multi(ws: GlmWorkspace, data: DesignMatrix, k: int, deltas,
     d = np.ascontiguousarray(deltas, dtype=np.float64).reshape(-1)
     if d.size < 1 or d.size > _lib.MAX_DELTAS:
         raise ValueError(f"between 1 and {_lib.MAX_DELTAS} deltas per pass")
-    if not np.isfinite(d).all():
-        raise ValueError("delta_beta_k must be finite")
     if data.n_rows != ws.n_rows or data.n_cols != ws.n_cols:
         raise ValueError("workspace/data shape mismatch")
     out = np.empty(d.size)
-    _lib.call("pm_ws_diff_eval", ws._ws, int(k), _lib.dptr(d), int(d.size), _lib.dptr(out))
+    # (the C entry rejects non-finite deltas with the reference's ValueError, glm.py:507-510)
+    rc = ws._diff_c(ws._ws, int(k), d.__array_interface__["data"][0], int(d.size),
+                    out.__array_interface__["data"][0])
+    if rc:
+        _lib.check(rc, "pm_ws_diff_eval")
     # glm.py:520-522: 8N flops, one PLF region and one merge per worker per evaluated delta
     counters.account(flops=ws.n_rows * _DIFF_FLOPS * d.size, parallel_regions=d.size,
                      merge_events=plan.workers * d.size, kernel_launches=1)
